@@ -1,0 +1,39 @@
+# Build everything in-tree (the .so files travel to the GPU box with gpurun).
+#   make            -> datagen + oracle + libsivf
+#   make datagen    -> datagen/libsivfgen.so        (seeded input generator, host)
+#   make oracle     -> oracle/libsivf_oracle.so     (CPU oracle: test infrastructure)
+#   make sivf       -> paper_2601_11808_b200/lib/libsivf.so (the product: sm_100a CUDA + C ABI)
+
+NVCC      ?= /usr/local/cuda/bin/nvcc
+CXX       ?= g++
+CC        ?= gcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+PKG       := paper_2601_11808_b200
+CSRC      := $(PKG)/csrc
+NVFLAGS   := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
+             -Iinclude -Idatagen --expt-relaxed-constexpr -Xptxas -v
+HOSTFP    := -O2 -ffp-contract=off -fno-fast-math -fPIC
+
+SIVF_SRCS := $(wildcard $(CSRC)/*.cu)
+SIVF_HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/sivf.h
+
+all: datagen oracle sivf
+
+datagen: datagen/libsivfgen.so
+oracle: oracle/libsivf_oracle.so
+sivf: $(PKG)/lib/libsivf.so
+
+datagen/libsivfgen.so: datagen/datagen_host.c datagen/sivf_datagen.h
+	$(CC) $(HOSTFP) -std=c11 -shared -o $@ datagen/datagen_host.c -lpthread -lm
+
+oracle/libsivf_oracle.so: oracle/sivf_oracle.cpp oracle/sivf_oracle.h
+	$(CXX) $(HOSTFP) -std=c++17 -shared -o $@ oracle/sivf_oracle.cpp
+
+$(PKG)/lib/libsivf.so: $(SIVF_SRCS) $(SIVF_HDRS)
+	@mkdir -p $(PKG)/lib build
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SIVF_SRCS) 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
+
+clean:
+	rm -f datagen/libsivfgen.so oracle/libsivf_oracle.so $(PKG)/lib/libsivf.so
+
+.PHONY: all datagen oracle sivf clean
