@@ -1,0 +1,368 @@
+// k_insert.cu — batched insert: claim -> assign -> reserve -> append.
+//
+// Paper: Alg. 1 Insert and Alg. 2.  The paper runs
+// one thread per vector with CAS slot reservation and CAS head publication.
+// Here a batch is stream-ordered, so reservation is done for the whole batch
+// at once (no CAS retries, no leaked slabs — readings C10, C11):
+//   k_claim        id range / shard / live-duplicate checks; atomicMin claim
+//                  on the id resolves in-batch duplicates (lowest position wins)
+//   (k_coarse.cu)  exact nearest centroid (reading C2)
+//   k_chunk_rank   stable within-list rank of each item, per 1024-item chunk
+//   k_chunk_prefix per list: exclusive prefix of chunk counts -> batch rank
+//   k_reserve      one CTA scans lists in ascending order: tail-slab free
+//                  slots, slabs needed, slabs granted from the free stack
+//                  (Eq. 2's atomicSub(P_top) done once per batch)
+//   k_dir_update   warp per list: append the granted slabs to the list
+//                  directory, initialise their metadata
+//   k_append       warp per item: payload, id, ATT entry, then the validity
+//                  bit is published with a release fence
+#include "sivf_host.h"
+
+namespace sivf {
+
+namespace {
+
+__global__ void k_claim(DevState st, const int64_t* __restrict__ ids, int64_t n, int32_t* __restrict__ status,
+                        int64_t* __restrict__ lid_out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t id = ids[i];
+  int s = SIVF_ST_OK;
+  int64_t lid = -1;
+  if (id < 0 || id >= st.cap) {
+    s = SIVF_ST_ID_OUT_OF_RANGE;
+  } else if (id % st.G != st.rank) {
+    s = SIVF_ST_WRONG_SHARD;
+  } else {
+    lid = id / st.G;
+    if (st.att[lid] != kAttInvalid) s = SIVF_ST_DUPLICATE;
+    else atomicMin(&st.claim[lid], (int32_t)i);
+  }
+  status[i] = s;
+  lid_out[i] = (s == SIVF_ST_OK) ? lid : -1;
+}
+
+// Stable rank of each OK row within its list, for one chunk of 1024 rows.
+// Sort (list << 11 | pos) keys in shared memory (bitonic), then rank = pos in
+// the sorted run.  Chunk counts go to hist[chunk][list].
+__global__ void __launch_bounds__(1024) k_chunk_rank(const unsigned long long* __restrict__ best, int64_t n,
+                                                     int32_t* __restrict__ status, const int64_t* __restrict__ lid,
+                                                     const int32_t* __restrict__ claim, int check_claim,
+                                                     int32_t* __restrict__ list_out, int32_t* __restrict__ rank_out,
+                                                     int32_t* __restrict__ hist, int nlist) {
+  __shared__ uint32_t keys[1024];
+  __shared__ int32_t wmax[32];
+  const int t = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * 1024;
+  const int64_t i = base + t;
+  uint32_t key = 0xffffffffu;
+  if (i < n) {
+    int s = status[i];
+    if (s == SIVF_ST_OK && check_claim && claim[lid[i]] != (int32_t)i) {
+      s = SIVF_ST_DUPLICATE;  // a lower batch position claimed this id (reading C12)
+      status[i] = s;
+    }
+    int l = -1;
+    if (s == SIVF_ST_OK) {
+      l = (int)(best[i] & 0xffffffffull);
+      key = ((uint32_t)l << 11) | (uint32_t)t;
+    }
+    list_out[i] = l;
+  }
+  keys[t] = key;
+  __syncthreads();
+  for (int size = 2; size <= 1024; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      int p = t ^ stride;
+      if (p > t) {
+        uint32_t a = keys[t], b = keys[p];
+        bool up = (t & size) == 0;
+        if ((a > b) == up) {
+          keys[t] = b;
+          keys[p] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const uint32_t k = keys[t];
+  const bool valid = k != 0xffffffffu;
+  const uint32_t l = k >> 11;
+  const bool head = valid && (t == 0 || (keys[t - 1] >> 11) != l);
+  // inclusive max-scan of (head ? t : 0) -> start of my run
+  int v = head ? t : 0;
+  const int lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int o = __shfl_up_sync(kFull, v, off);
+    if (lane >= off) v = max(v, o);
+  }
+  if (lane == 31) wmax[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int x = wmax[lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int o = __shfl_up_sync(kFull, x, off);
+      if (lane >= off) x = max(x, o);
+    }
+    wmax[lane] = x;
+  }
+  __syncthreads();
+  if (w > 0) v = max(v, wmax[w - 1]);
+  if (valid) {
+    const int start = v;
+    const int pos = (int)(k & 2047u);
+    rank_out[base + pos] = t - start;
+    const bool tail = (t == 1023) || (keys[t + 1] >> 11) != l || keys[t + 1] == 0xffffffffu;
+    if (tail) hist[(int64_t)blockIdx.x * nlist + l] = t - start + 1;
+  }
+}
+
+__global__ void k_chunk_prefix(int32_t* __restrict__ hist, int64_t nchunks, int nlist, int32_t* __restrict__ cnt) {
+  int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nlist) return;
+  int run = 0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    int h = hist[c * nlist + l];
+    hist[c * nlist + l] = run;
+    run += h;
+  }
+  cnt[l] = run;
+}
+
+// Single CTA: lists in ascending order share the free stack (reading C33 /
+// SURVEY a4 policy).  Slabs for list l: free_stack[newbase_l, newbase_l+granted_l).
+__global__ void __launch_bounds__(1024) k_reserve(DevState st, const int32_t* __restrict__ cnt,
+                                                  int32_t* __restrict__ tail_free, int32_t* __restrict__ tail_slab,
+                                                  int32_t* __restrict__ granted, int32_t* __restrict__ newbase,
+                                                  int32_t* __restrict__ short_flag) {
+  __shared__ int32_t wsum[32];
+  __shared__ int64_t carry_s;
+  __shared__ int32_t F;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) {
+    carry_s = 0;
+    F = st.ictr[I_FREE_TOP];
+  }
+  __syncthreads();
+  for (int l0 = 0; l0 < st.nlist; l0 += 1024) {
+    const int l = l0 + t;
+    int need = 0, tf = 0, ts = -1, c = 0;
+    if (l < st.nlist) {
+      c = cnt[l];
+      int len = st.dir_len[l];
+      if (len > 0) {
+        ts = st.dir_arena[st.dir_off[l] + len - 1];
+        tf = kSlot - (int)st.cursor[ts];
+      }
+      int rest = c > tf ? c - tf : 0;
+      need = (rest + kSlot - 1) / kSlot;
+    }
+    // block exclusive scan of need
+    int v = need;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int o = __shfl_up_sync(kFull, v, off);
+      if (lane >= off) v += o;
+    }
+    if (lane == 31) wsum[w] = v;
+    __syncthreads();
+    if (w == 0) {
+      int x = wsum[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        int o = __shfl_up_sync(kFull, x, off);
+        if (lane >= off) x += o;
+      }
+      wsum[lane] = x;
+    }
+    __syncthreads();
+    int64_t excl = carry_s + (w > 0 ? wsum[w - 1] : 0) + v - need;
+    if (l < st.nlist) {
+      int64_t avail = (int64_t)F - excl;
+      int g = (int)(avail <= 0 ? 0 : (avail < need ? avail : need));
+      tail_free[l] = tf;
+      tail_slab[l] = ts;
+      granted[l] = g;
+      newbase[l] = (int32_t)(avail - g > 0 ? avail - g : 0);
+      short_flag[l] = (g < need) ? 1 : 0;
+    }
+    __syncthreads();
+    if (t == 0) carry_s += wsum[31];
+    __syncthreads();
+  }
+  if (t == 0) {
+    int64_t total = carry_s;
+    st.ictr[I_FREE_TOP] = (int32_t)(total >= F ? 0 : F - total);
+  }
+}
+
+__global__ void k_dir_update(DevState st, const int32_t* __restrict__ cnt, const int32_t* __restrict__ tail_free,
+                             const int32_t* __restrict__ tail_slab, const int32_t* __restrict__ granted,
+                             const int32_t* __restrict__ newbase) {
+  const int lane = threadIdx.x & 31;
+  const int l = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (l >= st.nlist) return;
+  const int c = cnt[l];
+  if (c == 0) return;
+  const int tf = tail_free[l], g = granted[l];
+  const int served = min(c, tf + kSlot * g);
+  const int used_tail = min(served, tf);
+  if (lane == 0 && used_tail > 0) st.cursor[tail_slab[l]] += (uint32_t)used_tail;
+  if (g == 0) return;
+  int len = st.dir_len[l], cap = st.dir_cap[l];
+  int64_t off = st.dir_off[l];
+  if (len + g > cap) {
+    int ncap = max(max(2 * cap, len + g), 8);
+    int64_t noff = 0;
+    if (lane == 0) noff = atomicAdd(&st.ictr[I_DIR_BUMP], ncap);
+    noff = __shfl_sync(kFull, noff, 0);
+    if (noff + ncap > st.dir_arena_cap) {
+      if (lane == 0) atomicAdd(&st.ctr[C_DEVERR], 1ull);
+      return;
+    }
+    for (int j = lane; j < len; j += 32) st.dir_arena[noff + j] = st.dir_arena[off + j];
+    off = noff;
+    cap = ncap;
+    if (lane == 0) {
+      st.dir_off[l] = off;
+      st.dir_cap[l] = cap;
+    }
+  }
+  const int rem = served - used_tail;
+  for (int j = lane; j < g; j += 32) {
+    int s = st.free_stack[newbase[l] + j];
+    st.dir_arena[off + len + j] = s;
+    st.bitmap[s] = 0u;  // P:312 validity_bitmap <- 0
+    st.slab_list[s] = l;
+    int fill = rem - kSlot * j;
+    st.cursor[s] = (uint32_t)(fill > kSlot ? kSlot : fill);
+  }
+  if (lane == 0) st.dir_len[l] = len + g;
+}
+
+// Warp per item: slot from (tail_free, granted, batch rank), then writes.
+__global__ void __launch_bounds__(256) k_append(DevState st, const int64_t* __restrict__ ids,
+                                                const float* __restrict__ X, int64_t n,
+                                                int32_t* __restrict__ status, const int64_t* __restrict__ lid,
+                                                const int32_t* __restrict__ list, const int32_t* __restrict__ rank,
+                                                const int32_t* __restrict__ hist, const int32_t* __restrict__ tail_free,
+                                                const int32_t* __restrict__ tail_slab,
+                                                const int32_t* __restrict__ granted,
+                                                const int32_t* __restrict__ newbase, int32_t* __restrict__ d_status,
+                                                int32_t* __restrict__ d_list) {
+  __shared__ int ok_cnt, ex_cnt;
+  if (threadIdx.x == 0) ok_cnt = ex_cnt = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i < n) {
+    int s_ = status[i];
+    int l = -1;
+    if (s_ == SIVF_ST_OK) {
+      l = list[i];
+      const int r = hist[(i >> 10) * st.nlist + l] + rank[i];
+      const int tf = tail_free[l], g = granted[l];
+      const int64_t u = lid[i];
+      if (r >= tf + kSlot * g) {
+        s_ = SIVF_ST_POOL_EXHAUSTED;  // C9: per-item status, index unchanged
+        if (lane == 0) {
+          st.claim[u] = kClaimEmpty;
+          atomicAdd(&ex_cnt, 1);
+        }
+        l = -1;
+      } else {
+        int slab, o;
+        if (r < tf) {
+          slab = tail_slab[l];
+          o = kSlot - tf + r;
+        } else {
+          slab = st.free_stack[newbase[l] + ((r - tf) >> 5)];
+          o = (r - tf) & 31;
+        }
+        // payload: [Dp/4][32][4] — 16-B chunk c4 of slot o
+        float4* dst = reinterpret_cast<float4*>(st.payload + (size_t)slab * kSlot * st.Dp);
+        const float* xr = X + i * st.D;
+        const int nc4 = st.Dp >> 2;
+        if ((st.D & 3) == 0) {
+          const float4* src = reinterpret_cast<const float4*>(xr);
+          for (int c4 = lane; c4 < nc4; c4 += 32) dst[c4 * kSlot + o] = src[c4];
+        } else {
+          for (int c4 = lane; c4 < nc4; c4 += 32) {
+            float v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = (4 * c4 + e < st.D) ? xr[4 * c4 + e] : 0.f;
+            dst[c4 * kSlot + o] = make_float4(v[0], v[1], v[2], v[3]);
+          }
+        }
+        if (lane == 0) {
+          st.slab_ids[(size_t)slab * kSlot + o] = (uint32_t)ids[i];
+          st.att[u] = ((uint64_t)(uint32_t)slab << 32) | (uint32_t)o;  // Eq. att_encoding
+          st.claim[u] = kClaimEmpty;
+        }
+        __threadfence();  // payload, id and ATT visible before the publish
+        __syncwarp();
+        if (lane == 0) {
+          atomicOr(&st.bitmap[slab], 1u << o);  // P:300 publish
+          atomicAdd(&ok_cnt, 1);
+        }
+      }
+    }
+    if (lane == 0) {
+      if (d_status) d_status[i] = s_;
+      if (d_list) d_list[i] = l;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (ok_cnt) {
+      atomicAdd(&st.ctr[C_INSERTED], (unsigned long long)ok_cnt);
+      atomicAdd(&st.ctr[C_LIVE], (unsigned long long)ok_cnt);
+    }
+    if (ex_cnt) atomicAdd(&st.ctr[C_EXHAUSTED], (unsigned long long)ex_cnt);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_stable_ranks(Index& ix, int64_t n, int check_claim, cudaStream_t s) {
+  Scratch& sc = ix.sc;
+  const int nlist = ix.st.nlist;
+  const int64_t nchunks = ceil_div(n, 1024);
+  cudaMemsetAsync(sc.chunk_hist, 0, sizeof(int32_t) * nchunks * nlist, s);
+  k_chunk_rank<<<nchunks, 1024, 0, s>>>(sc.row_best, n, sc.row_status, sc.row_lid, ix.st.claim, check_claim,
+                                         sc.row_list, sc.row_rank, sc.chunk_hist, nlist);
+  k_chunk_prefix<<<ceil_div(nlist, 256), 256, 0, s>>>(sc.chunk_hist, nchunks, nlist, sc.list_cnt);
+  ix.launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_insert(Index& ix, const int64_t* d_ids, const float* d_x, int64_t n, int32_t* d_status,
+                          int32_t* d_list, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  Scratch& sc = ix.sc;
+  DevState& st = ix.st;
+  {
+  PhaseTimer pt(ix, SIVF_PH_APPEND, s);
+  k_claim<<<ceil_div(n, 256), 256, 0, s>>>(st, d_ids, n, sc.row_status, sc.row_lid);
+  ix.launches += 1;
+  }
+  cudaError_t e = launch_assign_exact(ix, d_x, n, s);
+  if (e != cudaSuccess) return e;
+  PhaseTimer pt(ix, SIVF_PH_APPEND, s);
+  e = launch_stable_ranks(ix, n, 1, s);
+  if (e != cudaSuccess) return e;
+  k_reserve<<<1, 1024, 0, s>>>(st, sc.list_cnt, sc.list_tail_free, sc.list_tail_slab, sc.list_granted,
+                               sc.list_newbase, sc.list_short);
+  k_dir_update<<<ceil_div((int64_t)st.nlist * 32, 256), 256, 0, s>>>(st, sc.list_cnt, sc.list_tail_free,
+                                                                     sc.list_tail_slab, sc.list_granted,
+                                                                     sc.list_newbase);
+  k_append<<<ceil_div(n * 32, 256), 256, 0, s>>>(st, d_ids, d_x, n, sc.row_status, sc.row_lid, sc.row_list,
+                                                 sc.row_rank, sc.chunk_hist, sc.list_tail_free, sc.list_tail_slab,
+                                                 sc.list_granted, sc.list_newbase, d_status, d_list);
+  ix.launches += 3;
+  return cudaGetLastError();
+}
+
+}  // namespace sivf

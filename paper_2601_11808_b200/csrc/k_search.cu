@@ -1,0 +1,419 @@
+// k_search.cu — batched search: coarse probe -> inverse map -> slab scan -> merge.
+//
+// Paper: Alg. 3 scans, per query, the slab chains of its nprobe
+// lists with one warp (lane j = slot j), gated by the validity bitmap
+// (Eq. slot_valid), computing Eq. l2, keeping a
+// per-lane top-k and merging.
+//
+// B200 design: the work is inverted to list-major.  A work
+// item is (list l, tile of <= QT queries that probe l).  A persistent CTA
+// stages each live slab of l (skipping bitmap == 0 slabs, Eq. slot_valid at
+// slab granularity) into shared memory with cp.async.bulk + mbarrier (one
+// producer warp, NS-deep ring) and every compute warp reuses it for its 4
+// queries: HBM bytes per list are read once per tile instead of once per
+// query.  The dim-interleaved slab layout [D/4][32][4] makes any 128-dim
+// chunk one contiguous block and lane=slot float4 reads conflict-free.
+// Lane (lq, ls) of a compute warp owns query lq and slots ls, ls+8, ls+16,
+// ls+24; distances use the difference form t = q - x, acc = fma(t, t, acc)
+// in ascending dimension order (|err| <= (D+2) u relative; exact on
+// integer-valued data).  Invalid slots (bit clear) become padding keys.
+// Per-(query, probe) partial top-k keys go to scratch; k_merge reduces the
+// nprobe partials of each query to the final (distance, id) top-k.
+#include "sivf_host.h"
+
+namespace sivf {
+
+namespace {
+
+constexpr int kNS = 4;     // stage ring depth
+constexpr int kCH = 128;   // dims per stage (16 KB of payload per stage)
+
+struct StageMeta {
+  int32_t slab;    // -1 = end of work item
+  uint32_t bitmap;
+  int32_t chunk;
+  int32_t last;    // 1 if this is the slab's last dim-chunk
+};
+
+struct ScanArgs {
+  DevState st;
+  const float* Q;
+  int nprobe, k;
+  const int32_t* inv_off;
+  const int32_t* inv_pairs;
+  const int32_t* tile_off;
+  const int32_t* work_list;
+  unsigned long long* partial;
+};
+
+__host__ __device__ inline size_t scan_smem_bytes(int NW, int Dp, int k) {
+  const int QT = kQPW * NW;
+  size_t b = 0;
+  b += (size_t)kNS * (kCH * kSlot * 4 + kSlot * 4);  // stage payload + ids
+  b += (size_t)QT * (Dp + 4) * 4;                   // query tile
+  b += (size_t)QT * k * 8;                          // top-k per query
+  b += (size_t)NW * k * 8;                          // merge tmp per warp
+  b += (size_t)NW * kQPW * kSlot * 8;               // candidate transposition
+  b += (size_t)kNS * sizeof(StageMeta) + 2 * kNS * 8 + 64;
+  return b;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
+  constexpr int QT = kQPW * NW;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const DevState& st = a.st;
+  const int Dp = st.Dp, Dq = Dp + 4, k = a.k;
+  float* stage_x = reinterpret_cast<float*>(smem);                        // [NS][CH*32]
+  uint32_t* stage_id = reinterpret_cast<uint32_t*>(stage_x + kNS * kCH * kSlot);  // [NS][32]
+  float* qs = reinterpret_cast<float*>(stage_id + kNS * kSlot);           // [QT][Dq]
+  unsigned long long* top = reinterpret_cast<unsigned long long*>(qs + (size_t)QT * Dq);  // [QT][k]
+  unsigned long long* tmp = top + (size_t)QT * k;                          // [NW][k]
+  unsigned long long* cand = tmp + (size_t)NW * k;                         // [NW][4][32]
+  StageMeta* meta = reinterpret_cast<StageMeta*>(cand + NW * kQPW * kSlot);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + kNS);
+  uint64_t* empty = full + kNS;
+  int* ctrl = reinterpret_cast<int*>(empty + kNS);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = (Dp + kCH - 1) / kCH;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kNS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int ntiles = st.ictr[I_NTILES];
+  uint32_t it = 0;  // stage sequence number (same sequence in producer and consumers)
+
+  for (;;) {
+    if (threadIdx.x == 0) ctrl[0] = atomicAdd(&st.ictr[I_WORK], 1);
+    __syncthreads();
+    const int w_item = ctrl[0];
+    if (w_item >= ntiles) break;
+    const int l = a.work_list[w_item];
+    const int p0 = a.inv_off[l] + (w_item - a.tile_off[l]) * QT;
+    const int nqt = min(QT, a.inv_off[l + 1] - p0);
+    // stage the query tile (zero padded) and reset the top-k lists
+    for (int e = threadIdx.x; e < QT * (Dp >> 2); e += blockDim.x) {
+      const int r = e / (Dp >> 2), c4 = e % (Dp >> 2);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nqt) {
+        const int q = a.inv_pairs[p0 + r] / a.nprobe;
+        const float* qr = a.Q + (int64_t)q * st.D;
+        float t[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[j] = (4 * c4 + j < st.D) ? qr[4 * c4 + j] : 0.f;
+        v = make_float4(t[0], t[1], t[2], t[3]);
+      }
+      *reinterpret_cast<float4*>(&qs[r * Dq + 4 * c4]) = v;
+    }
+    for (int e = threadIdx.x; e < QT * k; e += blockDim.x) top[e] = kPadKey;
+    __syncthreads();
+
+    if (warp == NW) {
+      // ---------------- producer: one elected lane issues bulk copies
+      if (lane == 0) {
+        const int len = st.dir_len[l];
+        const int32_t* dir = st.dir_arena + st.dir_off[l];
+        for (int j = 0; j < len; ++j) {
+          const int s = dir[j];
+          const uint32_t bm = st.bitmap[s];
+          if (bm == 0u) continue;  // nothing valid in this slab
+          const float* src = st.payload + (size_t)s * kSlot * Dp;
+          for (int c = 0; c < nch; ++c, ++it) {
+            const int stg = it % kNS;
+            mbar_wait(&empty[stg], ((it / kNS) & 1u) ^ 1u);
+            const int cw = min(kCH, Dp - c * kCH);
+            const bool last = c == nch - 1;
+            meta[stg] = StageMeta{s, bm, c, last ? 1 : 0};
+            mbar_arrive_expect_tx(&full[stg], cw * kSlot * 4 + (last ? kSlot * 4 : 0));
+            bulk_g2s(stage_x + stg * kCH * kSlot, src + (size_t)c * kCH * kSlot, cw * kSlot * 4, &full[stg]);
+            if (last) bulk_g2s(stage_id + stg * kSlot, st.slab_ids + (size_t)s * kSlot, kSlot * 4, &full[stg]);
+          }
+        }
+        const int stg = it % kNS;
+        mbar_wait(&empty[stg], ((it / kNS) & 1u) ^ 1u);
+        meta[stg].slab = -1;
+        mbar_arrive(&full[stg]);
+        ++it;
+      }
+    } else {
+      // ---------------- compute warps
+      const int lq = lane >> 3, ls = lane & 7;
+      const int qrow = warp * kQPW + lq;
+      const bool warp_active = warp * kQPW < nqt;
+      const float* qp = qs + qrow * Dq;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      unsigned long long* mycand = cand + warp * kQPW * kSlot;
+      for (;; ++it) {
+        const int stg = it % kNS;
+        mbar_wait(&full[stg], (it / kNS) & 1u);
+        const StageMeta m = meta[stg];
+        if (m.slab < 0) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stg]);
+          ++it;
+          break;
+        }
+        if (warp_active) {
+          const float* xs = stage_x + stg * kCH * kSlot;
+          const int cw = min(kCH, Dp - m.chunk * kCH);
+          const float* qc = qp + m.chunk * kCH;
+#pragma unroll 4
+          for (int i4 = 0; i4 < (cw >> 2); ++i4) {
+            const float4 qv = *reinterpret_cast<const float4*>(qc + 4 * i4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 xv = *reinterpret_cast<const float4*>(xs + (i4 * kSlot + ls + 8 * j) * 4);
+              float t;
+              t = qv.x - xv.x; acc[j] = fmaf(t, t, acc[j]);
+              t = qv.y - xv.y; acc[j] = fmaf(t, t, acc[j]);
+              t = qv.z - xv.z; acc[j] = fmaf(t, t, acc[j]);
+              t = qv.w - xv.w; acc[j] = fmaf(t, t, acc[j]);
+            }
+          }
+          if (m.last) {
+            const uint32_t* ids = stage_id + stg * kSlot;
+            const bool qvalid = qrow < nqt;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int slot = ls + 8 * j;
+              const bool valid = qvalid && ((m.bitmap >> slot) & 1u);  // Eq. slot_valid
+              mycand[lq * kSlot + slot] = valid ? make_key(acc[j], ids[slot]) : kPadKey;
+              acc[j] = 0.f;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stg]);  // stage buffer free
+        if (warp_active && m.last) {
+#pragma unroll 1
+          for (int qq = 0; qq < kQPW; ++qq) {
+            if (warp * kQPW + qq >= nqt) break;
+            warp_topk_insert(top + (size_t)(warp * kQPW + qq) * k, tmp + (size_t)warp * k, k,
+                             mycand[qq * kSlot + lane]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // write the partial top-k of every (query, probe) pair of the tile
+    for (int e = threadIdx.x; e < nqt * k; e += blockDim.x) {
+      const int r = e / k, j = e % k;
+      const int pair = a.inv_pairs[p0 + r];
+      a.partial[(size_t)pair * k + j] = top[r * k + j];
+    }
+  }
+}
+
+// ---- inverse probe map (list -> pairs) ----
+__global__ void k_inv_count(const int32_t* __restrict__ probes, int64_t npairs, int32_t* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < npairs) atomicAdd(&cnt[probes[i]], 1);
+}
+
+__global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ cnt, int nlist, int QT,
+                                                   int32_t* __restrict__ off, int32_t* __restrict__ cursor,
+                                                   int32_t* __restrict__ tile_off, int32_t* __restrict__ ictr) {
+  __shared__ int32_t ws[2][32];
+  __shared__ int32_t carry[2];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) carry[0] = carry[1] = 0;
+  __syncthreads();
+  for (int l0 = 0; l0 < nlist; l0 += 1024) {
+    const int l = l0 + t;
+    const int c = l < nlist ? cnt[l] : 0;
+    const int tl = (c + QT - 1) / QT;
+    int v0 = c, v1 = tl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int a0 = __shfl_up_sync(kFull, v0, o), a1 = __shfl_up_sync(kFull, v1, o);
+      if (lane >= o) {
+        v0 += a0;
+        v1 += a1;
+      }
+    }
+    if (lane == 31) {
+      ws[0][w] = v0;
+      ws[1][w] = v1;
+    }
+    __syncthreads();
+    if (w == 0) {
+      int x0 = ws[0][lane], x1 = ws[1][lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int a0 = __shfl_up_sync(kFull, x0, o), a1 = __shfl_up_sync(kFull, x1, o);
+        if (lane >= o) {
+          x0 += a0;
+          x1 += a1;
+        }
+      }
+      ws[0][lane] = x0;
+      ws[1][lane] = x1;
+    }
+    __syncthreads();
+    if (l < nlist) {
+      const int e0 = carry[0] + (w ? ws[0][w - 1] : 0) + v0 - c;
+      const int e1 = carry[1] + (w ? ws[1][w - 1] : 0) + v1 - tl;
+      off[l] = e0;
+      cursor[l] = e0;
+      tile_off[l] = e1;
+    }
+    __syncthreads();
+    if (t == 0) {
+      carry[0] += ws[0][31];
+      carry[1] += ws[1][31];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    off[nlist] = carry[0];
+    tile_off[nlist] = carry[1];
+    ictr[I_NTILES] = carry[1];
+    ictr[I_WORK] = 0;
+  }
+}
+
+__global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs, int32_t* __restrict__ cursor,
+                              int32_t* __restrict__ pairs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < npairs) pairs[atomicAdd(&cursor[probes[i]], 1)] = (int32_t)i;
+}
+
+__global__ void k_work_fill(const int32_t* __restrict__ tile_off, int nlist, int32_t* __restrict__ work) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nlist) return;
+  for (int t = tile_off[l]; t < tile_off[l + 1]; ++t) work[t] = l;
+}
+
+// Warp per query: k smallest of its nprobe partial lists (P:355 merge; C4, C5).
+__global__ void k_merge(const unsigned long long* __restrict__ partial, int64_t nq, int nprobe, int k,
+                        float* __restrict__ dist, int64_t* __restrict__ ids) {
+  extern __shared__ __align__(16) unsigned long long sm_merge[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+  if (q >= nq) return;
+  unsigned long long* top = sm_merge + (size_t)w * 2 * k;
+  unsigned long long* tmp = top + k;
+  warp_topk_init(top, k);
+  const unsigned long long* src = partial + (size_t)q * nprobe * k;
+  const int total = nprobe * k;
+  for (int i0 = 0; i0 < total; i0 += 32) {
+    const int i = i0 + lane;
+    warp_topk_insert(top, tmp, k, i < total ? src[i] : kPadKey);
+  }
+  for (int j = lane; j < k; j += 32) {
+    const uint64_t key = top[j];
+    const bool pad = key == kPadKey;
+    dist[q * k + j] = pad ? __int_as_float(0x7f800000) : key_dist(key);
+    ids[q * k + j] = pad ? -1 : (int64_t)key_id(key);
+  }
+}
+
+__global__ void k_merge_shards(const float* __restrict__ dg, const int64_t* __restrict__ ig, int G, int64_t nq, int k,
+                               float* __restrict__ dist, int64_t* __restrict__ ids) {
+  extern __shared__ __align__(16) unsigned long long sm_mg[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+  if (q >= nq) return;
+  unsigned long long* top = sm_mg + (size_t)w * 2 * k;
+  unsigned long long* tmp = top + k;
+  warp_topk_init(top, k);
+  const int total = G * k;
+  for (int i0 = 0; i0 < total; i0 += 32) {
+    const int i = i0 + lane;
+    uint64_t key = kPadKey;
+    if (i < total) {
+      const int g = i / k, j = i % k;
+      const size_t o = ((size_t)g * nq + q) * k + j;
+      const int64_t id = ig[o];
+      if (id >= 0) key = make_key(dg[o], (uint32_t)id);
+    }
+    warp_topk_insert(top, tmp, k, key);
+  }
+  for (int j = lane; j < k; j += 32) {
+    const uint64_t key = top[j];
+    const bool pad = key == kPadKey;
+    dist[q * k + j] = pad ? __int_as_float(0x7f800000) : key_dist(key);
+    ids[q * k + j] = pad ? -1 : (int64_t)key_id(key);
+  }
+}
+
+int pick_nw(const Index& ix, int k) {
+  for (int nw : {8, 4, 2})
+    if (scan_smem_bytes(nw, ix.st.Dp, k) <= ix.smem_optin) return nw;
+  return 0;
+}
+
+}  // namespace
+
+size_t scan_smem_for(const Index& ix, int k, int* nw_out) {
+  int nw = pick_nw(ix, k);
+  if (nw_out) *nw_out = nw;
+  return nw ? scan_smem_bytes(nw, ix.st.Dp, k) : 0;
+}
+
+cudaError_t setup_search_kernels(Index& ix) {
+  cudaError_t e = cudaSuccess;
+  for (int nw : {8, 4, 2}) {
+    size_t need = scan_smem_bytes(nw, ix.st.Dp, ix.cfg.max_k);
+    size_t want = need < ix.smem_optin ? need : ix.smem_optin;
+    if (nw == 8) e = cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    if (nw == 4) e = cudaFuncSetAttribute(k_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    if (nw == 2) e = cudaFuncSetAttribute(k_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
+                          int64_t* d_ids, int32_t* d_probes, cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  Scratch& sc = ix.sc;
+  const int nlist = ix.st.nlist;
+  int nw = 0;
+  const size_t smem = scan_smem_for(ix, k, &nw);
+  if (!nw) return cudaErrorInvalidConfiguration;
+  const int QT = kQPW * nw;
+  cudaError_t e = launch_probe_exact(ix, d_q, nq, nprobe, s);
+  if (e != cudaSuccess) return e;
+  const int64_t npairs = nq * nprobe;
+  if (d_probes) cudaMemcpyAsync(d_probes, sc.probes, sizeof(int32_t) * npairs, cudaMemcpyDeviceToDevice, s);
+  {
+  PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
+  cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * nlist, s);
+  k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, sc.inv_cnt);
+  k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nlist, QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr);
+  k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, sc.inv_cursor, sc.inv_pairs);
+  k_work_fill<<<ceil_div(nlist, 256), 256, 0, s>>>(sc.tile_off, nlist, sc.work_list);
+  }
+  ScanArgs a{ix.st, d_q, nprobe, k, sc.inv_off, sc.inv_pairs, sc.tile_off, sc.work_list, sc.partial};
+  const int grid = ix.num_sms;  // persistent: one CTA per SM
+  {
+  PhaseTimer pt(ix, SIVF_PH_SCAN, s);
+  if (nw == 8) k_scan<8><<<grid, 32 * 9, smem, s>>>(a);
+  else if (nw == 4) k_scan<4><<<grid, 32 * 5, smem, s>>>(a);
+  else k_scan<2><<<grid, 32 * 3, smem, s>>>(a);
+  }
+  PhaseTimer pt(ix, SIVF_PH_MERGE, s);
+  const int wpb = 4;
+  k_merge<<<ceil_div(nq, wpb), 32 * wpb, sizeof(unsigned long long) * 2 * k * wpb, s>>>(sc.partial, nq, nprobe, k,
+                                                                                        d_dist, d_ids);
+  ix.launches += 6;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int32_t G, int64_t nq, int32_t k,
+                              float* d_dist, int64_t* d_ids, cudaStream_t s, int64_t* launches) {
+  if (nq <= 0) return cudaSuccess;
+  const int wpb = 4;
+  k_merge_shards<<<ceil_div(nq, wpb), 32 * wpb, sizeof(unsigned long long) * 2 * k * wpb, s>>>(d_dist_g, d_ids_g, G,
+                                                                                              nq, k, d_dist, d_ids);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace sivf

@@ -1,0 +1,424 @@
+// sivf_api.cu — the C ABI (include/sivf.h): argument validation, arena
+// carving, and stream-ordered sequencing of the kernels.
+#include <cstring>
+#include <new>
+
+#include "sivf_host.h"
+
+namespace sivf {
+size_t scan_smem_for(const Index& ix, int k, int* nw_out);
+cudaError_t setup_search_kernels(Index& ix);
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+struct Layout {
+  size_t total = 0;
+  size_t payload, slab_ids, bitmap, cursor, slab_list, free_stack, slab_mark, att, claim, dir_off, dir_len, dir_cap,
+      dir_arena, centroids, ctr, ictr, tmp64;
+  size_t row_list, row_rank, row_status, row_lid, row_best, chunk_hist, list_cnt, list_tail_free, list_tail_slab,
+      list_granted, list_newbase, list_short;
+  size_t coarse, probes, inv_cnt, inv_off, inv_cursor, inv_pairs, tile_off, work_list, partial;
+  size_t train_perm, train_members, train_off;
+  int64_t Dp, cap_local, dir_arena_cap, max_rows, max_chunks, coarse_rows, max_work;
+};
+
+size_t take(Layout& L, size_t bytes) {
+  size_t off = L.total;
+  L.total += (bytes + kAlign - 1) / kAlign * kAlign;
+  return off;
+}
+
+bool valid_config(const sivf_config* c) {
+  if (!c) return false;
+  if (c->dim < 1 || c->nlist < 1 || c->nlist > 65536) return false;
+  if (c->id_capacity < 0 || c->id_capacity > 0xFFFFFFFEll) return false;
+  if (c->num_slabs < 1 || c->num_slabs > 0x7FFFFFFFll) return false;
+  if (c->max_batch < 0 || c->max_queries < 0 || c->max_train < 0) return false;
+  if (c->max_k < 1 || c->max_k > 128) return false;
+  if (c->max_nprobe < 1 || c->max_nprobe > c->nlist || c->max_nprobe > 1024) return false;
+  if (c->shard_count < 1 || c->shard_rank < 0 || c->shard_rank >= c->shard_count) return false;
+  if (c->max_train > 0 && c->max_train < c->nlist) return false;
+  if ((int64_t)c->max_queries * c->max_nprobe > 0x7FFFFFFFll) return false;
+  return true;
+}
+
+Layout make_layout(const sivf_config* c) {
+  Layout L;
+  const int64_t D = c->dim, nl = c->nlist, S = c->num_slabs;
+  L.Dp = (D + 3) / 4 * 4;
+  const int64_t cap = c->id_capacity, G = c->shard_count, r = c->shard_rank;
+  L.cap_local = cap > r ? (cap - r + G - 1) / G : 0;
+  L.dir_arena_cap = 4 * S + 16 * nl + 1024;
+  L.max_rows = c->max_batch > c->max_train ? c->max_batch : c->max_train;
+  if (L.max_rows < 1) L.max_rows = 1;
+  L.max_chunks = (L.max_rows + 1023) / 1024;
+  int64_t cr = ((int64_t)1 << 26) / nl;
+  if (cr < 64) cr = 64;
+  L.coarse_rows = c->max_queries < cr ? c->max_queries : cr;
+  if (L.coarse_rows < 1) L.coarse_rows = 1;
+  const int64_t npairs = (int64_t)c->max_queries * c->max_nprobe;
+  L.max_work = (npairs + 7) / 8 + nl + 1;
+
+  L.payload = take(L, (size_t)S * kSlot * L.Dp * 4);
+  L.slab_ids = take(L, (size_t)S * kSlot * 4);
+  L.bitmap = take(L, (size_t)S * 4);
+  L.cursor = take(L, (size_t)S * 4);
+  L.slab_list = take(L, (size_t)S * 4);
+  L.free_stack = take(L, (size_t)S * 4);
+  L.slab_mark = take(L, (size_t)S * 4);
+  L.att = take(L, (size_t)L.cap_local * 8);
+  L.claim = take(L, (size_t)L.cap_local * 4);
+  L.dir_off = take(L, (size_t)nl * 8);
+  L.dir_len = take(L, (size_t)nl * 4);
+  L.dir_cap = take(L, (size_t)nl * 4);
+  L.dir_arena = take(L, (size_t)L.dir_arena_cap * 4);
+  L.centroids = take(L, (size_t)nl * L.Dp * 4);
+  L.ctr = take(L, C_NCTR * 8);
+  L.ictr = take(L, I_NICTR * 4);
+  L.tmp64 = take(L, 16 * 8);
+  L.row_list = take(L, (size_t)L.max_rows * 4);
+  L.row_rank = take(L, (size_t)L.max_rows * 4);
+  L.row_status = take(L, (size_t)L.max_rows * 4);
+  L.row_lid = take(L, (size_t)L.max_rows * 8);
+  L.row_best = take(L, (size_t)L.max_rows * 8);
+  L.chunk_hist = take(L, (size_t)L.max_chunks * nl * 4);
+  L.list_cnt = take(L, (size_t)nl * 4);
+  L.list_tail_free = take(L, (size_t)nl * 4);
+  L.list_tail_slab = take(L, (size_t)nl * 4);
+  L.list_granted = take(L, (size_t)nl * 4);
+  L.list_newbase = take(L, (size_t)nl * 4);
+  L.list_short = take(L, (size_t)nl * 4);
+  L.coarse = take(L, (size_t)L.coarse_rows * nl * 4);
+  L.probes = take(L, (size_t)npairs * 4 + 4);
+  L.inv_cnt = take(L, (size_t)nl * 4);
+  L.inv_off = take(L, (size_t)(nl + 1) * 4);
+  L.inv_cursor = take(L, (size_t)nl * 4);
+  L.inv_pairs = take(L, (size_t)npairs * 4 + 4);
+  L.tile_off = take(L, (size_t)(nl + 1) * 4);
+  L.work_list = take(L, (size_t)L.max_work * 4);
+  L.partial = take(L, (size_t)npairs * c->max_k * 8 + 8);
+  L.train_perm = take(L, (size_t)(c->max_train > 0 ? c->max_train : 1) * 4);
+  L.train_members = take(L, (size_t)(c->max_train > 0 ? c->max_train : 1) * 4);
+  L.train_off = take(L, (size_t)(nl + 1) * 4);
+  return L;
+}
+
+__global__ void k_init(DevState st) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < st.num_slabs) {
+    st.free_stack[i] = (int32_t)i;  // free list [0..num_slabs), P_top = pool size
+    st.slab_list[i] = -1;
+    st.bitmap[i] = 0u;
+    st.cursor[i] = 0u;
+  }
+  if (i < st.nlist) {
+    st.dir_off[i] = 0;
+    st.dir_len[i] = 0;  // P:194 list heads "initialized to an invalid value"
+    st.dir_cap[i] = 0;
+  }
+  if (i < C_NCTR) st.ctr[i] = 0ull;
+  if (i < I_NICTR) st.ictr[i] = 0;
+  if (i == 0) st.ictr[I_FREE_TOP] = (int32_t)st.num_slabs;
+}
+
+template <typename T>
+T* at(void* base, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(base) + off);
+}
+
+sivf_rc cuda_rc(cudaError_t e) { return e == cudaSuccess ? SIVF_OK : SIVF_E_CUDA; }
+
+}  // namespace
+}  // namespace sivf
+
+using namespace sivf;
+
+extern "C" {
+
+const char* sivf_rc_string(sivf_rc rc) {
+  switch (rc) {
+    case SIVF_OK: return "ok";
+    case SIVF_E_INVALID_ARG: return "invalid argument";
+    case SIVF_E_CUDA: return "CUDA error";
+    case SIVF_E_ARENA_TOO_SMALL: return "arena too small or misaligned";
+    case SIVF_E_NOT_TRAINED: return "index has no centroids";
+    case SIVF_E_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown";
+}
+
+sivf_rc sivf_arena_bytes(const sivf_config* cfg, size_t* bytes) {
+  if (!valid_config(cfg) || !bytes) return SIVF_E_INVALID_ARG;
+  *bytes = make_layout(cfg).total;
+  return SIVF_OK;
+}
+
+sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, sivf_stream_t stream,
+                    sivf_index* out) {
+  if (!valid_config(cfg) || !out) return SIVF_E_INVALID_ARG;
+  const Layout L = make_layout(cfg);
+  if (!d_arena || arena_bytes < L.total || (reinterpret_cast<uintptr_t>(d_arena) % kAlign) != 0)
+    return SIVF_E_ARENA_TOO_SMALL;
+  Index* ix = new (std::nothrow) Index();
+  if (!ix) return SIVF_E_INVALID_ARG;
+  ix->cfg = *cfg;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (optin > 0) ix->smem_optin = (size_t)optin;
+  DevState& st = ix->st;
+  st.D = cfg->dim;
+  st.Dp = (int32_t)L.Dp;
+  st.nlist = cfg->nlist;
+  st.G = cfg->shard_count;
+  st.rank = cfg->shard_rank;
+  st.cap = cfg->id_capacity;
+  st.cap_local = L.cap_local;
+  st.num_slabs = cfg->num_slabs;
+  st.payload = at<float>(d_arena, L.payload);
+  st.slab_ids = at<uint32_t>(d_arena, L.slab_ids);
+  st.bitmap = at<uint32_t>(d_arena, L.bitmap);
+  st.cursor = at<uint32_t>(d_arena, L.cursor);
+  st.slab_list = at<int32_t>(d_arena, L.slab_list);
+  st.free_stack = at<int32_t>(d_arena, L.free_stack);
+  st.att = at<uint64_t>(d_arena, L.att);
+  st.claim = at<int32_t>(d_arena, L.claim);
+  st.dir_off = at<int64_t>(d_arena, L.dir_off);
+  st.dir_len = at<int32_t>(d_arena, L.dir_len);
+  st.dir_cap = at<int32_t>(d_arena, L.dir_cap);
+  st.dir_arena = at<int32_t>(d_arena, L.dir_arena);
+  st.dir_arena_cap = L.dir_arena_cap;
+  st.centroids = at<float>(d_arena, L.centroids);
+  st.ctr = at<unsigned long long>(d_arena, L.ctr);
+  st.ictr = at<int32_t>(d_arena, L.ictr);
+  Scratch& sc = ix->sc;
+  sc.max_rows = L.max_rows;
+  sc.row_list = at<int32_t>(d_arena, L.row_list);
+  sc.row_rank = at<int32_t>(d_arena, L.row_rank);
+  sc.row_status = at<int32_t>(d_arena, L.row_status);
+  sc.row_lid = at<int64_t>(d_arena, L.row_lid);
+  sc.row_best = at<unsigned long long>(d_arena, L.row_best);
+  sc.chunk_hist = at<int32_t>(d_arena, L.chunk_hist);
+  sc.max_chunks = L.max_chunks;
+  sc.list_cnt = at<int32_t>(d_arena, L.list_cnt);
+  sc.list_tail_free = at<int32_t>(d_arena, L.list_tail_free);
+  sc.list_tail_slab = at<int32_t>(d_arena, L.list_tail_slab);
+  sc.list_granted = at<int32_t>(d_arena, L.list_granted);
+  sc.list_newbase = at<int32_t>(d_arena, L.list_newbase);
+  sc.list_short = at<int32_t>(d_arena, L.list_short);
+  sc.coarse = at<float>(d_arena, L.coarse);
+  sc.coarse_rows = L.coarse_rows;
+  sc.probes = at<int32_t>(d_arena, L.probes);
+  sc.inv_cnt = at<int32_t>(d_arena, L.inv_cnt);
+  sc.inv_off = at<int32_t>(d_arena, L.inv_off);
+  sc.inv_cursor = at<int32_t>(d_arena, L.inv_cursor);
+  sc.inv_pairs = at<int32_t>(d_arena, L.inv_pairs);
+  sc.tile_off = at<int32_t>(d_arena, L.tile_off);
+  sc.work_list = at<int32_t>(d_arena, L.work_list);
+  sc.max_work = L.max_work;
+  sc.partial = at<unsigned long long>(d_arena, L.partial);
+  sc.train_perm = at<int32_t>(d_arena, L.train_perm);
+  sc.train_members = at<int32_t>(d_arena, L.train_members);
+  sc.train_off = at<int32_t>(d_arena, L.train_off);
+  sc.slab_mark = at<uint32_t>(d_arena, L.slab_mark);
+  sc.tmp64 = at<long long>(d_arena, L.tmp64);
+
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(st.att, 0xff, (size_t)L.cap_local * 8, s);          // ATT <- INVALID
+  cudaMemsetAsync(st.claim, 0x7f, (size_t)L.cap_local * 4, s);        // kClaimEmpty
+  cudaMemsetAsync(st.centroids, 0, (size_t)cfg->nlist * L.Dp * 4, s);
+  int64_t m = st.num_slabs > st.nlist ? st.num_slabs : st.nlist;
+  if (m < 64) m = 64;
+  k_init<<<ceil_div(m, 256), 256, 0, s>>>(st);
+  ix->launches += 1;
+  cudaError_t e = setup_search_kernels(*ix);
+  if (e == cudaSuccess) {
+    int wpb = 4;
+    size_t sel = sizeof(unsigned long long) * 2 * cfg->max_nprobe * wpb;
+    (void)sel;
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    delete ix;
+    return SIVF_E_CUDA;
+  }
+  *out = reinterpret_cast<sivf_index>(ix);
+  return SIVF_OK;
+}
+
+sivf_rc sivf_destroy(sivf_index h) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  delete reinterpret_cast<Index*>(h);
+  return SIVF_OK;
+}
+
+sivf_rc sivf_set_centroids(sivf_index h, const float* d_c, sivf_stream_t stream) {
+  if (!h || !d_c) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int D = ix->st.D, Dp = ix->st.Dp;
+  cudaError_t e = cudaMemcpy2DAsync(ix->st.centroids, (size_t)Dp * 4, d_c, (size_t)D * 4, (size_t)D * 4,
+                                    ix->st.nlist, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return SIVF_E_CUDA;
+  ix->trained = true;
+  return SIVF_OK;
+}
+
+sivf_rc sivf_get_centroids(sivf_index h, float* d_c, sivf_stream_t stream) {
+  if (!h || !d_c) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  const int D = ix->st.D, Dp = ix->st.Dp;
+  return cuda_rc(cudaMemcpy2DAsync(d_c, (size_t)D * 4, ix->st.centroids, (size_t)Dp * 4, (size_t)D * 4,
+                                   ix->st.nlist, cudaMemcpyDeviceToDevice, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sivf_rc sivf_train_centroids(sivf_index h, const float* d_x, int64_t n, int32_t niter, sivf_stream_t stream) {
+  if (!h || !d_x) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (n < ix->st.nlist || n > ix->cfg.max_train || niter < 0) return SIVF_E_INVALID_ARG;
+  cudaError_t e = launch_train(*ix, d_x, n, niter, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return SIVF_E_CUDA;
+  ix->trained = true;
+  return SIVF_OK;
+}
+
+sivf_rc sivf_insert(sivf_index h, const int64_t* d_ids, const float* d_x, int64_t n, int32_t* d_status,
+                    int32_t* d_list, sivf_stream_t stream) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (n < 0 || n > ix->cfg.max_batch) return SIVF_E_INVALID_ARG;
+  if (n > 0 && (!d_ids || !d_x)) return SIVF_E_INVALID_ARG;
+  if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  return cuda_rc(launch_insert(*ix, d_ids, d_x, n, d_status, d_list, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sivf_rc sivf_delete(sivf_index h, const int64_t* d_ids, int64_t n, int64_t* d_ndeleted, sivf_stream_t stream) {
+  if (!h || n < 0 || (n > 0 && !d_ids)) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  return cuda_rc(launch_delete(*ix, d_ids, n, d_ndeleted, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sivf_rc sivf_search(sivf_index h, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
+                    int64_t* d_ids, int32_t* d_probes, sivf_stream_t stream) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (nq < 0 || nq > ix->cfg.max_queries) return SIVF_E_INVALID_ARG;
+  if (k < 1 || k > ix->cfg.max_k) return SIVF_E_INVALID_ARG;
+  if (nprobe < 1 || nprobe > ix->cfg.max_nprobe || nprobe > ix->st.nlist) return SIVF_E_INVALID_ARG;
+  if (nq > 0 && (!d_q || !d_dist || !d_ids)) return SIVF_E_INVALID_ARG;
+  if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  return cuda_rc(launch_search(*ix, d_q, nq, k, nprobe, d_dist, d_ids, d_probes, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sivf_rc sivf_reclaim(sivf_index h, int64_t* d_nreclaimed, sivf_stream_t stream) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  return cuda_rc(launch_reclaim(*reinterpret_cast<Index*>(h), d_nreclaimed, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const float* d_new_x, int64_t n_new,
+                                 const int64_t* d_old_ids, int64_t n_old, const float* d_q, int64_t nq, int32_t k,
+                                 int32_t nprobe, float* d_dist, int64_t* d_ids, int32_t* d_status,
+                                 int64_t* d_ndeleted, sivf_stream_t stream) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (n_new < 0 || n_new > ix->cfg.max_batch || n_old < 0 || nq < 0 || nq > ix->cfg.max_queries)
+    return SIVF_E_INVALID_ARG;
+  if ((n_new > 0 && (!d_new_ids || !d_new_x)) || (n_old > 0 && !d_old_ids)) return SIVF_E_INVALID_ARG;
+  if (nq > 0) {
+    if (k < 1 || k > ix->cfg.max_k || nprobe < 1 || nprobe > ix->cfg.max_nprobe || nprobe > ix->st.nlist)
+      return SIVF_E_INVALID_ARG;
+    if (!d_q || !d_dist || !d_ids) return SIVF_E_INVALID_ARG;
+  }
+  if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_insert(*ix, d_new_ids, d_new_x, n_new, d_status, nullptr, s);
+  if (e == cudaSuccess) e = launch_delete(*ix, d_old_ids, n_old, d_ndeleted, s);
+  if (e == cudaSuccess && nq > 0) e = launch_search(*ix, d_q, nq, k, nprobe, d_dist, d_ids, nullptr, s);
+  if (e == cudaSuccess) e = launch_reclaim(*ix, nullptr, s);
+  return cuda_rc(e);
+}
+
+sivf_rc sivf_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int32_t G, int64_t nq, int32_t k,
+                        float* d_dist, int64_t* d_ids, sivf_stream_t stream) {
+  if (G < 1 || nq < 0 || k < 1 || k > 1024) return SIVF_E_INVALID_ARG;
+  if (nq > 0 && (!d_dist_g || !d_ids_g || !d_dist || !d_ids)) return SIVF_E_INVALID_ARG;
+  if ((int64_t)G * nq * k > 0x7FFFFFFFll) return SIVF_E_INVALID_ARG;
+  return cuda_rc(launch_merge_topk(d_dist_g, d_ids_g, G, nq, k, d_dist, d_ids, reinterpret_cast<cudaStream_t>(stream),
+                                   nullptr));
+}
+
+sivf_rc sivf_dump_state(sivf_index h, int32_t* d_list_of_id, int64_t* d_live_per_list, int64_t* d_violations,
+                        sivf_stream_t stream) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  return cuda_rc(launch_dump(*reinterpret_cast<Index*>(h), d_list_of_id, d_live_per_list, d_violations,
+                             reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sivf_rc sivf_dump_att(sivf_index h, uint64_t* d_att, sivf_stream_t stream) {
+  if (!h || !d_att) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  return cuda_rc(cudaMemcpyAsync(d_att, ix->st.att, (size_t)ix->st.cap_local * 8, cudaMemcpyDeviceToDevice,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sivf_rc sivf_stats(sivf_index h, sivf_stats_t* out, sivf_stream_t stream) {
+  if (!h || !out) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long c[C_NCTR];
+  int32_t ic[I_NICTR];
+  cudaError_t e = cudaMemcpyAsync(c, ix->st.ctr, sizeof(c), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ic, ix->st.ictr, sizeof(ic), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return SIVF_E_CUDA;
+  std::memset(out, 0, sizeof(*out));
+  out->live = (int64_t)c[C_LIVE];
+  out->inserted = (int64_t)c[C_INSERTED];
+  out->deleted = (int64_t)c[C_DELETED];
+  out->pool_exhausted_items = (int64_t)c[C_EXHAUSTED];
+  out->reclaimed_slabs = (int64_t)c[C_RECLAIMED];
+  out->device_errors = (int64_t)c[C_DEVERR];
+  out->slabs_free = ic[I_FREE_TOP];
+  out->slabs_in_use = ix->st.num_slabs - ic[I_FREE_TOP];
+  const double d = ix->st.D;
+  out->overhead_paper = 128.0 / (32.0 * (4.0 * d + 8.0));
+  const double live_bytes = (double)out->live * (4.0 * d + 4.0);
+  out->overhead_actual =
+      live_bytes > 0 ? (16.0 * out->slabs_in_use + 8.0 * (double)ix->st.cap_local) / live_bytes : 0.0;
+  return SIVF_OK;
+}
+
+int64_t sivf_local_capacity(sivf_index h) { return h ? reinterpret_cast<Index*>(h)->st.cap_local : -1; }
+
+int64_t sivf_launch_count(sivf_index h) { return h ? reinterpret_cast<Index*>(h)->launches : -1; }
+
+sivf_rc sivf_profile_enable(sivf_index h, int32_t on) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  reinterpret_cast<Index*>(h)->prof = on != 0;
+  return SIVF_OK;
+}
+
+sivf_rc sivf_profile_read(sivf_index h, double* ms, int64_t* count) {
+  if (!h || !ms || !count) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  for (auto& r : ix->recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return SIVF_E_CUDA;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) return SIVF_E_CUDA;
+    if (r.phase >= 0 && r.phase < SIVF_NPHASE) {
+      ms[r.phase] += t;
+      count[r.phase] += 1;
+    }
+    ix->ev_pool.push_back(r.a);
+    ix->ev_pool.push_back(r.b);
+  }
+  ix->recs.clear();
+  return SIVF_OK;
+}
+
+}  // extern "C"

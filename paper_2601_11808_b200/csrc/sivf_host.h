@@ -1,0 +1,136 @@
+// sivf_host.h — host-side handle and the internal launcher interface shared by
+// the .cu translation units of libsivf.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "sivf_internal.cuh"
+
+namespace sivf {
+
+// Scan tiling (k_scan.cu): QPW queries per compute warp.
+constexpr int kQPW = 4;
+
+struct Scratch {
+  // insert / train (max_rows = max(max_batch, max_train))
+  int64_t max_rows = 0;
+  int32_t* row_list = nullptr;      // [max_rows] assigned list
+  int32_t* row_rank = nullptr;      // [max_rows] within-chunk rank
+  int32_t* row_status = nullptr;    // [max_rows]
+  int64_t* row_lid = nullptr;       // [max_rows] local id or -1
+  unsigned long long* row_best = nullptr; // [max_rows] argmin key (dist32 bits << 32 | list)
+  int32_t* chunk_hist = nullptr;    // [max_chunks][nlist] -> exclusive prefix over chunks
+  int64_t max_chunks = 0;
+  int32_t* list_cnt = nullptr;      // [nlist]
+  int32_t* list_tail_free = nullptr;// [nlist]
+  int32_t* list_tail_slab = nullptr;// [nlist]
+  int32_t* list_granted = nullptr;  // [nlist]
+  int32_t* list_newbase = nullptr;  // [nlist] index into free_stack of the list's first new slab
+  int32_t* list_short = nullptr;    // [nlist] 1 if the list was not fully served
+  // search (max_queries x max_nprobe)
+  float* coarse = nullptr;          // [coarse_rows][nlist]
+  int64_t coarse_rows = 0;
+  int32_t* probes = nullptr;        // [max_queries][max_nprobe]
+  int32_t* inv_cnt = nullptr;       // [nlist]
+  int32_t* inv_off = nullptr;       // [nlist + 1]
+  int32_t* inv_cursor = nullptr;    // [nlist]
+  int32_t* inv_pairs = nullptr;     // [max_queries * max_nprobe] pair = q * nprobe + p
+  int32_t* tile_off = nullptr;      // [nlist + 1]
+  int32_t* work_list = nullptr;     // [max_work] list of each work item
+  int64_t max_work = 0;
+  unsigned long long* partial = nullptr; // [max_queries][max_nprobe][kp]
+  int32_t kp = 0;                   // padded k for partials
+  // train
+  float* train_sums = nullptr;      // unused (sums written straight to centroids)
+  int32_t* train_perm = nullptr;    // [max_train]
+  int32_t* train_members = nullptr; // [max_train]
+  int32_t* train_cnt = nullptr;     // [nlist]
+  int32_t* train_off = nullptr;     // [nlist + 1]
+  // validation
+  uint32_t* slab_mark = nullptr;    // [num_slabs]
+  long long* tmp64 = nullptr;       // [16] small device scalars
+};
+
+struct PhaseRec {
+  int phase;
+  cudaEvent_t a, b;
+};
+
+struct Index {
+  sivf_config cfg{};
+  DevState st{};
+  Scratch sc{};
+  bool trained = false;
+  int64_t launches = 0;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  // phase profiling (sivf_profile_*)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<PhaseRec> recs;
+  cudaEvent_t get_event() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  ~Index() {
+    for (auto& r : recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : ev_pool) cudaEventDestroy(e);
+  }
+};
+
+// RAII phase bracket: records an event pair on `s` when profiling is on.
+struct PhaseTimer {
+  Index& ix;
+  int phase;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  PhaseTimer(Index& ix_, int ph, cudaStream_t s_) : ix(ix_), phase(ph), s(s_) {
+    if (ix.prof) {
+      a = ix.get_event();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~PhaseTimer() {
+    if (ix.prof) {
+      cudaEvent_t b = ix.get_event();
+      cudaEventRecord(b, s);
+      ix.recs.push_back(PhaseRec{phase, a, b});
+    }
+  }
+};
+
+// ---- launchers (each returns cudaGetLastError after enqueueing) ----
+// k_insert.cu
+cudaError_t launch_insert(Index& ix, const int64_t* d_ids, const float* d_x, int64_t n, int32_t* d_status,
+                          int32_t* d_list, cudaStream_t s);
+// k_delete.cu
+cudaError_t launch_delete(Index& ix, const int64_t* d_ids, int64_t n, int64_t* d_ndeleted, cudaStream_t s);
+cudaError_t launch_reclaim(Index& ix, int64_t* d_nreclaimed, cudaStream_t s);
+cudaError_t launch_dump(Index& ix, int32_t* d_list_of_id, int64_t* d_live_per_list, int64_t* d_viol, cudaStream_t s);
+// k_coarse.cu
+cudaError_t launch_assign_exact(Index& ix, const float* d_x, int64_t n, cudaStream_t s);  // -> sc.row_best
+cudaError_t launch_probe_exact(Index& ix, const float* d_q, int64_t nq, int32_t nprobe, cudaStream_t s); // -> sc.probes
+// k_search.cu
+cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
+                          int64_t* d_ids, int32_t* d_probes, cudaStream_t s);
+cudaError_t launch_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int32_t G, int64_t nq, int32_t k,
+                              float* d_dist, int64_t* d_ids, cudaStream_t s, int64_t* launches);
+// k_train.cu
+cudaError_t launch_train(Index& ix, const float* d_x, int64_t n, int32_t niter, cudaStream_t s);
+// shared by insert and train: stable per-list ranks of rows with row_status==OK
+cudaError_t launch_stable_ranks(Index& ix, int64_t n, int check_claim, cudaStream_t s);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace sivf

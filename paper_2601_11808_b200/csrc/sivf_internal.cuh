@@ -1,0 +1,161 @@
+// sivf_internal.cuh — device-side layout and shared primitives of libsivf.so.
+// (Product code: no relation to oracle/.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sivf.h"
+
+namespace sivf {
+
+constexpr int kSlot = 32;                          // slab capacity C = 32 ("align with the warp size")
+constexpr uint64_t kAttInvalid = ~0ull;            // INVALID sentinel (reading C14)
+constexpr int32_t kClaimEmpty = 0x7f7f7f7f;        // byte-memsettable "no claimant"
+constexpr uint64_t kPadKey = 0x7F800000FFFFFFFFull; // (+inf, id 0xFFFFFFFF): sorts after every real key
+constexpr unsigned kFull = 0xffffffffu;
+using u64 = unsigned long long;
+
+// Counters (u64, arena) — index into DevState::ctr
+enum { C_LIVE = 0, C_INSERTED, C_DELETED, C_EXHAUSTED, C_RECLAIMED, C_DEVERR, C_NDEL_TMP, C_NCTR = 8 };
+// Counters (i32, arena) — index into DevState::ictr
+enum { I_FREE_TOP = 0, I_DIR_BUMP, I_WORK, I_NTILES, I_NICTR = 8 };
+
+// POD view of the arena, passed by value to kernels (the paper's
+// SlabManagerDevice).
+struct DevState {
+  int32_t D, Dp, nlist, G, rank;
+  int64_t cap, cap_local, num_slabs;
+  float* payload;        // [num_slabs][Dp/4][32][4]  dim-interleaved: lane = slot loads are 16-B coalesced
+  uint32_t* slab_ids;    // [num_slabs][32] user ids (u32)
+  uint32_t* bitmap;      // [num_slabs] validity bitmap b_valid (Eq. 1)
+  uint32_t* cursor;      // [num_slabs] monotone slot-reservation count (c_valid as cursor, reading C6)
+  int32_t* slab_list;    // [num_slabs] owning list, -1 if free
+  int32_t* free_stack;   // [num_slabs] free-slab stack; height = ictr[I_FREE_TOP] (Eq. 2)
+  uint64_t* att;         // [cap_local] address translation table (Eq. 3, att_encoding)
+  int32_t* claim;        // [cap_local] in-batch duplicate arbitration (atomicMin of batch position)
+  int64_t* dir_off;      // [nlist] offset of list l's slab directory in dir_arena
+  int32_t* dir_len;      // [nlist] slabs in list l (oldest first; last = tail)
+  int32_t* dir_cap;      // [nlist]
+  int32_t* dir_arena;    // [dir_arena_cap]
+  int64_t dir_arena_cap;
+  float* centroids;      // [nlist][Dp] (zero padded)
+  unsigned long long* ctr;
+  int32_t* ictr;
+};
+
+__device__ __forceinline__ u64 make_key(float d, uint32_t id) {
+  return ((u64)__float_as_uint(d) << 32) | (u64)id;
+}
+__device__ __forceinline__ float key_dist(u64 k) { return __uint_as_float((uint32_t)(k >> 32)); }
+__device__ __forceinline__ uint32_t key_id(u64 k) { return (uint32_t)(k & 0xffffffffu); }
+
+__device__ __forceinline__ u64 umin64(u64 a, u64 b) { return a < b ? a : b; }
+__device__ __forceinline__ u64 umax64(u64 a, u64 b) { return a < b ? b : a; }
+
+// Ascending bitonic sort of one u64 per lane across the warp.
+__device__ __forceinline__ u64 warp_sort32(u64 v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      u64 o = __shfl_xor_sync(kFull, v, stride);
+      bool up = (lane & size) == 0 || size == 32;
+      bool lower = (lane & stride) == 0;
+      v = (lower == up) ? umin64(v, o) : umax64(v, o);
+    }
+  }
+  return v;
+}
+
+// Number of lanes whose (sorted ascending) value is < t; t may differ per lane.
+__device__ __forceinline__ int warp_count_less(u64 sorted_v, u64 t) {
+  int pos = 0;
+#pragma unroll
+  for (int s = 32; s >= 1; s >>= 1) {
+    int idx = pos + s - 1;
+    u64 a = __shfl_sync(kFull, sorted_v, idx > 31 ? 31 : idx);
+    if (pos + s <= 32 && a < t) pos += s;
+  }
+  return pos;
+}
+
+// Warp-cooperative top-k over u64 keys (lexicographic (dist, id), unique).
+// top[0..k) in shared memory, sorted ascending, padded with kPadKey; tmp is
+// a second shared buffer of >= k entries.  Each call offers one candidate per
+// lane; after the call top holds the k smallest of (old top ∪ candidates).
+// All 32 lanes must call it (warp-uniform arguments).
+__device__ __forceinline__ void warp_topk_insert(u64* top, u64* tmp, int k, u64 cand) {
+  const int lane = threadIdx.x & 31;
+  const u64 thr = top[k - 1];
+  const unsigned m = __ballot_sync(kFull, cand < thr);
+  if (m == 0) return;
+  u64 v = warp_sort32((cand < thr) ? cand : kPadKey);
+  const int c = __popc(m);
+  if (lane < c) {  // position of survivor `lane` in the merged order = lane + #top < v
+    int lo = 0, hi = k;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (top[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    int pos = lane + lo;
+    if (pos < k) tmp[pos] = v;
+  }
+  for (int j0 = 0; j0 < k; j0 += 32) {
+    int j = j0 + lane;
+    u64 t = j < k ? top[j] : kPadKey;
+    int cnt = warp_count_less(v, t);  // all lanes participate
+    int pos = j + cnt;
+    if (j < k && pos < k) tmp[pos] = t;
+  }
+  __syncwarp();
+  for (int j = lane; j < k; j += 32) top[j] = tmp[j];
+  __syncwarp();
+}
+
+__device__ __forceinline__ void warp_topk_init(u64* top, int k) {
+  for (int j = threadIdx.x & 31; j < k; j += 32) top[j] = kPadKey;
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- mbarrier + bulk copy (sm_90+ PTX)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// 1-D bulk async copy global -> shared, completion via mbarrier tx bytes.
+// size and addresses must be multiples of 16 B.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------- host-side launch helpers
+struct Index;  // host handle (sivf_api.cu)
+
+}  // namespace sivf

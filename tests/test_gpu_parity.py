@@ -1,0 +1,312 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle,
+element by element on the same seeded inputs (SURVEY §8(c) parity matrix)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2601_11808_b200 as S
+from datagen import Generator, gist_shape, sift_shape
+from tests.checkers import check_assign, check_search, check_state
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def T(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(DEV)
+
+
+def make_pair(dim, nlist, cap, C, num_slabs=None, max_batch=4096, max_queries=1024, max_k=128, max_nprobe=None,
+              shard_rank=0, shard_count=1, max_train=0):
+    if num_slabs is None:
+        num_slabs = S.num_slabs_for(cap, nlist)
+    g = S.Index(dim, nlist, cap, num_slabs, max_batch=max_batch, max_queries=max_queries, max_k=max_k,
+                max_nprobe=max_nprobe, shard_rank=shard_rank, shard_count=shard_count, max_train=max_train)
+    o = O.Index(dim, nlist, cap, num_slabs=num_slabs, shard_rank=shard_rank, shard_count=shard_count)
+    g.set_centroids(T(C))
+    o.set_centroids(C)
+    return g, o
+
+
+def ins(g, o, ids, X):
+    st, ls = g.insert(T(ids, torch.int64), T(X))
+    ost, ols = o.insert(ids, X)
+    st, ls = st.cpu().numpy(), ls.cpu().numpy()
+    assert np.array_equal(st, ost), f"insert statuses differ: {np.nonzero(st != ost)[0][:10]}"
+    assert np.array_equal(ls, ols), f"assigned lists differ: {np.nonzero(ls != ols)[0][:10]}"
+    return st
+
+
+def dele(g, o, ids):
+    n = int(g.delete(T(ids, torch.int64)).item())
+    assert n == o.delete(ids)
+    return n
+
+
+def srch(g, o, Q, k, nprobe, exact=True):
+    gd, gi, gp = g.search(T(Q), k, nprobe, return_probes=True)
+    od, oi, op = o.search(Q, k, nprobe)
+    return check_search((gd.cpu().numpy(), gi.cpu().numpy(), gp.cpu().numpy()), (od, oi, op), exact=exact)
+
+
+# ------------------------------------------------------------------ SPEC examples
+def test_spec_worked_example():
+    g, o = make_pair(2, 1, 16, np.zeros((1, 2), np.float32))
+    ins(g, o, np.array([0, 1, 2]), np.array([[0, 0], [3, 4], [1, 1]], np.float32))
+    d, i = g.search(T(np.zeros((1, 2), np.float32)), 2, 1)
+    assert i.cpu().tolist() == [[0, 2]] and d.cpu().tolist() == [[0.0, 2.0]]
+    check_state(g, o)
+
+
+def test_spec_equivalence_suite_full_probe_is_bruteforce():
+    # N=2000, d=16, nlist=64, 100 queries, k=10, nprobe=64 -> exactly brute force
+    rng = np.random.default_rng(0)
+    X = rng.integers(0, 32, (2000, 16)).astype(np.float32)
+    C = X[rng.choice(2000, 64, replace=False)] + 0.5
+    g, o = make_pair(16, 64, 2000, C)
+    ins(g, o, np.arange(2000), X)
+    Q = rng.integers(0, 32, (100, 16)).astype(np.float32)
+    srch(g, o, Q, 10, 64)
+    bd, bi = o.bruteforce(Q, 10)
+    d, i = g.search(T(Q), 10, 64)
+    assert np.array_equal(i.cpu().numpy(), bi) and np.array_equal(d.cpu().numpy(), bd)
+    check_state(g, o)
+
+
+# ------------------------------------------------------------------ tiny config (BJ configs[0])
+def test_tiny_config_rounds():
+    gen = Generator(sift_shape(seed=0x7111))
+    X = gen.range(0, 10000)
+    C = O.kmeans(X, 64, 20, 0x7111)
+    g, o = make_pair(128, 64, 10000, C, max_batch=1000, max_queries=100)
+    Q = gen.queries(0, 100)
+    live = []
+    rng = np.random.default_rng(0x7111)
+    for r in range(10):
+        ids = np.arange(r * 1000, (r + 1) * 1000)
+        ins(g, o, ids, X[ids])
+        live.extend(ids.tolist())
+        check_state(g, o, f"round {r} insert")
+        if r >= 1:
+            dels = rng.choice(np.array(live), 1000, replace=False)
+            dele(g, o, dels)
+            live = sorted(set(live) - set(dels.tolist()))
+            check_state(g, o, f"round {r} delete")
+        srch(g, o, Q, 10, 8)
+        srch(g, o, Q, 10, 64)  # nprobe = nlist: exactly brute force
+        bd, bi = o.bruteforce(Q, 10)
+        d, i = g.search(T(Q), 10, 64)
+        assert np.array_equal(i.cpu().numpy(), bi)
+
+
+# ------------------------------------------------------------------ structure cases
+def test_first_insert_and_33rd_insert():
+    g, o = make_pair(4, 1, 100, np.zeros((1, 4), np.float32), num_slabs=8)
+    X = np.arange(400, dtype=np.float32).reshape(100, 4)
+    ins(g, o, np.array([0]), X[:1])
+    assert g.stats()["slabs_in_use"] == 1
+    ins(g, o, np.arange(1, 33), X[1:33])
+    assert g.stats()["slabs_in_use"] == 2
+    check_state(g, o)
+
+
+def test_skew_single_list_10k():
+    gen = Generator(sift_shape(seed=5))
+    X = gen.range(0, 10000)
+    C = np.stack([X.mean(0), X.mean(0) + 1e4]).astype(np.float32)
+    g, o = make_pair(128, 2, 10000, C, max_batch=10000)
+    ins(g, o, np.arange(10000), X)
+    loi, lpl, viol = g.dump_state()
+    assert lpl.cpu().tolist() == [10000, 0] and viol.item() == 0
+    assert g.stats()["slabs_in_use"] == 313  # ceil(10000/32)
+    check_state(g, o)
+    srch(g, o, gen.queries(0, 50), 10, 2)
+
+
+def test_duplicates_oor_shard_and_reinsert():
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((64, 8)).astype(np.float32)
+    C = rng.standard_normal((4, 8)).astype(np.float32)
+    g, o = make_pair(8, 4, 50, C)
+    st = ins(g, o, np.array([0, 1, 1, 49, 50, -3, 7, 0]), X[:8])
+    assert st.tolist() == [0, 0, 2, 0, 3, 3, 0, 2]
+    st = ins(g, o, np.array([1, 2]), X[8:10])  # live duplicate
+    assert st.tolist() == [2, 0]
+    assert dele(g, o, np.array([1, 1, 2, 99, -1, 30])) == 2
+    assert dele(g, o, np.array([1, 2])) == 0  # idempotent
+    st = ins(g, o, np.array([1, 2]), X[10:12])  # re-insert after delete
+    assert st.tolist() == [0, 0]
+    check_state(g, o)
+
+
+def test_delete_everything_then_search_and_k_gt_live():
+    rng = np.random.default_rng(4)
+    X = rng.integers(0, 100, (300, 16)).astype(np.float32)
+    C = X[:8] + 0.5
+    g, o = make_pair(16, 8, 300, C)
+    ins(g, o, np.arange(300), X)
+    dele(g, o, np.arange(295))
+    Q = X[:20]
+    srch(g, o, Q, 10, 8)  # k > live (5): all live, sorted, padded
+    dele(g, o, np.arange(295, 300))
+    d, i = g.search(T(Q), 10, 8)
+    assert (i.cpu().numpy() == -1).all() and torch.isinf(d).all()
+    check_state(g, o)
+
+
+def test_equidistant_centroid_tie():
+    C = np.array([[0, 2, 0, 0], [2, 0, 0, 0], [0, -2, 0, 0], [-2, 0, 0, 0], [9, 9, 9, 9]], np.float32)
+    g, o = make_pair(4, 5, 10, C)
+    st = ins(g, o, np.array([0, 1]), np.array([[0, 0, 0, 0], [1, 1, 0, 0]], np.float32))
+    _, ls = o.insert(np.array([5]), np.zeros((1, 4), np.float32))
+    loi, _, _ = g.dump_state()
+    assert loi.cpu().tolist()[0] == 0  # ties -> lowest list
+    d, i, p = g.search(T(np.zeros((1, 4), np.float32)), 2, 4, return_probes=True)
+    assert p.cpu().tolist()[0] == [0, 1, 2, 3]
+
+
+def test_near_tie_centroids_ulp():
+    # centroids 1 ulp apart around a query: exact dist32 decides (zero exemptions)
+    q = np.full(16, 100.0, np.float32)
+    c0 = q.copy()
+    c0[0] = np.nextafter(np.float32(101.0), np.float32(200.0))
+    c1 = q.copy()
+    c1[0] = np.float32(101.0)
+    c2 = q.copy()
+    c2[1] = np.float32(101.0)
+    C = np.stack([c0, c1, c2]).astype(np.float32)
+    g, o = make_pair(16, 3, 10, C)
+    ins(g, o, np.array([0, 1]), np.stack([q, q]))
+    d, i, p = g.search(T(q[None]), 2, 2, return_probes=True)
+    assert set(p.cpu().tolist()[0]) == set(O.probe(C, q, 2).tolist())
+
+
+def test_pool_exhaustion_then_reclaim():
+    C = np.array([[0, 0], [100, 100]], np.float32)
+    g, o = make_pair(2, 2, 1000, C, num_slabs=3)
+    X = np.zeros((200, 2), np.float32)
+    st = ins(g, o, np.arange(100), X[:100])
+    assert (st[96:] == S.ST_POOL_EXHAUSTED).all()
+    check_state(g, o, "exhausted")
+    dele(g, o, np.arange(32, 64))
+    assert int(g.reclaim().item()) == o.reclaim() == 1
+    check_state(g, o, "after reclaim")
+    st = ins(g, o, np.arange(100, 140), X[:40])
+    check_state(g, o, "re-insert")
+    X2 = np.array([[100, 100]] * 40 + [[0, 0]] * 40, np.float32)
+    st = ins(g, o, np.arange(200, 280), X2)  # lists served in ascending order
+    check_state(g, o, "two lists")
+
+
+def test_ragged_and_empty_batches():
+    rng = np.random.default_rng(6)
+    X = rng.integers(0, 50, (3001, 20)).astype(np.float32)  # D=20 -> padded to 20, not a multiple of 32
+    C = X[:37] + 0.25
+    g, o = make_pair(20, 37, 3001, C, max_batch=3001, max_queries=333)
+    ins(g, o, np.arange(0), X[:0])
+    ins(g, o, np.arange(3001), X)
+    assert dele(g, o, np.arange(0)) == 0
+    dele(g, o, np.arange(0, 3001, 7))
+    check_state(g, o)
+    Q = rng.integers(0, 50, (333, 20)).astype(np.float32)
+    srch(g, o, Q, 7, 5)
+    srch(g, o, Q, 33, 37)
+    srch(g, o, Q, 128, 11)
+
+
+def test_gist_shaped_float_data():
+    gen = Generator(gist_shape(seed=0x6157))
+    X = gen.range(0, 4000)
+    C = O.kmeans(X, 32, 5, 1)
+    g, o = make_pair(960, 32, 4000, C, max_queries=64)
+    ins(g, o, np.arange(4000), X)
+    dele(g, o, np.arange(0, 4000, 3))
+    check_state(g, o)
+    Q = gen.queries(0, 64)
+    ex = srch(g, o, Q, 100, 8, exact=False)
+    assert ex <= 2
+    ex = srch(g, o, Q, 10, 32, exact=False)
+    assert ex <= 2
+
+
+def test_sliding_window_scaled():
+    gen = Generator(sift_shape(seed=0x51F7))
+    W, B, steps = 20000, 1000, 25
+    C = O.kmeans(gen.train(4000), 64, 10, 9)
+    cap = W + B * (steps + 1)
+    g, o = make_pair(128, 64, cap, C, num_slabs=S.num_slabs_for(W, 64) + 2 * (B // 32 + 64), max_batch=W,
+                     max_queries=100)
+    ins(g, o, np.arange(W), gen.range(0, W))
+    for t in range(steps):
+        new = np.arange(W + t * B, W + (t + 1) * B)
+        old = np.arange(t * B, (t + 1) * B)
+        Q = gen.queries(t * 100, 100)
+        dist, ids, status, ndel = g.sliding_window_step(T(new, torch.int64), T(gen.range(new[0], B)),
+                                                        T(old, torch.int64), T(Q), 10, 16)
+        ost, _ = o.insert(new, gen.range(new[0], B))
+        assert np.array_equal(status.cpu().numpy()[:B], ost)
+        assert int(ndel.item()) == o.delete(old) == B
+        od, oi, _ = o.search(Q, 10, 16)
+        assert np.array_equal(ids.cpu().numpy(), oi) and np.array_equal(dist.cpu().numpy(), od)
+        o.reclaim()
+        check_state(g, o, f"step {t}")
+        assert g.stats()["live"] == W
+
+
+def test_merge_topk_matches_oracle():
+    rng = np.random.default_rng(8)
+    G, nq, k = 4, 50, 10
+    d = np.sort(rng.integers(0, 1000, (G, nq, k)).astype(np.float32), axis=2)
+    ids = rng.permutation(G * nq * k).reshape(G, nq, k).astype(np.int64)
+    ids[1, :, 7:] = -1
+    d[1, :, 7:] = np.inf
+    gd, gi = S.merge_topk(T(d), T(ids))
+    od, oi = O.merge_topk(d, ids, k)
+    assert np.array_equal(gi.cpu().numpy(), oi) and np.array_equal(gd.cpu().numpy(), od)
+
+
+def test_att_encoding_and_slot_uniqueness():
+    rng = np.random.default_rng(9)
+    X = rng.standard_normal((500, 8)).astype(np.float32)
+    C = rng.standard_normal((5, 8)).astype(np.float32)
+    g, o = make_pair(8, 5, 500, C)
+    ins(g, o, np.arange(500), X)
+    att = g.dump_att().cpu().numpy().view(np.uint64)
+    slab, slot = att >> np.uint64(32), att & np.uint64(0xFFFFFFFF)
+    assert (slot < 32).all() and (slab < g.cfg.num_slabs).all()  # Eq. att_encoding
+    coords = set(zip(slab.tolist(), slot.tolist()))
+    assert len(coords) == 500  # slot exclusivity
+    dele(g, o, np.arange(100))
+    att = g.dump_att().cpu().numpy().view(np.uint64)
+    assert (att[:100] == np.uint64(0xFFFFFFFFFFFFFFFF)).all()  # INVALID sentinel
+
+
+# ------------------------------------------------------------------ k-means (a1)
+def test_train_centroids_bitexact():
+    gen = Generator(sift_shape(seed=0x7111))
+    Xt = gen.train(6000)
+    for nlist, it, seed in ((1, 3, 1), (64, 10, 0x7111), (100, 4, 5)):
+        g = S.Index(128, nlist, 10, 64, max_batch=16, max_queries=16, max_train=6000, seed=seed)
+        g.train(T(Xt), niter=it)
+        Cg = g.get_centroids().cpu().numpy()
+        Co = O.kmeans(Xt, nlist, it, seed)
+        assert np.array_equal(Cg, Co), f"k-means differs (nlist={nlist}): max |d| {np.abs(Cg - Co).max()}"
+
+
+def test_train_spec_4_points_and_empty_clusters():
+    P = np.array([[0, 0], [0, 1], [10, 10], [10, 11]], np.float32)
+    g = S.Index(2, 2, 10, 8, max_batch=4, max_queries=4, max_train=4, seed=3)
+    g.train(T(P), niter=5)
+    got = sorted(map(tuple, g.get_centroids().cpu().numpy().tolist()))
+    assert got == [(0.0, 0.5), (10.0, 10.5)]
+    X = np.array([[0, 0]] * 6 + [[50, 50], [51, 50]], np.float32)
+    g = S.Index(2, 4, 10, 8, max_batch=8, max_queries=8, max_train=8, seed=3)
+    g.train(T(X), niter=4)
+    assert np.array_equal(g.get_centroids().cpu().numpy(), O.kmeans(X, 4, 4, 3))
