@@ -76,7 +76,10 @@ EXPORTS = {
     "sivf_rc_string": (ctypes.c_char_p, [_i32]),
     "sivf_profile_enable": (_i32, [_P, _i32]),
     "sivf_profile_read": (_i32, [_P, _P, _P]),
+    "sivf_set_option": (_i32, [_P, _i32, _i64]),
 }
+
+OPT_TC_SCAN = 1
 
 PHASES = ("assign", "append", "delete", "coarse", "invmap", "scan", "merge", "reclaim")
 
@@ -264,6 +267,9 @@ class Index:
 
     def launch_count(self) -> int:
         return int(lib().sivf_launch_count(self._h))
+
+    def set_option(self, option: int, value: int):
+        _check(lib().sivf_set_option(self._h, option, value), "sivf_set_option")
 
     def profile(self, on: bool = True):
         _check(lib().sivf_profile_enable(self._h, 1 if on else 0), "sivf_profile_enable")

@@ -236,6 +236,7 @@ __global__ void k_dir_update(DevState st, const int32_t* __restrict__ cnt, const
     st.dir_arena[off + len + j] = s;
     st.bitmap[s] = 0u;  // P:312 validity_bitmap <- 0
     st.slab_list[s] = l;
+    st.slab_flag[s] = 1u;  // integral until an appended vector says otherwise
     int fill = rem - kSlot * j;
     st.cursor[s] = (uint32_t)(fill > kSlot ? kSlot : fill);
   }
@@ -285,18 +286,29 @@ __global__ void __launch_bounds__(256) k_append(DevState st, const int64_t* __re
         float4* dst = reinterpret_cast<float4*>(st.payload + (size_t)slab * kSlot * st.Dp);
         const float* xr = X + i * st.D;
         const int nc4 = st.Dp >> 2;
-        if ((st.D & 3) == 0) {
-          const float4* src = reinterpret_cast<const float4*>(xr);
-          for (int c4 = lane; c4 < nc4; c4 += 32) dst[c4 * kSlot + o] = src[c4];
-        } else {
-          for (int c4 = lane; c4 < nc4; c4 += 32) {
-            float v[4];
+        float nrm = 0.f;
+        bool integral = true;
+        for (int c4 = lane; c4 < nc4; c4 += 32) {
+          float4 v;
+          if ((st.D & 3) == 0 && 4 * c4 + 3 < st.D) {
+            v = reinterpret_cast<const float4*>(xr)[c4];
+          } else {
+            float t[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) v[e] = (4 * c4 + e < st.D) ? xr[4 * c4 + e] : 0.f;
-            dst[c4 * kSlot + o] = make_float4(v[0], v[1], v[2], v[3]);
+            for (int e = 0; e < 4; ++e) t[e] = (4 * c4 + e < st.D) ? xr[4 * c4 + e] : 0.f;
+            v = make_float4(t[0], t[1], t[2], t[3]);
           }
+          dst[c4 * kSlot + o] = v;
+          nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nrm))));
+          integral = integral && v.x == rintf(v.x) && v.y == rintf(v.y) && v.z == rintf(v.z) && v.w == rintf(v.w) &&
+                     fabsf(v.x) <= 2048.f && fabsf(v.y) <= 2048.f && fabsf(v.z) <= 2048.f && fabsf(v.w) <= 2048.f;
         }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) nrm += __shfl_xor_sync(kFull, nrm, off);
+        integral = __all_sync(kFull, integral);
         if (lane == 0) {
+          st.slab_norm[(size_t)slab * kSlot + o] = nrm;
+          if (!integral) atomicAnd(&st.slab_flag[slab], 0u);
           st.slab_ids[(size_t)slab * kSlot + o] = (uint32_t)ids[i];
           st.att[u] = ((uint64_t)(uint32_t)slab << 32) | (uint32_t)o;  // Eq. att_encoding
           st.claim[u] = kClaimEmpty;

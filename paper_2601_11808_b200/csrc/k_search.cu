@@ -210,9 +210,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
 }
 
 // ---- inverse probe map (list -> pairs) ----
-__global__ void k_inv_count(const int32_t* __restrict__ probes, int64_t npairs, int32_t* __restrict__ cnt) {
+__global__ void k_inv_count(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int32_t* __restrict__ cnt,
+                            uint32_t* __restrict__ gthr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < npairs) atomicAdd(&cnt[probes[i]], 1);
+  if (i >= npairs) return;
+  atomicAdd(&cnt[probes[i]], 1);
+  if (i % nprobe == 0) gthr[i / nprobe] = 0x7F800000u;  // per-query bound = +inf
 }
 
 __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ cnt, int nlist, int QT,
@@ -356,8 +359,14 @@ size_t scan_smem_for(const Index& ix, int k, int* nw_out) {
   return nw ? scan_smem_bytes(nw, ix.st.Dp, k) : 0;
 }
 
+bool scan_tc_supported(const Index& ix, int k);
+cudaError_t setup_scan_tc(Index& ix);
+cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s);
+int scan_tc_tile();
+
 cudaError_t setup_search_kernels(Index& ix) {
-  cudaError_t e = cudaSuccess;
+  cudaError_t e = setup_scan_tc(ix);
+  if (e != cudaSuccess) return e;
   for (int nw : {8, 4, 2}) {
     size_t need = scan_smem_bytes(nw, ix.st.Dp, ix.cfg.max_k);
     size_t want = need < ix.smem_optin ? need : ix.smem_optin;
@@ -374,10 +383,11 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   if (nq <= 0) return cudaSuccess;
   Scratch& sc = ix.sc;
   const int nlist = ix.st.nlist;
+  const bool tc = ix.use_tc_scan && scan_tc_supported(ix, k);
   int nw = 0;
-  const size_t smem = scan_smem_for(ix, k, &nw);
-  if (!nw) return cudaErrorInvalidConfiguration;
-  const int QT = kQPW * nw;
+  const size_t smem = tc ? 0 : scan_smem_for(ix, k, &nw);
+  if (!tc && !nw) return cudaErrorInvalidConfiguration;
+  const int QT = tc ? scan_tc_tile() : kQPW * nw;
   cudaError_t e = launch_probe_exact(ix, d_q, nq, nprobe, s);
   if (e != cudaSuccess) return e;
   const int64_t npairs = nq * nprobe;
@@ -385,7 +395,7 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   {
   PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
   cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * nlist, s);
-  k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, sc.inv_cnt);
+  k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, sc.inv_cnt, sc.gthr);
   k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nlist, QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr);
   k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, sc.inv_cursor, sc.inv_pairs);
   k_work_fill<<<ceil_div(nlist, 256), 256, 0, s>>>(sc.tile_off, nlist, sc.work_list);
@@ -394,7 +404,8 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   const int grid = ix.num_sms;  // persistent: one CTA per SM
   {
   PhaseTimer pt(ix, SIVF_PH_SCAN, s);
-  if (nw == 8) k_scan<8><<<grid, 32 * 9, smem, s>>>(a);
+  if (tc) e = launch_scan_tc(ix, d_q, k, nprobe, s);
+  else if (nw == 8) k_scan<8><<<grid, 32 * 9, smem, s>>>(a);
   else if (nw == 4) k_scan<4><<<grid, 32 * 5, smem, s>>>(a);
   else k_scan<2><<<grid, 32 * 3, smem, s>>>(a);
   }

@@ -15,8 +15,8 @@ constexpr size_t kAlign = 256;
 
 struct Layout {
   size_t total = 0;
-  size_t payload, slab_ids, bitmap, cursor, slab_list, free_stack, slab_mark, att, claim, dir_off, dir_len, dir_cap,
-      dir_arena, centroids, ctr, ictr, tmp64;
+  size_t payload, slab_ids, slab_norm, slab_flag, bitmap, cursor, slab_list, free_stack, slab_mark, att, claim,
+      dir_off, dir_len, dir_cap, dir_arena, centroids, ctr, ictr, tmp64, gthr;
   size_t row_list, row_rank, row_status, row_lid, row_best, chunk_hist, list_cnt, list_tail_free, list_tail_slab,
       list_granted, list_newbase, list_short;
   size_t coarse, probes, inv_cnt, inv_off, inv_cursor, inv_pairs, tile_off, work_list, partial;
@@ -47,7 +47,7 @@ bool valid_config(const sivf_config* c) {
 Layout make_layout(const sivf_config* c) {
   Layout L;
   const int64_t D = c->dim, nl = c->nlist, S = c->num_slabs;
-  L.Dp = (D + 3) / 4 * 4;
+  L.Dp = (D + 7) / 8 * 8;  // tf32 MMA K-step = 8 dims
   const int64_t cap = c->id_capacity, G = c->shard_count, r = c->shard_rank;
   L.cap_local = cap > r ? (cap - r + G - 1) / G : 0;
   L.dir_arena_cap = 4 * S + 16 * nl + 1024;
@@ -63,6 +63,8 @@ Layout make_layout(const sivf_config* c) {
 
   L.payload = take(L, (size_t)S * kSlot * L.Dp * 4);
   L.slab_ids = take(L, (size_t)S * kSlot * 4);
+  L.slab_norm = take(L, (size_t)S * kSlot * 4);
+  L.slab_flag = take(L, (size_t)S * 4);
   L.bitmap = take(L, (size_t)S * 4);
   L.cursor = take(L, (size_t)S * 4);
   L.slab_list = take(L, (size_t)S * 4);
@@ -78,6 +80,7 @@ Layout make_layout(const sivf_config* c) {
   L.ctr = take(L, C_NCTR * 8);
   L.ictr = take(L, I_NICTR * 4);
   L.tmp64 = take(L, 16 * 8);
+  L.gthr = take(L, (size_t)(c->max_queries > 0 ? c->max_queries : 1) * 4);
   L.row_list = take(L, (size_t)L.max_rows * 4);
   L.row_rank = take(L, (size_t)L.max_rows * 4);
   L.row_status = take(L, (size_t)L.max_rows * 4);
@@ -181,6 +184,8 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   st.num_slabs = cfg->num_slabs;
   st.payload = at<float>(d_arena, L.payload);
   st.slab_ids = at<uint32_t>(d_arena, L.slab_ids);
+  st.slab_norm = at<float>(d_arena, L.slab_norm);
+  st.slab_flag = at<uint32_t>(d_arena, L.slab_flag);
   st.bitmap = at<uint32_t>(d_arena, L.bitmap);
   st.cursor = at<uint32_t>(d_arena, L.cursor);
   st.slab_list = at<int32_t>(d_arena, L.slab_list);
@@ -226,6 +231,7 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   sc.train_off = at<int32_t>(d_arena, L.train_off);
   sc.slab_mark = at<uint32_t>(d_arena, L.slab_mark);
   sc.tmp64 = at<long long>(d_arena, L.tmp64);
+  sc.gthr = at<uint32_t>(d_arena, L.gthr);
 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaMemsetAsync(st.att, 0xff, (size_t)L.cap_local * 8, s);          // ATT <- INVALID
@@ -396,6 +402,15 @@ sivf_rc sivf_stats(sivf_index h, sivf_stats_t* out, sivf_stream_t stream) {
 int64_t sivf_local_capacity(sivf_index h) { return h ? reinterpret_cast<Index*>(h)->st.cap_local : -1; }
 
 int64_t sivf_launch_count(sivf_index h) { return h ? reinterpret_cast<Index*>(h)->launches : -1; }
+
+sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  switch (option) {
+    case SIVF_OPT_TC_SCAN: ix->use_tc_scan = value != 0; return SIVF_OK;
+  }
+  return SIVF_E_INVALID_ARG;
+}
 
 sivf_rc sivf_profile_enable(sivf_index h, int32_t on) {
   if (!h) return SIVF_E_INVALID_ARG;

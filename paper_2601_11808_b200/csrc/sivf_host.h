@@ -50,6 +50,7 @@ struct Scratch {
   int32_t* train_off = nullptr;     // [nlist + 1]
   // validation
   uint32_t* slab_mark = nullptr;    // [num_slabs]
+  uint32_t* gthr = nullptr;         // [max_queries] per-query global k-th distance bound (fp32 bits)
   long long* tmp64 = nullptr;       // [16] small device scalars
 };
 
@@ -63,6 +64,7 @@ struct Index {
   DevState st{};
   Scratch sc{};
   bool trained = false;
+  bool use_tc_scan = true;  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
   int64_t launches = 0;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;

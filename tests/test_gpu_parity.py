@@ -24,11 +24,12 @@ def T(a, dtype=None):
 
 
 def make_pair(dim, nlist, cap, C, num_slabs=None, max_batch=4096, max_queries=1024, max_k=128, max_nprobe=None,
-              shard_rank=0, shard_count=1, max_train=0):
+              shard_rank=0, shard_count=1, max_train=0, tc=True):
     if num_slabs is None:
         num_slabs = S.num_slabs_for(cap, nlist)
     g = S.Index(dim, nlist, cap, num_slabs, max_batch=max_batch, max_queries=max_queries, max_k=max_k,
                 max_nprobe=max_nprobe, shard_rank=shard_rank, shard_count=shard_count, max_train=max_train)
+    g.set_option(S.OPT_TC_SCAN, 1 if tc else 0)
     o = O.Index(dim, nlist, cap, num_slabs=num_slabs, shard_rank=shard_rank, shard_count=shard_count)
     g.set_centroids(T(C))
     o.set_centroids(C)
@@ -81,11 +82,12 @@ def test_spec_equivalence_suite_full_probe_is_bruteforce():
 
 
 # ------------------------------------------------------------------ tiny config (BJ configs[0])
-def test_tiny_config_rounds():
+@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05-scan", "simt-scan"])
+def test_tiny_config_rounds(tc):
     gen = Generator(sift_shape(seed=0x7111))
     X = gen.range(0, 10000)
     C = O.kmeans(X, 64, 20, 0x7111)
-    g, o = make_pair(128, 64, 10000, C, max_batch=1000, max_queries=100)
+    g, o = make_pair(128, 64, 10000, C, max_batch=1000, max_queries=100, tc=tc)
     Q = gen.queries(0, 100)
     live = []
     rng = np.random.default_rng(0x7111)
@@ -205,11 +207,12 @@ def test_pool_exhaustion_then_reclaim():
     check_state(g, o, "two lists")
 
 
-def test_ragged_and_empty_batches():
+@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05-scan", "simt-scan"])
+def test_ragged_and_empty_batches(tc):
     rng = np.random.default_rng(6)
-    X = rng.integers(0, 50, (3001, 20)).astype(np.float32)  # D=20 -> padded to 20, not a multiple of 32
+    X = rng.integers(0, 50, (3001, 20)).astype(np.float32)  # D=20 -> padded to 24
     C = X[:37] + 0.25
-    g, o = make_pair(20, 37, 3001, C, max_batch=3001, max_queries=333)
+    g, o = make_pair(20, 37, 3001, C, max_batch=3001, max_queries=333, tc=tc)
     ins(g, o, np.arange(0), X[:0])
     ins(g, o, np.arange(3001), X)
     assert dele(g, o, np.arange(0)) == 0
@@ -234,6 +237,26 @@ def test_gist_shaped_float_data():
     assert ex <= 2
     ex = srch(g, o, Q, 10, 32, exact=False)
     assert ex <= 2
+
+
+@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05-scan", "simt-scan"])
+def test_float_data_d128_rerank_path(tc):
+    # GIST-like non-integer data at d=128: the tensor-core distance only filters;
+    # survivors are re-ranked exactly (certified band)
+    gen = Generator(gist_shape(seed=0x6157, dim=128))
+    X = gen.range(0, 6000)
+    C = O.kmeans(X, 48, 6, 2)
+    g, o = make_pair(128, 48, 6000, C, max_batch=6000, max_queries=300, tc=tc)
+    ins(g, o, np.arange(6000), X)
+    dele(g, o, np.arange(1, 6000, 5))
+    Q = gen.queries(0, 300)
+    for k, npb in ((10, 8), (1, 1), (32, 48), (17, 3)):
+        assert srch(g, o, Q, k, npb, exact=False) <= 3
+    # scaled inputs: large norms (||q||^2 + ||x||^2 >= 2^24 forces the re-rank even on integers)
+    Xi = np.rint(X * 1000).astype(np.float32)
+    g2, o2 = make_pair(128, 48, 6000, np.rint(C * 1000).astype(np.float32), max_batch=6000, max_queries=300, tc=tc)
+    ins(g2, o2, np.arange(6000), Xi)
+    assert srch(g2, o2, np.rint(Q * 1000).astype(np.float32), 10, 8, exact=False) <= 3
 
 
 def test_sliding_window_scaled():
