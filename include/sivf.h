@@ -194,8 +194,9 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
 
 /* Kernel-path switches (tests compare every path against the oracle).
  *   SIVF_OPT_TC_SCAN   (default 1): slab scan on tcgen05 tensor cores when
- *                      the padded dim <= 256 and k <= 32; 0 = CUDA-core scan. */
-enum { SIVF_OPT_TC_SCAN = 1 };
+ *                      the padded dim <= 256 and k <= 32; 0 = CUDA-core scan.
+ *   SIVF_OPT_TC_TWO_PHASE (default 0): scan every query's nearest list first. */
+enum { SIVF_OPT_TC_SCAN = 1, SIVF_OPT_TC_TWO_PHASE = 2 };
 sivf_rc sivf_set_option(sivf_index ix, int32_t option, int64_t value);
 sivf_rc sivf_profile_read(sivf_index ix, double* h_ms, int64_t* h_count);
 

@@ -15,7 +15,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsivf.so")
+LIB_PATH = os.environ.get("SIVF_LIB_PATH") or os.path.join(_HERE, "lib", "libsivf.so")  # override: experiments
 
 ST_OK, ST_POOL_EXHAUSTED, ST_DUPLICATE, ST_ID_OUT_OF_RANGE, ST_WRONG_SHARD = 0, 1, 2, 3, 4
 

@@ -39,10 +39,10 @@ struct ScanArgs {
   DevState st;
   const float* Q;
   int nprobe, k;
-  const int32_t* inv_off;
   const int32_t* inv_pairs;
-  const int32_t* tile_off;
-  const int32_t* work_list;
+  const int32_t* work_l;
+  const int32_t* work_p0;
+  const int32_t* work_n;
   unsigned long long* partial;
 };
 
@@ -93,9 +93,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
     __syncthreads();
     const int w_item = ctrl[0];
     if (w_item >= ntiles) break;
-    const int l = a.work_list[w_item];
-    const int p0 = a.inv_off[l] + (w_item - a.tile_off[l]) * QT;
-    const int nqt = min(QT, a.inv_off[l + 1] - p0);
+    const int l = a.work_l[w_item];
+    const int p0 = a.work_p0[w_item];
+    const int nqt = a.work_n[w_item];
     // stage the query tile (zero padded) and reset the top-k lists
     for (int e = threadIdx.x; e < QT * (Dp >> 2); e += blockDim.x) {
       const int r = e / (Dp >> 2), c4 = e % (Dp >> 2);
@@ -209,16 +209,22 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
   }
 }
 
-// ---- inverse probe map (list -> pairs) ----
-__global__ void k_inv_count(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int32_t* __restrict__ cnt,
-                            uint32_t* __restrict__ gthr) {
+// ---- inverse probe map (list -> pairs), bucketed by probe rank ----
+// Entry idx = b * nlist + l.  With nb = 2, bucket 0 holds every query's nearest
+// probed list (rank 0) and bucket 1 the rest; work items are laid out bucket-
+// major, so each query's nearest list is scanned first and the per-query bound
+// on its k-th distance is already in place for its other lists.
+__global__ void k_inv_count(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int nb, int nlist,
+                            int32_t* __restrict__ cnt, uint32_t* __restrict__ gthr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npairs) return;
-  atomicAdd(&cnt[probes[i]], 1);
-  if (i % nprobe == 0) gthr[i / nprobe] = 0x7F800000u;  // per-query bound = +inf
+  const int p = (int)(i % nprobe);
+  if (p == 0) gthr[i / nprobe] = 0x7F800000u;  // per-query bound = +inf
+  const int b = (nb == 2 && p > 0) ? 1 : 0;
+  atomicAdd(&cnt[b * nlist + probes[i]], 1);
 }
 
-__global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ cnt, int nlist, int QT,
+__global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ cnt, int nent, int QT,
                                                    int32_t* __restrict__ off, int32_t* __restrict__ cursor,
                                                    int32_t* __restrict__ tile_off, int32_t* __restrict__ ictr) {
   __shared__ int32_t ws[2][32];
@@ -226,9 +232,9 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (t == 0) carry[0] = carry[1] = 0;
   __syncthreads();
-  for (int l0 = 0; l0 < nlist; l0 += 1024) {
+  for (int l0 = 0; l0 < nent; l0 += 1024) {
     const int l = l0 + t;
-    const int c = l < nlist ? cnt[l] : 0;
+    const int c = l < nent ? cnt[l] : 0;
     const int tl = (c + QT - 1) / QT;
     int v0 = c, v1 = tl;
 #pragma unroll
@@ -258,7 +264,7 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
       ws[1][lane] = x1;
     }
     __syncthreads();
-    if (l < nlist) {
+    if (l < nent) {
       const int e0 = carry[0] + (w ? ws[0][w - 1] : 0) + v0 - c;
       const int e1 = carry[1] + (w ? ws[1][w - 1] : 0) + v1 - tl;
       off[l] = e0;
@@ -273,23 +279,34 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
     __syncthreads();
   }
   if (t == 0) {
-    off[nlist] = carry[0];
-    tile_off[nlist] = carry[1];
+    off[nent] = carry[0];
+    tile_off[nent] = carry[1];
     ictr[I_NTILES] = carry[1];
     ictr[I_WORK] = 0;
   }
 }
 
-__global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs, int32_t* __restrict__ cursor,
-                              int32_t* __restrict__ pairs) {
+__global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int nb, int nlist,
+                              int32_t* __restrict__ cursor, int32_t* __restrict__ pairs) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < npairs) pairs[atomicAdd(&cursor[probes[i]], 1)] = (int32_t)i;
+  if (i >= npairs) return;
+  const int p = (int)(i % nprobe);
+  const int b = (nb == 2 && p > 0) ? 1 : 0;
+  pairs[atomicAdd(&cursor[b * nlist + probes[i]], 1)] = (int32_t)i;
 }
 
-__global__ void k_work_fill(const int32_t* __restrict__ tile_off, int nlist, int32_t* __restrict__ work) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= nlist) return;
-  for (int t = tile_off[l]; t < tile_off[l + 1]; ++t) work[t] = l;
+// Materialise the work items: (list, first pair, number of pairs).
+__global__ void k_work_fill(const int32_t* __restrict__ tile_off, const int32_t* __restrict__ off, int nent,
+                            int nlist, int QT, int32_t* __restrict__ work_l, int32_t* __restrict__ work_p0,
+                            int32_t* __restrict__ work_n) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nent) return;
+  const int c = off[e + 1] - off[e];
+  for (int t = tile_off[e], j = 0; t < tile_off[e + 1]; ++t, ++j) {
+    work_l[t] = e % nlist;
+    work_p0[t] = off[e] + j * QT;
+    work_n[t] = min(QT, c - j * QT);
+  }
 }
 
 // Warp per query: k smallest of its nprobe partial lists (P:355 merge; C4, C5).
@@ -392,28 +409,35 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   if (e != cudaSuccess) return e;
   const int64_t npairs = nq * nprobe;
   if (d_probes) cudaMemcpyAsync(d_probes, sc.probes, sizeof(int32_t) * npairs, cudaMemcpyDeviceToDevice, s);
+  // Tensor-core path: probe-rank buckets (nearest list first), one scan launch.
+  const int nb = (tc && nprobe > 1 && ix.tc_two_phase) ? 2 : 1;
+  const int nent = nb * nlist;
   {
-  PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
-  cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * nlist, s);
-  k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, sc.inv_cnt, sc.gthr);
-  k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nlist, QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr);
-  k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, sc.inv_cursor, sc.inv_pairs);
-  k_work_fill<<<ceil_div(nlist, 256), 256, 0, s>>>(sc.tile_off, nlist, sc.work_list);
+    PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
+    cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * nent, s);
+    k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, nlist, sc.inv_cnt, sc.gthr);
+    k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr);
+    k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, nlist, sc.inv_cursor,
+                                                         sc.inv_pairs);
+    k_work_fill<<<ceil_div(nent, 256), 256, 0, s>>>(sc.tile_off, sc.inv_off, nent, nlist, QT, sc.work_l,
+                                                    sc.work_p0, sc.work_n);
+    ix.launches += 4;
   }
-  ScanArgs a{ix.st, d_q, nprobe, k, sc.inv_off, sc.inv_pairs, sc.tile_off, sc.work_list, sc.partial};
+  ScanArgs a{ix.st, d_q, nprobe, k, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial};
   const int grid = ix.num_sms;  // persistent: one CTA per SM
   {
-  PhaseTimer pt(ix, SIVF_PH_SCAN, s);
-  if (tc) e = launch_scan_tc(ix, d_q, k, nprobe, s);
-  else if (nw == 8) k_scan<8><<<grid, 32 * 9, smem, s>>>(a);
-  else if (nw == 4) k_scan<4><<<grid, 32 * 5, smem, s>>>(a);
-  else k_scan<2><<<grid, 32 * 3, smem, s>>>(a);
+    PhaseTimer pt(ix, SIVF_PH_SCAN, s);
+    if (tc) e = launch_scan_tc(ix, d_q, k, nprobe, s);
+    else if (nw == 8) k_scan<8><<<grid, 32 * 9, smem, s>>>(a);
+    else if (nw == 4) k_scan<4><<<grid, 32 * 5, smem, s>>>(a);
+    else k_scan<2><<<grid, 32 * 3, smem, s>>>(a);
+    if (!tc) ix.launches += 1;
   }
   PhaseTimer pt(ix, SIVF_PH_MERGE, s);
   const int wpb = 4;
   k_merge<<<ceil_div(nq, wpb), 32 * wpb, sizeof(unsigned long long) * 2 * k * wpb, s>>>(sc.partial, nq, nprobe, k,
                                                                                         d_dist, d_ids);
-  ix.launches += 6;
+  ix.launches += 1;
   return cudaGetLastError();
 }
 

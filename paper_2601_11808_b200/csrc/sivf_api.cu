@@ -19,7 +19,7 @@ struct Layout {
       dir_off, dir_len, dir_cap, dir_arena, centroids, ctr, ictr, tmp64, gthr;
   size_t row_list, row_rank, row_status, row_lid, row_best, chunk_hist, list_cnt, list_tail_free, list_tail_slab,
       list_granted, list_newbase, list_short;
-  size_t coarse, probes, inv_cnt, inv_off, inv_cursor, inv_pairs, tile_off, work_list, partial;
+  size_t coarse, probes, inv_cnt, inv_off, inv_cursor, inv_pairs, tile_off, work_l, work_p0, work_n, partial;
   size_t train_perm, train_members, train_off;
   int64_t Dp, cap_local, dir_arena_cap, max_rows, max_chunks, coarse_rows, max_work;
 };
@@ -59,7 +59,7 @@ Layout make_layout(const sivf_config* c) {
   L.coarse_rows = c->max_queries < cr ? c->max_queries : cr;
   if (L.coarse_rows < 1) L.coarse_rows = 1;
   const int64_t npairs = (int64_t)c->max_queries * c->max_nprobe;
-  L.max_work = (npairs + 7) / 8 + nl + 1;
+  L.max_work = (npairs + 7) / 8 + 2 * nl + 1;
 
   L.payload = take(L, (size_t)S * kSlot * L.Dp * 4);
   L.slab_ids = take(L, (size_t)S * kSlot * 4);
@@ -95,12 +95,14 @@ Layout make_layout(const sivf_config* c) {
   L.list_short = take(L, (size_t)nl * 4);
   L.coarse = take(L, (size_t)L.coarse_rows * nl * 4);
   L.probes = take(L, (size_t)npairs * 4 + 4);
-  L.inv_cnt = take(L, (size_t)nl * 4);
-  L.inv_off = take(L, (size_t)(nl + 1) * 4);
-  L.inv_cursor = take(L, (size_t)nl * 4);
+  L.inv_cnt = take(L, (size_t)2 * nl * 4);
+  L.inv_off = take(L, (size_t)(2 * nl + 1) * 4);
+  L.inv_cursor = take(L, (size_t)2 * nl * 4);
   L.inv_pairs = take(L, (size_t)npairs * 4 + 4);
-  L.tile_off = take(L, (size_t)(nl + 1) * 4);
-  L.work_list = take(L, (size_t)L.max_work * 4);
+  L.tile_off = take(L, (size_t)(2 * nl + 1) * 4);
+  L.work_l = take(L, (size_t)L.max_work * 4);
+  L.work_p0 = take(L, (size_t)L.max_work * 4);
+  L.work_n = take(L, (size_t)L.max_work * 4);
   L.partial = take(L, (size_t)npairs * c->max_k * 8 + 8);
   L.train_perm = take(L, (size_t)(c->max_train > 0 ? c->max_train : 1) * 4);
   L.train_members = take(L, (size_t)(c->max_train > 0 ? c->max_train : 1) * 4);
@@ -223,7 +225,9 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   sc.inv_cursor = at<int32_t>(d_arena, L.inv_cursor);
   sc.inv_pairs = at<int32_t>(d_arena, L.inv_pairs);
   sc.tile_off = at<int32_t>(d_arena, L.tile_off);
-  sc.work_list = at<int32_t>(d_arena, L.work_list);
+  sc.work_l = at<int32_t>(d_arena, L.work_l);
+  sc.work_p0 = at<int32_t>(d_arena, L.work_p0);
+  sc.work_n = at<int32_t>(d_arena, L.work_n);
   sc.max_work = L.max_work;
   sc.partial = at<unsigned long long>(d_arena, L.partial);
   sc.train_perm = at<int32_t>(d_arena, L.train_perm);
@@ -408,6 +412,7 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
   Index* ix = reinterpret_cast<Index*>(h);
   switch (option) {
     case SIVF_OPT_TC_SCAN: ix->use_tc_scan = value != 0; return SIVF_OK;
+    case SIVF_OPT_TC_TWO_PHASE: ix->tc_two_phase = value != 0; return SIVF_OK;
   }
   return SIVF_E_INVALID_ARG;
 }

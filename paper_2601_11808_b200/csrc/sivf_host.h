@@ -33,12 +33,14 @@ struct Scratch {
   float* coarse = nullptr;          // [coarse_rows][nlist]
   int64_t coarse_rows = 0;
   int32_t* probes = nullptr;        // [max_queries][max_nprobe]
-  int32_t* inv_cnt = nullptr;       // [nlist]
-  int32_t* inv_off = nullptr;       // [nlist + 1]
-  int32_t* inv_cursor = nullptr;    // [nlist]
+  int32_t* inv_cnt = nullptr;       // [2 nlist]   (probe-rank bucket, list)
+  int32_t* inv_off = nullptr;       // [2 nlist + 1]
+  int32_t* inv_cursor = nullptr;    // [2 nlist]
   int32_t* inv_pairs = nullptr;     // [max_queries * max_nprobe] pair = q * nprobe + p
-  int32_t* tile_off = nullptr;      // [nlist + 1]
-  int32_t* work_list = nullptr;     // [max_work] list of each work item
+  int32_t* tile_off = nullptr;      // [2 nlist + 1]
+  int32_t* work_l = nullptr;        // [max_work] list of each work item
+  int32_t* work_p0 = nullptr;       // [max_work] first pair (index into inv_pairs)
+  int32_t* work_n = nullptr;        // [max_work] number of pairs (queries) in the item
   int64_t max_work = 0;
   unsigned long long* partial = nullptr; // [max_queries][max_nprobe][kp]
   int32_t kp = 0;                   // padded k for partials
@@ -64,7 +66,8 @@ struct Index {
   DevState st{};
   Scratch sc{};
   bool trained = false;
-  bool use_tc_scan = true;  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
+  bool use_tc_scan = true;
+  bool tc_two_phase = false;  // nearest-list-first scan phase (SIVF_OPT_TC_TWO_PHASE)  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
   int64_t launches = 0;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
