@@ -35,6 +35,10 @@ sys.path.insert(0, ROOT)
 METRIC = "deletes/s, inserts/s, sliding-window step p50/p99 ms, QPS@recall10≥0.9"
 N_BASE, DIM, NLIST, BATCH, NQ, K, NPROBE = 1_000_000, 128, 1024, 10_000, 10_000, 10, 32
 N_TRAIN, N_ITER, SEED = 262_144, 20, 0x51F7
+# dram__bytes_read.sum + dram__bytes_write.sum of one k_scan_tc launch, from the committed ncu
+# --set full capture of this bench step (per launch; compare with roofline.hbm_view).
+SCAN_TRAFFIC_NCU = 561.944576e6 + 30.705920e6
+SCAN_TRAFFIC_SRC = "profiles/r01a_scan_full.txt (ncu --set full, bench.py --steps 1 --warmup 1)"
 WORKLOAD = ("SIFT1M-shaped sliding step: 1M x 128 fp32 live window, nlist=1024; per step insert 10k new + "
             "delete 10k oldest + search 10k queries (k=10, nprobe=32) + reclaim")
 
@@ -408,28 +412,49 @@ def run_sivf(args):
                 qps_at_09, recall_point = qps, npb
         log("sweep " + ", ".join(f"np{k}: r={v['recall10']:.3f} {v['qps'] / 1e6:.2f}Mqps" for k, v in sweep.items()))
 
-    # ---------------- roofline of the dominant kernel (k_scan)
+    # ---------------- roofline of the dominant kernel (the slab scan) + per-phase rooflines
     ph_ms = {p: (v[0] / v[1] if v[1] else 0.0) for p, v in prof.items()}
-    # algorithmic work of one scan launch: every (query, probed list, live slot) triple, 3 flops per dim
+    # algorithmic work of one scan launch: every (query, probed list, live slot) triple
     _, _, probes = ix.search(dev_inputs[-1][3], K, NPROBE, return_probes=True)
     _, lpl, _ = ix.dump_state()
     cand = int(lpl[probes.long()].sum().item())
-    flops = 3.0 * DIM * cand
     mp = measured_peaks()
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     clk_s = clk.summary()
     mhz = float(mp.get("sm_max_mhz", clk_s["sm_max_mhz"] or 1965.0))
-    peak_alu = fp32_alu_peak_tflops(sm_count, mhz)
+    hbm_peak = float(mp.get("hbm_gbs", 6650.0))
+    # tf32 dense peak = measured bf16 (sustained: the scan runs inside a long step) x nominal tf32/bf16 (1.1/2.25)
+    tf32_peak = float(mp.get("bf16_tflops_sustained", 1400.0)) * (1.1 / 2.25)
     scan_ms = ph_ms["scan"]
+    uniq = torch.unique(probes).long()
+    uniq_bytes = float(lpl[uniq].sum().item()) * (4 * DIM + 8)
+    flops = 2.0 * DIM * cand  # q.x on the tensor cores (the norms are per-slot / per-query precomputes)
     achieved = flops / (scan_ms / 1e3) / 1e12 if scan_ms else 0.0
-    uniq_lists = torch.unique(probes).numel()
-    uniq_bytes = float(lpl[torch.unique(probes).long()].sum().item()) * (4 * DIM + 4)
-    roofline = {"bound": "alu", "achieved": achieved, "peak": peak_alu, "unit": "TFLOP/s",
-                "frac": achieved / peak_alu if peak_alu else None, "traffic": None,
-                "kernel": "k_scan", "kernel_ms": scan_ms, "algorithmic_flops": flops,
-                "candidates_per_launch": cand, "unique_list_bytes": uniq_bytes,
-                "hbm_achieved_gbs_unique": uniq_bytes / (scan_ms / 1e3) / 1e9 if scan_ms else None,
-                "peak_note": f"FP32 SIMT {sm_count} SMs x 128 lanes x 2 flops x {mhz:.0f} MHz (derived, DESIGN.md)"}
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": achieved / tf32_peak if tf32_peak else None, "traffic": SCAN_TRAFFIC_NCU,
+                "traffic_source": SCAN_TRAFFIC_SRC,
+                "kernel": "k_scan_tc (tcgen05 kind::tf32)", "kernel_ms": scan_ms, "algorithmic_flops": flops,
+                "per_unit": "2*D flop per (query, probed live slot)", "candidates_per_launch": cand,
+                "unique_list_bytes": uniq_bytes,
+                "hbm_view": {"achieved_gbs": uniq_bytes / (scan_ms / 1e3) / 1e9 if scan_ms else None,
+                             "peak_gbs": hbm_peak,
+                             "frac": uniq_bytes / (scan_ms / 1e3) / 1e9 / hbm_peak if scan_ms else None,
+                             "per_unit": "4*D+8 B per live slot of each probed list, read once per step"},
+                "peak_note": "tf32 = MEASURED_PEAKS bf16_tflops_sustained x 1.1/2.25 (guide nominal ratio)"}
+
+    def tfrac(fl, ms):
+        return None if not ms else {"achieved_tflops": fl / (ms / 1e3) / 1e12, "frac": fl / (ms / 1e3) / 1e12 / tf32_peak}
+
+    def hfrac(b, ms):
+        return None if not ms else {"achieved_gbs": b / (ms / 1e3) / 1e9, "frac": b / (ms / 1e3) / 1e9 / hbm_peak}
+
+    rooflines = {
+        "assign (tensor, 2*nlist*D flop/vector)": tfrac(2.0 * NLIST * DIM * BATCH / G, ph_ms["assign"]),
+        "coarse (tensor, 2*nlist*D flop/query)": tfrac(2.0 * NLIST * DIM * NQ, ph_ms["coarse"]),
+        "append (hbm, 8D+24 B/vector)": hfrac((8.0 * DIM + 24) * BATCH / G, ph_ms["append"]),
+        "delete (hbm, 28 B/id)": hfrac(28.0 * BATCH / G, ph_ms["delete"]),
+        "merge (hbm, nprobe*k*8 + k*12 B/query)": hfrac((NPROBE * K * 8.0 + K * 12.0) * NQ, ph_ms["merge"]),
+    }
     share = {p: (ph_ms[p] / ms_per_step if ms_per_step else None) for p in ph_ms}
 
     # ---------------- cpu baseline (oracle, rank 0, N=1 only)
@@ -477,6 +502,7 @@ def run_sivf(args):
         "phase_share_of_step": share,
         "sweep": sweep,
         "roofline": roofline,
+        "rooflines_by_phase": rooflines,
         "cpu_baseline": cpu,
         "e2e": {"value": 1e3 / e2e_ms, "unit": "steps/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

@@ -195,8 +195,12 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
 /* Kernel-path switches (tests compare every path against the oracle).
  *   SIVF_OPT_TC_SCAN   (default 1): slab scan on tcgen05 tensor cores when
  *                      the padded dim <= 256 and k <= 32; 0 = CUDA-core scan.
- *   SIVF_OPT_TC_TWO_PHASE (default 0): scan every query's nearest list first. */
-enum { SIVF_OPT_TC_SCAN = 1, SIVF_OPT_TC_TWO_PHASE = 2 };
+ *   SIVF_OPT_TC_TWO_PHASE (default 0): scan every query's nearest list first.
+ *   SIVF_OPT_TC_COARSE (default 1): assignment and probe selection (nprobe <= 32)
+ *                      on tcgen05 tensor cores with a certified band and exact
+ *                      dist32 re-rank (bit-identical result); 0 = exact CUDA-core
+ *                      distance matrix. */
+enum { SIVF_OPT_TC_SCAN = 1, SIVF_OPT_TC_TWO_PHASE = 2, SIVF_OPT_TC_COARSE = 3 };
 sivf_rc sivf_set_option(sivf_index ix, int32_t option, int64_t value);
 sivf_rc sivf_profile_read(sivf_index ix, double* h_ms, int64_t* h_count);
 

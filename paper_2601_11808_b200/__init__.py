@@ -80,6 +80,8 @@ EXPORTS = {
 }
 
 OPT_TC_SCAN = 1
+OPT_TC_TWO_PHASE = 2
+OPT_TC_COARSE = 3
 
 PHASES = ("assign", "append", "delete", "coarse", "invmap", "scan", "merge", "reclaim")
 

@@ -118,6 +118,7 @@ __global__ void k_select_probes(const float* __restrict__ dist, int64_t nq, int6
 cudaError_t launch_assign_exact(Index& ix, const float* d_x, int64_t n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   PhaseTimer pt(ix, SIVF_PH_ASSIGN, s);
+  if (coarse_tc_supported(ix, 1)) return launch_coarse_tc(ix, d_x, n, 1, ix.sc.row_best, nullptr, s);
   cudaMemsetAsync(ix.sc.row_best, 0xff, sizeof(unsigned long long) * n, s);
   dim3 grid(ceil_div(ix.st.nlist, BN), ceil_div(n, BM));
   k_dist_exact<0><<<grid, 256, 0, s>>>(d_x, n, ix.st.D, ix.st.centroids, ix.st.Dp, ix.st.nlist, ix.sc.row_best,
@@ -130,6 +131,7 @@ cudaError_t launch_probe_exact(Index& ix, const float* d_q, int64_t nq, int32_t 
   const int nlist = ix.st.nlist;
   const int64_t rows = ix.sc.coarse_rows;
   PhaseTimer pt(ix, SIVF_PH_COARSE, s);
+  if (coarse_tc_supported(ix, nprobe)) return launch_coarse_tc(ix, d_q, nq, nprobe, nullptr, ix.sc.probes, s);
   for (int64_t q0 = 0; q0 < nq; q0 += rows) {
     int64_t m = nq - q0 < rows ? nq - q0 : rows;
     dim3 grid(ceil_div(nlist, BN), ceil_div(m, BM));

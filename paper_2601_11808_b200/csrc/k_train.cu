@@ -182,7 +182,9 @@ cudaError_t launch_train(Index& ix, const float* d_x, int64_t n, int32_t niter, 
                                                                          st.centroids);
   ix.launches += 3;
   for (int it = 0; it < niter; ++it) {
-    cudaError_t e = launch_assign_exact(ix, d_x, n, s);
+    cudaError_t e = refresh_centroid_tiles(ix, s);
+    if (e != cudaSuccess) return e;
+    e = launch_assign_exact(ix, d_x, n, s);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(sc.row_status, 0, sizeof(int32_t) * n, s);
     e = launch_stable_ranks(ix, n, 0, s);
@@ -197,7 +199,7 @@ cudaError_t launch_train(Index& ix, const float* d_x, int64_t n, int32_t niter, 
                                                                            nlist, st.D, st.Dp, st.centroids);
     ix.launches += 4;
   }
-  return cudaGetLastError();
+  return refresh_centroid_tiles(ix, s);
 }
 
 }  // namespace sivf

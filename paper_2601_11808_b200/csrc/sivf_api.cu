@@ -21,6 +21,8 @@ struct Layout {
       list_granted, list_newbase, list_short;
   size_t coarse, probes, inv_cnt, inv_off, inv_cursor, inv_pairs, tile_off, work_l, work_p0, work_n, partial;
   size_t train_perm, train_members, train_off;
+  size_t x_tiles, x_norm, c_tiles, c_norm, c_csa, c_cnb, cand, cand_ubv, cand_cnt;
+  int64_t tc_rows, cap_assign, cap_probe;
   int64_t Dp, cap_local, dir_arena_cap, max_rows, max_chunks, coarse_rows, max_work;
 };
 
@@ -107,6 +109,25 @@ Layout make_layout(const sivf_config* c) {
   L.train_perm = take(L, (size_t)(c->max_train > 0 ? c->max_train : 1) * 4);
   L.train_members = take(L, (size_t)(c->max_train > 0 ? c->max_train : 1) * 4);
   L.train_off = take(L, (size_t)(nl + 1) * 4);
+  // tensor-core coarse quantisation: rows per pass = max(batch, queries), 128-row tiles
+  int64_t tr = c->max_batch > c->max_queries ? c->max_batch : c->max_queries;
+  if (tr < 128) tr = 128;
+  L.tc_rows = (tr + 127) / 128 * 128;
+  const int64_t nct = (nl + 255) / 256;
+  L.cap_assign = nl < 32 ? nl : 32;
+  L.cap_probe = nl < 512 ? nl : 512;
+  const int64_t cap_rows = L.tc_rows * L.cap_assign > (int64_t)c->max_queries * L.cap_probe
+                               ? L.tc_rows * L.cap_assign
+                               : (int64_t)c->max_queries * L.cap_probe;
+  L.x_tiles = take(L, (size_t)L.tc_rows * L.Dp * 4);
+  L.x_norm = take(L, (size_t)L.tc_rows * 4);
+  L.c_tiles = take(L, (size_t)nct * 256 * L.Dp * 4);
+  L.c_norm = take(L, (size_t)nct * 256 * 4);
+  L.c_csa = take(L, (size_t)nct * 256 * 4);
+  L.c_cnb = take(L, (size_t)nct * 256 * 4);
+  L.cand = take(L, (size_t)cap_rows * 8);
+  L.cand_ubv = take(L, (size_t)cap_rows * 4);
+  L.cand_cnt = take(L, (size_t)L.tc_rows * 4);
   return L;
 }
 
@@ -236,6 +257,18 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   sc.slab_mark = at<uint32_t>(d_arena, L.slab_mark);
   sc.tmp64 = at<long long>(d_arena, L.tmp64);
   sc.gthr = at<uint32_t>(d_arena, L.gthr);
+  sc.tc_rows = L.tc_rows;
+  sc.x_tiles = at<float>(d_arena, L.x_tiles);
+  sc.x_norm = at<float>(d_arena, L.x_norm);
+  sc.c_tiles = at<float>(d_arena, L.c_tiles);
+  sc.c_norm = at<float>(d_arena, L.c_norm);
+  sc.c_csa = at<float>(d_arena, L.c_csa);
+  sc.c_cnb = at<float>(d_arena, L.c_cnb);
+  sc.cand = at<unsigned long long>(d_arena, L.cand);
+  sc.cand_ubv = at<float>(d_arena, L.cand_ubv);
+  sc.cand_cnt = at<int32_t>(d_arena, L.cand_cnt);
+  sc.cand_cap_assign = (int32_t)L.cap_assign;
+  sc.cand_cap_probe = (int32_t)L.cap_probe;
 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaMemsetAsync(st.att, 0xff, (size_t)L.cap_local * 8, s);          // ATT <- INVALID
@@ -246,6 +279,7 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   k_init<<<ceil_div(m, 256), 256, 0, s>>>(st);
   ix->launches += 1;
   cudaError_t e = setup_search_kernels(*ix);
+  if (e == cudaSuccess) e = setup_coarse_tc(*ix);
   if (e == cudaSuccess) {
     int wpb = 4;
     size_t sel = sizeof(unsigned long long) * 2 * cfg->max_nprobe * wpb;
@@ -273,6 +307,7 @@ sivf_rc sivf_set_centroids(sivf_index h, const float* d_c, sivf_stream_t stream)
   const int D = ix->st.D, Dp = ix->st.Dp;
   cudaError_t e = cudaMemcpy2DAsync(ix->st.centroids, (size_t)Dp * 4, d_c, (size_t)D * 4, (size_t)D * 4,
                                     ix->st.nlist, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = refresh_centroid_tiles(*ix, s);
   if (e != cudaSuccess) return SIVF_E_CUDA;
   ix->trained = true;
   return SIVF_OK;
@@ -413,6 +448,7 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
   switch (option) {
     case SIVF_OPT_TC_SCAN: ix->use_tc_scan = value != 0; return SIVF_OK;
     case SIVF_OPT_TC_TWO_PHASE: ix->tc_two_phase = value != 0; return SIVF_OK;
+    case SIVF_OPT_TC_COARSE: ix->use_tc_coarse = value != 0; return SIVF_OK;
   }
   return SIVF_E_INVALID_ARG;
 }

@@ -54,6 +54,18 @@ struct Scratch {
   uint32_t* slab_mark = nullptr;    // [num_slabs]
   uint32_t* gthr = nullptr;         // [max_queries] per-query global k-th distance bound (fp32 bits)
   long long* tmp64 = nullptr;       // [16] small device scalars
+  // tensor-core coarse quantisation (k_coarse_tc.cu)
+  int64_t tc_rows = 0;              // rows per k_coarse_gemm pass
+  float* x_tiles = nullptr;         // [tc_rows/128][Dp/4][128][4]
+  float* x_norm = nullptr;          // [tc_rows]
+  float* c_tiles = nullptr;         // [nlist/256][Dp/4][256][4]
+  float* c_norm = nullptr;          // [nlist/256 * 256] ||c||^2
+  float* c_csa = nullptr;           // [nlist/256 * 256] ka ||c||
+  float* c_cnb = nullptr;           // [nlist/256 * 256] kb ||c||^2
+  unsigned long long* cand = nullptr; // [rows][cap] candidate lower-bound keys
+  float* cand_ubv = nullptr;        // [rows][cap] candidate upper bounds
+  int32_t* cand_cnt = nullptr;      // [tc_rows]
+  int32_t cand_cap_assign = 0, cand_cap_probe = 0;
 };
 
 struct PhaseRec {
@@ -67,6 +79,7 @@ struct Index {
   Scratch sc{};
   bool trained = false;
   bool use_tc_scan = true;
+  bool use_tc_coarse = true;  // tcgen05 coarse quantisation (k_coarse_tc.cu); false = exact SIMT k_dist_exact
   bool tc_two_phase = false;  // nearest-list-first scan phase (SIVF_OPT_TC_TWO_PHASE)  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
   int64_t launches = 0;
   int num_sms = 148;
@@ -123,9 +136,17 @@ cudaError_t launch_insert(Index& ix, const int64_t* d_ids, const float* d_x, int
 cudaError_t launch_delete(Index& ix, const int64_t* d_ids, int64_t n, int64_t* d_ndeleted, cudaStream_t s);
 cudaError_t launch_reclaim(Index& ix, int64_t* d_nreclaimed, cudaStream_t s);
 cudaError_t launch_dump(Index& ix, int32_t* d_list_of_id, int64_t* d_live_per_list, int64_t* d_viol, cudaStream_t s);
-// k_coarse.cu
+// k_coarse.cu (dispatch: tensor cores when supported, else exact SIMT)
 cudaError_t launch_assign_exact(Index& ix, const float* d_x, int64_t n, cudaStream_t s);  // -> sc.row_best
 cudaError_t launch_probe_exact(Index& ix, const float* d_q, int64_t nq, int32_t nprobe, cudaStream_t s); // -> sc.probes
+// k_coarse_tc.cu
+bool coarse_tc_supported(const Index& ix, int m);
+cudaError_t setup_coarse_tc(Index& ix);
+cudaError_t refresh_centroid_tiles(Index& ix, cudaStream_t s);
+int coarse_tc_tile_rows();
+int coarse_tc_tile_cols();
+cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsigned long long* best,
+                             int32_t* probes, cudaStream_t s);
 // k_search.cu
 cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
                           int64_t* d_ids, int32_t* d_probes, cudaStream_t s);

@@ -24,12 +24,13 @@ def T(a, dtype=None):
 
 
 def make_pair(dim, nlist, cap, C, num_slabs=None, max_batch=4096, max_queries=1024, max_k=128, max_nprobe=None,
-              shard_rank=0, shard_count=1, max_train=0, tc=True):
+              shard_rank=0, shard_count=1, max_train=0, tc=True, coarse=True):
     if num_slabs is None:
         num_slabs = S.num_slabs_for(cap, nlist)
     g = S.Index(dim, nlist, cap, num_slabs, max_batch=max_batch, max_queries=max_queries, max_k=max_k,
                 max_nprobe=max_nprobe, shard_rank=shard_rank, shard_count=shard_count, max_train=max_train)
     g.set_option(S.OPT_TC_SCAN, 1 if tc else 0)
+    g.set_option(S.OPT_TC_COARSE, 1 if coarse else 0)
     o = O.Index(dim, nlist, cap, num_slabs=num_slabs, shard_rank=shard_rank, shard_count=shard_count)
     g.set_centroids(T(C))
     o.set_centroids(C)
@@ -309,6 +310,61 @@ def test_att_encoding_and_slot_uniqueness():
     dele(g, o, np.arange(100))
     att = g.dump_att().cpu().numpy().view(np.uint64)
     assert (att[:100] == np.uint64(0xFFFFFFFFFFFFFFFF)).all()  # INVALID sentinel
+
+
+# ------------------------------------------------------------------ tensor-core coarse quantisation (a3, a7)
+@pytest.mark.parametrize("coarse", [True, False], ids=["tcgen05-coarse", "simt-coarse"])
+def test_coarse_sift_shaped_nlist1024(coarse):
+    # BJ configs[1] geometry: nlist=1024, nprobe=32; assignments and probe sets bit-exact
+    gen = Generator(sift_shape(seed=0x51F7))
+    X = gen.range(0, 20000)
+    rng = np.random.default_rng(11)
+    C = (X[rng.choice(20000, 1024, replace=False)] + rng.integers(-3, 4, (1024, 128))).astype(np.float32)
+    g, o = make_pair(128, 1024, 20000, C, max_batch=10000, max_queries=1000, max_nprobe=128, coarse=coarse)
+    ins(g, o, np.arange(10000), X[:10000])  # 10k batch: assignment parity
+    ins(g, o, np.arange(10000, 20000), X[10000:])
+    Q = gen.queries(0, 1000)
+    for npb in (1, 8, 32, 33, 128):  # 33/128 exercise the CUDA-core fallback of the probe selection
+        srch(g, o, Q, 10, npb)
+    check_state(g, o)
+
+
+def test_coarse_gist_shaped_d960_float():
+    gen = Generator(gist_shape(seed=0x6157))
+    X = gen.range(0, 3000)
+    rng = np.random.default_rng(12)
+    C = X[rng.choice(3000, 300, replace=False)] * np.float32(1.001)
+    g, o = make_pair(960, 300, 3000, C, max_batch=3000, max_queries=200)
+    ins(g, o, np.arange(3000), X)
+    Q = gen.queries(0, 200)
+    for npb in (1, 7, 32):
+        gd, gi, gp = g.search(T(Q), 10, npb, return_probes=True)
+        op = np.stack([np.sort(O.probe(C, q, npb)) for q in Q])
+        assert np.array_equal(np.sort(gp.cpu().numpy(), axis=1), op)
+    check_state(g, o)
+
+
+def test_coarse_exact_ties_and_band_overflow():
+    # every centroid at exactly the same distance from the query (sign flips /
+    # permutations of one integer vector): the whole nlist is inside the band,
+    # the candidate buffer overflows, and the full exact re-rank must return the
+    # lowest list indices (reading C2/C3)
+    rng = np.random.default_rng(13)
+    v = rng.integers(1, 20, 32).astype(np.float32)
+    C = np.stack([rng.permutation(v) * rng.choice([-1.0, 1.0], 32) for _ in range(1024)]).astype(np.float32)
+    g, o = make_pair(32, 1024, 100, C, max_batch=64, max_queries=8, max_nprobe=64)
+    Z = np.zeros((8, 32), np.float32)
+    st, ls = g.insert(T(np.arange(8), torch.int64), T(Z))
+    assert (ls.cpu().numpy() == 0).all()
+    _, _, p = g.search(T(Z), 1, 32, return_probes=True)
+    assert (np.sort(p.cpu().numpy(), axis=1) == np.arange(32)).all()
+    # near-ties 1 ulp apart inside the band (integer data, exact distances)
+    q = rng.integers(0, 100, (4, 32)).astype(np.float32)
+    C2 = np.repeat(q[:1], 300, axis=0)
+    C2[:, 0] += np.arange(300, dtype=np.float32) % 3  # distances 0, 1, 4 repeating
+    g2, o2 = make_pair(32, 300, 100, C2.astype(np.float32), max_batch=64, max_queries=8, max_nprobe=64)
+    ins(g2, o2, np.arange(4), q)
+    srch(g2, o2, q, 5, 32)
 
 
 # ------------------------------------------------------------------ k-means (a1)
