@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="sivf", choices=["sivf", "reference"])
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the sliding-window (W) and GIST (G) legs")
+    ap.add_argument("--window-steps", type=int, default=1000)
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run only N steps, no extras")
     return ap.parse_args()
@@ -509,10 +511,188 @@ def run_sivf(args):
         "gpu_launches": launches,
         "clocks": clk_s,
     }
+    if G == 1 and not args.no_extra:
+        C_sift = ix.get_centroids()
+        del ix
+        torch.cuda.empty_cache()
+        line["configs"] = {}
+        line["configs"]["W_sliding_window"] = leg_window(S, dev, C_sift, args.window_steps, log)
+        torch.cuda.empty_cache()
+        line["configs"]["G_gist1m"] = leg_gist(S, dev, log)
+        torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.destroy_process_group()
+
+
+def _ev():
+    import torch
+
+    return torch.cuda.Event(enable_timing=True)
+
+
+def leg_window(S, dev, C, steps, log):
+    """BASELINE configs[3]: sliding window on SIFT1M-shaped data, window 1M, slide 10k per
+    step (insert new + delete expired + 1k queries, k=10, nprobe=32) + reclaim, one CUDA-graph
+    replay per step; p50/p99 over `steps` steps.  New vectors come from a pool of 50 steps'
+    worth of generated vectors (ids are always new; contents recycle) so the inputs stay
+    resident in HBM."""
+    import torch
+
+    from datagen import Generator, sift_shape
+
+    W, B, NQW, POOL = N_BASE, BATCH, 1000, 50
+    gen = Generator(sift_shape(seed=SEED))
+    cap = W + (steps + 40) * B
+    ix = S.Index(DIM, NLIST, cap, S.num_slabs_for(W + 2 * B, NLIST), max_batch=max(B, 65536), max_queries=NQW,
+                 max_k=K, max_nprobe=NPROBE, seed=SEED, device=dev)
+    ix.set_centroids(C)
+    Xw = torch.from_numpy(gen.range(0, W)).to(dev)
+    ids = torch.arange(W, device=dev)
+    for b0 in range(0, W, 65536):
+        ix.insert(ids[b0:b0 + 65536], Xw[b0:b0 + 65536])
+    del Xw
+    pool = torch.from_numpy(gen.range(W, POOL * B)).to(dev).view(POOL, B, DIM)
+    qpool = torch.from_numpy(gen.queries(0, POOL * NQW)).to(dev).view(POOL, NQW, DIM)
+    s_new, s_old = torch.empty(B, dtype=torch.int64, device=dev), torch.empty(B, dtype=torch.int64, device=dev)
+    s_x, s_q = torch.empty(B, DIM, device=dev), torch.empty(NQW, DIM, device=dev)
+    out = (torch.empty(NQW, K, device=dev), torch.empty(NQW, K, dtype=torch.int64, device=dev),
+           torch.empty(B, dtype=torch.int32, device=dev), torch.empty(1, dtype=torch.int64, device=dev))
+    ar = torch.arange(B, device=dev)
+
+    def stage(t):
+        torch.add(ar, W + t * B, out=s_new)
+        torch.add(ar, t * B, out=s_old)
+        s_x.copy_(pool[t % POOL])
+        s_q.copy_(qpool[t % POOL])
+
+    def step():
+        ix.sliding_window_step(s_new, s_x, s_old, s_q, K, NPROBE, out=out)
+
+    warm = 20
+    for t in range(warm):
+        stage(t)
+        step()
+    torch.cuda.synchronize()
+    l0 = ix.launch_count()
+    g = torch.cuda.CUDAGraph()
+    stage(warm)
+    with torch.cuda.graph(g):
+        step()
+    per_replay = ix.launch_count() - l0
+    g.replay()  # step `warm`
+    torch.cuda.synchronize()
+    evs = [(_ev(), _ev()) for _ in range(steps)]
+    for i in range(steps):
+        t = warm + 1 + i
+        evs[i][0].record()
+        stage(t)
+        g.replay()
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    st = ix.stats()
+    assert st["live"] == W and st["device_errors"] == 0, st
+    res = {"workload": "BASELINE configs[3]: SIFT1M-shaped window 1M, slide 10k/step (insert new + delete expired "
+                       "+ 1k queries k=10 nprobe=32) + reclaim; one CUDA-graph replay per step",
+           "steps": steps, "step_ms_p50": pct(ms, 50), "step_ms_p99": pct(ms, 99), "step_ms_mean": statistics.mean(ms),
+           "step_ms_max": max(ms), "kernels_per_step": per_replay, "live_after": st["live"],
+           "slabs_in_use_after": st["slabs_in_use"], "reclaimed_slabs": st["reclaimed_slabs"],
+           "inputs": "per-step ids computed on device, vectors/queries copied from a 50-step HBM pool into the "
+                     "graph's static buffers inside the timed region"}
+    log(f"window: p50 {res['step_ms_p50']:.3f} ms p99 {res['step_ms_p99']:.3f} ms over {steps} steps")
+    return res
+
+
+def leg_gist(S, dev, log):
+    """BASELINE configs[2]: GIST1M-shaped 1M x 960 fp32, nlist=1024: 10k-vector delete batch latency,
+    insert throughput (10k batches and bulk 64k batches), search 10k queries k=100 nprobe=32 and the
+    recall@10 sweep (first 10 of the k=100 results vs exact top-10)."""
+    import torch
+
+    from datagen import Generator, gist_shape
+
+    N, D, KG = 1_000_000, 960, 100
+    gen = Generator(gist_shape())
+    reps = 30
+    cap = N + (reps + 2) * BATCH
+    ix = S.Index(D, NLIST, cap, S.num_slabs_for(N + (reps + 2) * BATCH, NLIST), max_batch=65536, max_queries=NQ,
+                 max_k=KG, max_nprobe=64, max_train=N_TRAIN, seed=0x6157, device=dev)
+    t0 = time.time()
+    ix.train(torch.from_numpy(gen.train(N_TRAIN)).to(dev), niter=N_ITER)
+    torch.cuda.synchronize()
+    t_train = time.time() - t0
+    X = torch.from_numpy(gen.range(0, N)).to(dev)
+    ids = torch.arange(cap, device=dev)
+    e0, e1 = _ev(), _ev()
+    e0.record()
+    for b0 in range(0, N, 65536):
+        ix.insert(ids[b0:min(N, b0 + 65536)], X[b0:b0 + 65536])
+    e1.record()
+    torch.cuda.synchronize()
+    build_rate = N / (e0.elapsed_time(e1) / 1e3)
+    Q = torch.from_numpy(gen.queries(0, NQ)).to(dev)
+    # exact top-10 (fp32 GEMM, no tf32) for recall
+    torch.backends.cuda.matmul.allow_tf32 = False
+    xn = (X * X).sum(1)
+    gt = []
+    for q0 in range(0, NQ, 250):
+        q = Q[q0:q0 + 250]
+        d = (q * q).sum(1)[:, None] + xn[None, :] - 2.0 * (q @ X.T)
+        gt.append(torch.topk(d, 10, dim=1, largest=False).indices)
+    gt = torch.cat(gt).cpu().numpy()
+    sweep, qps_at_09, np_at_09 = {}, None, None
+    for npb in (4, 8, 16, 32, 64):
+        ix.search(Q, KG, npb)
+        torch.cuda.synchronize()
+        reps_ms = []
+        for _ in range(3):
+            a, b = _ev(), _ev()
+            a.record()
+            _, ii = ix.search(Q, KG, npb)
+            b.record()
+            torch.cuda.synchronize()
+            reps_ms.append(a.elapsed_time(b))
+        res = ii[:, :10].cpu().numpy()
+        rec = float(np.mean([len(set(r) & set(g)) / 10 for r, g in zip(res, gt)]))
+        qps = NQ / (statistics.median(reps_ms) / 1e3)
+        sweep[npb] = {"recall10": rec, "qps": qps, "ms": statistics.median(reps_ms)}
+        if qps_at_09 is None and rec >= 0.9:
+            qps_at_09, np_at_09 = qps, npb
+    # mutation latencies: 30 delete batches of 10k random live ids, 30 insert batches of 10k new ids
+    rng = np.random.default_rng(0x6157)
+    perm = torch.from_numpy(rng.permutation(N)[: reps * BATCH].astype(np.int64)).to(dev)
+    del_ms, ins_ms = [], []
+    for r in range(reps):
+        a, b = _ev(), _ev()
+        a.record()
+        ix.delete(perm[r * BATCH:(r + 1) * BATCH])
+        b.record()
+        c, d = _ev(), _ev()
+        c.record()
+        ix.insert(ids[N + r * BATCH:N + (r + 1) * BATCH], X[r * BATCH:(r + 1) * BATCH])
+        d.record()
+        del_ms.append((a, b))
+        ins_ms.append((c, d))
+    torch.cuda.synchronize()
+    del_ms = [a.elapsed_time(b) for a, b in del_ms]
+    ins_ms = [a.elapsed_time(b) for a, b in ins_ms]
+    st = ix.stats()
+    assert st["live"] == N and st["device_errors"] == 0, st
+    res = {"workload": "BASELINE configs[2]: GIST1M-shaped 1M x 960 fp32, nlist=1024 (GPU-trained, 262144 samples, "
+                       "20 iters)",
+           "delete_10k_ms_p50": pct(del_ms, 50), "delete_10k_ms_p99": pct(del_ms, 99),
+           "deletes_per_s": BATCH / (pct(del_ms, 50) / 1e3),
+           "insert_10k_ms_p50": pct(ins_ms, 50), "insert_10k_ms_p99": pct(ins_ms, 99),
+           "inserts_per_s_10k_batches": BATCH / (pct(ins_ms, 50) / 1e3),
+           "inserts_per_s_bulk_64k_batches": build_rate,
+           "qps_k100_nprobe32": sweep[32]["qps"], "recall10_nprobe32": sweep[32]["recall10"],
+           "qps_at_recall10_0.9": qps_at_09, "nprobe_at_recall10_0.9": np_at_09, "sweep_k100": sweep,
+           "train_s": t_train, "overhead_paper": st["overhead_paper"], "overhead_actual": st["overhead_actual"]}
+    log(f"gist: delete p50 {res['delete_10k_ms_p50']:.4f} ms, insert10k {res['insert_10k_ms_p50']:.3f} ms, "
+        f"qps@32 {sweep[32]['qps']:.0f} r={sweep[32]['recall10']:.3f}")
+    return res
 
 
 def main():
