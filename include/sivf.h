@@ -199,8 +199,19 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
  *   SIVF_OPT_TC_COARSE (default 1): assignment and probe selection (nprobe <= 32)
  *                      on tcgen05 tensor cores with a certified band and exact
  *                      dist32 re-rank (bit-identical result); 0 = exact CUDA-core
- *                      distance matrix. */
-enum { SIVF_OPT_TC_SCAN = 1, SIVF_OPT_TC_TWO_PHASE = 2, SIVF_OPT_TC_COARSE = 3 };
+ *                      distance matrix.
+ *   SIVF_OPT_SEED_SLABS (default 8): before the tensor-core scan, each query's
+ *                      bound on its k-th distance is seeded with exact distances
+ *                      to the first `value` live slabs of its nearest probed list
+ *                      (any k real candidates bound the final k-th distance from
+ *                      above); 0 = no seeding.  Changes speed only, never results.
+ *   SIVF_OPT_RANK_SPLIT (default 1): tensor-core scan work items ordered so that
+ *                      every query's nprobe/4 nearest lists are scanned before
+ *                      its other lists (when that adds no work items on
+ *                      average); the bounds on the k-th distances are then
+ *                      tight early.  Changes speed only, never results. */
+enum { SIVF_OPT_TC_SCAN = 1, SIVF_OPT_TC_TWO_PHASE = 2, SIVF_OPT_TC_COARSE = 3, SIVF_OPT_SEED_SLABS = 4,
+       SIVF_OPT_RANK_SPLIT = 5 };
 sivf_rc sivf_set_option(sivf_index ix, int32_t option, int64_t value);
 sivf_rc sivf_profile_read(sivf_index ix, double* h_ms, int64_t* h_count);
 

@@ -3,40 +3,54 @@
 // Work decomposition as in k_search.cu (a work item = list l x a tile of
 // <= 128 queries probing l).  Eq. l2 for (query tile, slabs) is a
 // dense contraction:  d(q, x) = ||q||^2 + ||x||^2 - 2 q.x.
-// q.x is computed with tcgen05.mma kind::tf32, M = 128 queries (A, resident in
-// TMEM for the whole work item), N = 128 slots = a GROUP of 4 slabs (B, in
-// shared memory), K = 8 per instruction, fp32 accumulators in TMEM.
+// q.x runs on tcgen05.mma kind::tf32 with M = 128 queries (A, resident in
+// TMEM), N = 128 slots = a GROUP of 4 slabs (B, shared memory), K = 8 per
+// instruction, fp32 accumulators in TMEM.
 //
 // Why groups of 4 slabs: one MMA re-reads the whole A tile, so an N=32 (one
-// slab) instruction costs as much as N=128 (measured: ~68 cycles each,
-// tools/mma_probe.cu); N=128 reaches the tf32 tensor floor.  The B operand must
-// be in the K-major SWIZZLE_NONE layout with a uniform 8-row-group stride, so
-// the 4 bulk-copied slabs (each [D/4][32][4], itself a valid B layout for N=32)
-// are interleaved into [D/4][4 slabs][32][4] by two "transposer" warps: a
-// shared-memory pass at full bandwidth (512-B bulk copies of the same layout
-// run at ~40% of HBM bandwidth, tools/pipe_probe.cu).
+// slab) instruction costs as much as N=128 (tools/mma_probe.cu).  The B
+// operand must be K-major SWIZZLE_NONE with a uniform 8-row-group stride, i.e.
+// [Dp/4][4 slabs][32 slots][4 floats].  The slab payload is [Dp/4][32][4]:
+// viewed as a 2-D tensor of 512-B rows (row = slab * Dp/4 + c4) a TMA
+// tile::gather4 of rows {s0,s1,s2,s3} * Dp/4 + c4 lands exactly the c4-th
+// 2-KB slice of that interleaved layout, so Dp/4 gather4 instructions per
+// group build the operand straight from HBM (tools/g4_probe.cu: layout
+// checked, 6.9 TB/s streaming random groups).  No shared-memory transpose.
 //
-// Roles (1 CTA per SM, persistent, 12 warps):
-//   warp 0      producer: counts the item's live slabs (bitmap != 0, Eq.
-//               slot_valid at slab granularity), then bulk-copies them into a
-//               4-stage ring (stage j = slab position j of a group)
-//   warp 1      MMA issuer (one lane) and TMEM owner
-//   warps 2-3   transposers: stage -> interleaved group buffer (x2), group
-//               metadata (ids, norms, bitmaps)
-//   warps 4-11  epilogue: TMEM lane quarter (warp % 4) = 32 query rows,
-//               column half = 2 of the 4 slabs; filter + register top-k
+// Roles (1 persistent CTA per SM, 10 warps, no CTA-wide barrier after setup;
+// every hand-off is an mbarrier):
+//   warp 0      producer: claims work items (one ahead, published in a
+//               4-entry item ring), walks the list's slab directory, keeps
+//               the live slabs (bitmap != 0, Eq. slot_valid at slab
+//               granularity) and issues gather4 + bulk copies of ids/norms
+//               into an nst-stage group ring
+//   warp 1      MMA: per group turns the bitmap into a NaN mask on the slot
+//               norms (group metadata for the epilogue), then one lane
+//               issues Dp/8 tcgen05.mma into one of two TMEM accumulators;
+//               tcgen05.commit frees the stage and signals the epilogue
+//   warps 2-5   query loaders: load the next item's 128 query rows into the
+//               spare one of two TMEM A buffers (double-buffered across
+//               items) with ||q||^2 and an integrality flag
+//   warps 6-9   epilogue: thread = query row (TMEM lane); per slab,
+//               t = ||x||^2 - 2 q.x is one FFMA and the slab's filter one
+//               FMNMX per candidate; only chunks whose min passes the row's
+//               threshold take the per-lane slow path (exact distance, then
+//               a sorted register top-k of (dist, id) keys)
+// TMEM columns: A[0] [0,128), A[1] [128,256), D[0] [256,384), D[1] [384,512).
 //
 // Exactness (BASELINE.json tolerances): when query and slab values are
 // integers with |v| <= 2048 (tf32-exact; slab flag set by k_append) and
-// ||q||^2 + ||x||^2 < 2^24, every product and partial sum is an exact integer,
-// so the tensor-core distance IS the exact distance (the SIFT-shaped case).
-// Otherwise the tensor-core value only filters: a slot is re-ranked with the
-// exact fp32 difference form iff d_tc - E <= current k-th distance, E a
-// certified bound on |d_tc - d_exact| (tf32 truncation + fp32 accumulation),
-// so no member of the exact top-k is ever dropped.  A per-query bound
-// (atomicMin of the k-th distance of finished half lists, shared between
-// the two halves of a row every group) prunes later candidates: any k real
-// candidates bound the final k-th distance from above.
+// (||q|| + ||x||)^2 < 2^24, every product, partial sum, t and ||q||^2 + t is
+// an exact integer: the tensor-core distance IS the exact distance (the
+// SIFT-shaped case).  Otherwise the value only filters: a slot is re-ranked
+// with the exact fp32 difference form iff t <= (thr - ||q||^2) + E, rounded
+// up, E a certified bound on |d_tc - d_exact| evaluated at the slab's largest
+// ||x||^2 (tf32 truncation + fp32 accumulation + the roundings of t and the
+// norms, safety factor 2), so no member of the exact top-k is ever dropped.
+// thr is the row's current k-th distance, seeded from a per-query bound
+// (atomicMin of the k-th distance of finished items of the same query).
+#include <cuda.h>
+
 #include <cstdio>
 
 #include "sivf_host.h"
@@ -48,56 +62,109 @@ namespace {
 constexpr int TM = 128;   // queries per tile (TMEM lanes, UMMA M)
 constexpr int GS = 4;     // slabs per group (UMMA N = 128)
 constexpr int GN = GS * kSlot;
-constexpr int NST = 2 * GS;  // stage ring: two groups in flight
-constexpr int TEPI = 8;   // epilogue warps
-constexpr int NTR = 2;    // transposer warps
-constexpr int W_PROD = 0, W_MMA = 1, W_TR0 = 2, W_EPI0 = W_TR0 + NTR;
-constexpr int TTHREADS = 32 * (W_EPI0 + TEPI);
+constexpr int NITEM = 4;  // work-item ring
+constexpr int MAXST = 6;  // group ring depth cap
+constexpr int NLD = 4, NEPI = 8;
+constexpr int W_SCHED = 0, W_MMA = 1, W_LD0 = 2, W_EPI0 = W_LD0 + NLD, W_TMA = W_EPI0 + NEPI;
+constexpr int TTHREADS = 32 * (W_TMA + 1);
+constexpr int MAXS = 64;  // live slabs per item prefetched by the scheduler (the producer walks the rest)
 
 struct TcArgs {
   DevState st;
   const float* Q;
-  int nprobe, k;
+  int nprobe, k, nst;
   const int32_t* inv_pairs;
   const int32_t* work_l;
   const int32_t* work_p0;
   const int32_t* work_n;
   unsigned long long* partial;
   uint32_t* gthr;
+  int dbg;  // experiments only (SIVF_OPT_DEBUG): bit0 skip the slow path, bit1 skip the fast path
 };
 
+struct ItemRec {
+  int32_t l, p0, nqt;  // l < 0: no more work
+  int32_t npre;        // live slabs prefetched into the slot's record array
+  int32_t dir_pos;     // directory position where the prefetch stopped (-1: complete)
+  int32_t len, pad[2];
+};
 struct StageMeta {
-  int32_t slab;   // -1: padding (no slab at this group position)
-  uint32_t bitmap;
-  uint32_t flag;
-  int32_t pad;
-};
-
-struct GroupMeta {
-  uint32_t id[GN];
-  float xn[GN];
+  int32_t slab[GS];  // -1: padding position
   uint32_t bm[GS];
   uint32_t flag[GS];
+  int32_t last, pad[3];
+};
+struct GroupMeta {
+  float xnm[GN];     // ||x||^2 per slot, NaN where the validity bit is clear
+  uint32_t id[GN];
+  float xnmax[GS];   // max ||x||^2 over the slab's valid slots
+  uint32_t flag[GS];
   int32_t slab[GS];
+  int32_t last, pad[3];
+};
+struct QInfo {
+  float qn;
+  int32_t pair;
+  uint32_t qint;
+  uint32_t pad;
 };
 
-// shared memory plan (bytes)
-struct TcSmem {
-  size_t stage, ib, gmeta, misc, total;
+struct TcPlan {
+  size_t stage_bytes, off_meta, off_gm, off_q, off_items, off_thr, off_mrg, off_bar, total;
 };
-__host__ __device__ inline TcSmem tc_smem_plan(int Dp, int KP) {
-  TcSmem p;
-  p.stage = (size_t)NST * (kSlot * Dp * 4 + kSlot * 8);  // payload + ids + norms per stage
-  p.ib = (size_t)GN * Dp * 4;                           // one interleaved group buffer
-  const size_t q = (size_t)TM * (Dp + 4) * 4;           // query staging (aliases the group buffers)
-  const size_t m = (size_t)TM * 2 * KP * 8;             // end-of-item half lists (alias too)
-  if (q > p.ib) p.ib = q;
-  if (m > p.ib) p.ib = m;
-  p.gmeta = 2 * sizeof(GroupMeta);
-  p.misc = (size_t)TM * 4 * 5 + NST * sizeof(StageMeta) + (2 * NST + 8) * 8 + 64;
-  p.total = p.stage + p.ib + p.gmeta + p.misc;
+__host__ __device__ inline TcPlan tc_plan(int Dp, int nst, int KP) {
+  TcPlan p;
+  p.stage_bytes = ((size_t)GN * Dp * 4 + 1023) & ~(size_t)1023;
+  p.off_meta = (size_t)nst * p.stage_bytes;
+  p.off_gm = p.off_meta + MAXST * sizeof(StageMeta);
+  p.off_q = p.off_gm + 2 * sizeof(GroupMeta);
+  p.off_items = p.off_q + 2 * TM * sizeof(QInfo);
+  p.off_thr = p.off_items + NITEM * (sizeof(ItemRec) + MAXS * sizeof(uint2));
+  p.off_mrg = p.off_thr + 2 * TM * 8;
+  p.off_bar = p.off_mrg + (size_t)TM * KP * 8;
+  p.total = p.off_bar + (3 * MAXST + 8 + 2 * NITEM + 2) * 8 + 1024;  // + alignment slack
   return p;
 }
+
+template <int KP>
+__device__ __forceinline__ void topk_reg_insert(u64 (&keys)[KP], u64 c) {
+#pragma unroll
+  for (int i = KP - 1; i > 0; --i) {
+    const u64 prev = keys[i - 1];
+    keys[i] = prev > c ? prev : (keys[i] > c ? c : keys[i]);
+  }
+  keys[0] = keys[0] > c ? c : keys[0];
+}
+
+// v[c] for a per-lane dynamic c without local memory: a 31-select tree.
+__device__ __forceinline__ uint32_t pick32(const uint32_t (&v)[32], int c) {
+  uint32_t a16[16], a8[8], a4[4], a2[2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a16[i] = (c & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a8[i] = (c & 2) ? a16[2 * i + 1] : a16[2 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a4[i] = (c & 4) ? a8[2 * i + 1] : a8[2 * i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) a2[i] = (c & 8) ? a4[2 * i + 1] : a4[2 * i];
+  return (c & 16) ? a2[1] : a2[0];
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+#ifdef SIVF_TC_PROF
+__device__ long long g_tr[6][1024];
+#define TR(r, g, v) \
+  do {              \
+    if (blockIdx.x == 0 && (g) < 1024u) g_tr[r][g] = (v); \
+  } while (0)
+#else
+#define TR(r, g, v) \
+  do {              \
+  } while (0)
+#endif
 
 #ifdef SIVF_TC_PROF
 #define PW(slot, stmt)                    \
@@ -111,410 +178,522 @@ __host__ __device__ inline TcSmem tc_smem_plan(int Dp, int KP) {
 #endif
 
 template <int KP>
-__device__ __forceinline__ void topk_reg_insert(u64 (&keys)[KP], u64 c) {
-#pragma unroll
-  for (int i = KP - 1; i > 0; --i) {
-    const u64 prev = keys[i - 1];
-    keys[i] = prev > c ? prev : (keys[i] > c ? c : keys[i]);
-  }
-  keys[0] = keys[0] > c ? c : keys[0];
-}
-
-template <int KP>
-__global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
-  extern __shared__ __align__(1024) unsigned char smem[];
+__global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const DevState& st = a.st;
-  const int Dp = st.Dp, Dq = Dp + 4, k = a.k, nquad = Dp >> 2;
-  const TcSmem plan = tc_smem_plan(Dp, KP);
-  float* stage_x = reinterpret_cast<float*>(smem);                                  // [NST][32*Dp]
-  uint32_t* stage_id = reinterpret_cast<uint32_t*>(stage_x + (size_t)NST * kSlot * Dp);  // [NST][32]
-  float* stage_nrm = reinterpret_cast<float*>(stage_id + NST * kSlot);              // [NST][32]
-  float* ib = reinterpret_cast<float*>(smem + plan.stage);                          // [Dp/4][128][4]
-  float* qs = ib;                                                                   // item start only
-  u64* mrg = reinterpret_cast<u64*>(ib);                                            // item end only
-  GroupMeta* gm = reinterpret_cast<GroupMeta*>(smem + plan.stage + plan.ib);        // [2]
-  float* qn_half = reinterpret_cast<float*>(gm + 2);                                // [2][TM]
-  int* qpair = reinterpret_cast<int*>(qn_half + 2 * TM);                           // [TM]
-  float* thr_sh = reinterpret_cast<float*>(qpair + TM);                            // [2][TM]
-  StageMeta* smeta = reinterpret_cast<StageMeta*>(thr_sh + 2 * TM);                // [NST]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smeta + NST);                        // [NST] producer -> transposer
-  uint64_t* empty = full + NST;                                                     // [NST] transposer -> producer
-  uint64_t* ib_full = empty + NST;                                                  // [1]   transposers -> MMA
-  uint64_t* ib_free = ib_full + 1;                                                  // [1]   MMA commit -> transposers
-  uint64_t* d_full = ib_free + 1;                                                   // [2]   MMA -> epilogue
-  uint64_t* grp_free = d_full + 2;                                                  // [2]   epilogue -> MMA, transposers
-  int* ctrl = reinterpret_cast<int*>(grp_free + 2);                                 // [0] item, [1] nlive
-  uint32_t* tmem_base_sm = reinterpret_cast<uint32_t*>(ctrl + 4);
-
+  const int Dp = st.Dp, nq4 = Dp >> 2, nst = a.nst, k = a.k;
+  const TcPlan p = tc_plan(Dp, nst, KP);
+  StageMeta* smeta = reinterpret_cast<StageMeta*>(smem + p.off_meta);
+  GroupMeta* gm = reinterpret_cast<GroupMeta*>(smem + p.off_gm);
+  QInfo* qinfo = reinterpret_cast<QInfo*>(smem + p.off_q);  // [2][TM]
+  ItemRec* items = reinterpret_cast<ItemRec*>(smem + p.off_items);
+  uint2* irec = reinterpret_cast<uint2*>(items + NITEM);  // [NITEM][MAXS] (slab | flag << 31, bitmap)
+  u64* thr_sh = reinterpret_cast<u64*>(smem + p.off_thr);    // [2][TM] (item << 32 | k-th bound bits)
+  u64* mrg = reinterpret_cast<u64*>(smem + p.off_mrg);       // [TM][KP] half-list hand-over
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);  // [MAXST] producer -> MMA (tx bytes)
+  uint64_t* empty = full + MAXST;                                  // [MAXST] MMA commit -> producer
+  uint64_t* meta_full = empty + MAXST;                             // [MAXST] producer -> MMA (stage metadata)
+  uint64_t* d_full = meta_full + MAXST;                            // [2] MMA -> epilogue
+  uint64_t* grp_free = d_full + 2;                                 // [2] epilogue -> MMA
+  uint64_t* a_full = grp_free + 2;                                 // [2] loaders -> MMA, epilogue
+  uint64_t* a_free = a_full + 2;                                   // [2] MMA commit + epilogue -> loaders
+  uint64_t* item_full = a_free + 2;                                // [NITEM] scheduler -> all
+  uint64_t* item_empty = item_full + NITEM;                        // [NITEM] epilogue -> scheduler
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(item_empty + NITEM);
+  auto stage_x = [&](int s) { return reinterpret_cast<float*>(smem + (size_t)s * p.stage_bytes); };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef SIVF_TC_PROF
   long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const long long tstart = clock64();
-  long long nitems = 0, ngrp = 0;
 #endif
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NST; ++i) {
+    for (int i = 0; i < MAXST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
+      mbar_init(&meta_full[i], 1);
     }
-    mbar_init(ib_full, NTR);
-    mbar_init(ib_free, 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&d_full[b], 1);
-      mbar_init(&grp_free[b], TEPI);
+      mbar_init(&d_full[b], 2);
+      mbar_init(&grp_free[b], NEPI);
+      mbar_init(&a_full[b], NLD);
+      mbar_init(&a_free[b], 1 + NEPI);
+    }
+    for (int i = 0; i < NITEM; ++i) {
+      mbar_init(&item_full[i], 1);
+      mbar_init(&item_empty[i], NEPI);
     }
     fence_mbar_init();
   }
-  if (warp == W_MMA) tmem_alloc(tmem_base_sm, 512);
+  for (int t = threadIdx.x; t < 2 * TM; t += blockDim.x) thr_sh[t] = ~0ull;  // tag matches no item
+  if (warp == W_MMA) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tmem_base_sm;
-  const uint32_t dcol0 = 128;  // A: columns [0, Dp <= 128); D[b]: columns [128 + 128 b, 256 + 128 b)
-  const int ntiles = st.ictr[I_NTILES];
-  const uint32_t idesc = umma_idesc_tf32(TM, GN);
-  uint32_t gg = 0;  // global group sequence number (all roles agree)
+  const uint32_t tbase = *tmem_holder;
 
-  for (;;) {
-    if (threadIdx.x == 0) ctrl[0] = atomicAdd(&st.ictr[I_WORK], 1);
-    PW(0, __syncthreads());
-    const int w_item = ctrl[0];
-    if (w_item >= ntiles) break;
-    const int l = a.work_l[w_item];
-    const int p0 = a.work_p0[w_item];
-    const int nqt = a.work_n[w_item];
-    const int len = st.dir_len[l];
-    const int32_t* dir = st.dir_arena + st.dir_off[l];
-    const int g4 = warp & 3, h = (warp - W_EPI0) >> 2;
-    const int row = 32 * g4 + lane;
-
-    // ------------------------------------------------ item setup
-    if (warp == W_PROD) {
-      int nlive = 0;
-      for (int j0 = 0; j0 < len; j0 += 32) {
-        const int j = j0 + lane;
-        const bool live = j < len && st.bitmap[dir[j]] != 0u;
-        nlive += __popc(__ballot_sync(kFull, live));
-      }
-      if (lane == 0) ctrl[1] = nlive;
-    } else if (warp >= W_EPI0) {
-#ifdef SIVF_TC_PROF
-      long long _tst = clock64();
-#endif
-      // stage the query tile: coalesced global -> smem rows, then each thread moves
-      // its row half into TMEM (the UMMA A operand)
-      const int te = threadIdx.x - 32 * W_EPI0;
-      if (te < TM) qpair[te] = te < nqt ? a.inv_pairs[p0 + te] : -1;
-      asm volatile("bar.sync 3, %0;" ::"r"(32 * TEPI));
-      {
-        // 2 threads per row, each a contiguous half row: independent loads in flight
-        const int r = te >> 1, hq = nquad >> 1, q0 = (te & 1) * hq;
-        const int pr = qpair[r];
-        const float* qr = a.Q + (int64_t)(pr >= 0 ? pr / a.nprobe : 0) * st.D;
-        const bool vec = (st.D & 3) == 0;
-#pragma unroll 8
-        for (int c4 = q0; c4 < q0 + hq + ((te & 1) ? (nquad & 1) : 0); ++c4) {
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (pr >= 0) {
-            if (vec && 4 * c4 + 3 < st.D) {
-              v = __ldg(reinterpret_cast<const float4*>(qr + 4 * c4));
-            } else {
-              float t[4];
-#pragma unroll
-              for (int jj = 0; jj < 4; ++jj) t[jj] = 4 * c4 + jj < st.D ? qr[4 * c4 + jj] : 0.f;
-              v = make_float4(t[0], t[1], t[2], t[3]);
-            }
+  if (warp == W_SCHED) {
+    // ------------------------------------------------------------ scheduler
+    // claims work items and walks each list's slab directory ahead of the
+    // producer (up to NITEM - 1 items ahead): the dependent loads (item ->
+    // directory -> bitmap -> flag) leave the TMA issue path
+    const int ntiles = st.ictr[I_NTILES];
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint32_t i = 0;; ++i) {
+      const int slot = (int)(i % NITEM);
+      if (lane == 0) PW(0, mbar_wait_sleep(&item_empty[slot], ((i / NITEM) & 1u) ^ 1u));
+      int w = 0;
+      if (lane == 0) w = atomicAdd(&st.ictr[I_WORK], 1);
+      w = __shfl_sync(kFull, w, 0);
+      ItemRec r{-1, 0, 0, 0, -1, 0, 0, 0};
+      if (w < ntiles) {
+        const int l = a.work_l[w];
+        const int len = st.dir_len[l];
+        const int32_t* dir = st.dir_arena + st.dir_off[l];
+        uint2* rec = irec + slot * MAXS;
+        int npre = 0, j0 = 0;
+        for (; j0 < len; j0 += 32) {
+          const int j = j0 + lane;
+          int sl = 0;
+          uint32_t bm = 0u;
+          if (j < len) {
+            sl = dir[j];
+            bm = st.bitmap[sl];
           }
-          *reinterpret_cast<float4*>(qs + r * Dq + 4 * c4) = v;
+          const unsigned live = __ballot_sync(kFull, bm != 0u);
+          if (npre + __popc(live) > MAXS) break;  // the producer walks the rest
+          if (bm) {
+            const uint32_t fl = st.slab_flag[sl] & 1u;
+            rec[npre + __popc(live & lt)] = make_uint2((uint32_t)sl | (fl << 31), bm);
+          }
+          npre += __popc(live);
         }
+        r = ItemRec{l, a.work_p0[w], a.work_n[w], npre, j0 < len ? j0 : -1, len, 0, 0};
       }
-      asm volatile("bar.sync 3, %0;" ::"r"(32 * TEPI));
-      float nrm = 0.f;
-      bool integral = true;
-      for (int c8 = h; c8 < (Dp >> 3); c8 += 2) {
-        uint32_t v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float x = qs[row * Dq + 8 * c8 + j];
-          v[j] = __float_as_uint(x);
-          nrm = fmaf(x, x, nrm);
-          integral = integral && x == rintf(x) && fabsf(x) <= 2048.f;
-        }
-        tmem_st8(tbase + ((uint32_t)(32 * g4) << 16) + (uint32_t)(8 * c8), v);
+      __syncwarp();
+      if (lane == 0) {
+        items[slot] = r;
+        mbar_arrive(&item_full[slot]);
       }
-      qn_half[h * TM + row] = integral ? nrm : -1.f - nrm;  // sign carries this half's integrality
-      const int pair = qpair[row];
-      thr_sh[h * TM + row] = pair >= 0 ? __uint_as_float(a.gthr[pair / a.nprobe]) : -1.f;
-      tmem_st_wait();
-#ifdef SIVF_TC_PROF
-      pw[0] += clock64() - _tst;
-#endif
+      if (w >= ntiles) break;
     }
-    tc_fence_before();
-    PW(1, __syncthreads());  // A in TMEM, nlive known, query staging area free again
-    tc_fence_after();
-    const int nlive = ctrl[1];
-    const int ngroups = (nlive + GS - 1) / GS;
-
-    // ------------------------------------------------ roles
-    if (warp == W_PROD) {
-      // bulk copies of the live slabs; group positions beyond nlive get an empty arrival
-      const uint32_t bytes = (uint32_t)kSlot * Dp * 4;
-      int i = 0;  // live slab counter
-      for (int j0 = 0; j0 < len; j0 += 32) {
-        const int j = j0 + lane;
-        int s = 0;
-        uint32_t bm = 0u, fl = 0u;
-        if (j < len) {
-          s = dir[j];
-          bm = st.bitmap[s];
-          fl = st.slab_flag[s];
+  } else if (warp == W_TMA) {
+    // ------------------------------------------------------------ producer
+    uint32_t gseq = 0;
+    // group slabs are held lane-distributed: lanes 0-3 the group being filled,
+    // lanes 4-7 the completed group waiting to learn whether it is the item's last
+    int my_s = 0;
+    uint32_t my_bm = 0u, my_fl = 0u;
+    auto emit = [&](int base, int nvalid, int last) {
+      const int stg = (int)(gseq % (uint32_t)nst);
+      if (lane == 0) PW(1, mbar_wait_sleep(&empty[stg], ((gseq / (uint32_t)nst) & 1u) ^ 1u));
+      if (lane == 0) TR(0, gseq, clock64());
+      __syncwarp();
+      const int sl = __shfl_sync(kFull, my_s, base + (lane & 3));
+      const uint32_t bmv = __shfl_sync(kFull, my_bm, base + (lane & 3));
+      const uint32_t flv = __shfl_sync(kFull, my_fl, base + (lane & 3));
+      const int s0 = nvalid > 0 ? __shfl_sync(kFull, sl, 0) : 0;
+      const int sp = (lane & 3) < nvalid ? sl : s0;  // padding positions re-read a real slab (masked)
+      int sj[GS];
+#pragma unroll
+      for (int j = 0; j < GS; ++j) sj[j] = __shfl_sync(kFull, sp, j);
+      StageMeta& m = smeta[stg];
+      if (lane < GS) {
+        m.slab[lane] = lane < nvalid ? sl : -1;
+        m.bm[lane] = lane < nvalid ? bmv : 0u;
+        m.flag[lane] = lane < nvalid ? flv : 0u;
+      }
+      if (lane == 0) m.last = last;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&meta_full[stg]);  // the MMA warp fetches the slot norms while the payload is in flight
+        mbar_arrive_expect_tx(&full[stg], (uint32_t)nq4 * 2048u);
+      }
+      __syncwarp();
+      if (lane < nq4)
+        tma_gather4(stage_x(stg) + lane * 512, &tmap, 0, sj[0] * nq4 + lane, sj[1] * nq4 + lane,
+                    sj[2] * nq4 + lane, sj[3] * nq4 + lane, &full[stg]);
+      ++gseq;
+    };
+    int cnt = 0;
+    bool has_pend = false;
+    auto feed = [&](int ss, uint32_t sbm, uint32_t sfl) {  // warp-uniform arguments
+      if (cnt == GS) {
+        if (has_pend) emit(4, GS, 0);
+        const int ps = __shfl_sync(kFull, my_s, lane & 3);
+        const uint32_t pb = __shfl_sync(kFull, my_bm, lane & 3), pf = __shfl_sync(kFull, my_fl, lane & 3);
+        if (lane >= 4 && lane < 8) {
+          my_s = ps;
+          my_bm = pb;
+          my_fl = pf;
         }
-        unsigned live = __ballot_sync(kFull, bm != 0u);
-        while (live) {
-          const int src = __ffs(live) - 1;
-          live &= live - 1;
-          const int ss = __shfl_sync(kFull, s, src);
-          const uint32_t sbm = __shfl_sync(kFull, bm, src), sfl = __shfl_sync(kFull, fl, src);
-          if (lane == 0) {
-            const uint32_t seq = gg * GS + (uint32_t)i;
-            const int pos = (int)(seq % NST);
-            const uint32_t use = seq / NST;
-            PW(2, mbar_wait(&empty[pos], (use & 1u) ^ 1u));
-            smeta[pos] = StageMeta{ss, sbm, sfl, 0};
-            mbar_arrive_expect_tx(&full[pos], bytes + 2 * kSlot * 4);
-            bulk_g2s(stage_x + (size_t)pos * kSlot * Dp, st.payload + (size_t)ss * kSlot * Dp, bytes, &full[pos]);
-            bulk_g2s(stage_id + pos * kSlot, st.slab_ids + (size_t)ss * kSlot, kSlot * 4, &full[pos]);
-            bulk_g2s(stage_nrm + pos * kSlot, st.slab_norm + (size_t)ss * kSlot, kSlot * 4, &full[pos]);
+        has_pend = true;
+        cnt = 0;
+      }
+      if (lane == cnt) {
+        my_s = ss;
+        my_bm = sbm;
+        my_fl = sfl;
+      }
+      ++cnt;
+    };
+    for (uint32_t i = 0;; ++i) {
+      const int slot = (int)(i % NITEM);
+      mbar_wait_sleep(&item_full[slot], (i / NITEM) & 1u);
+      const ItemRec rec = items[slot];
+      if (rec.l < 0) break;
+      cnt = 0;
+      has_pend = false;
+      const uint2* rr = irec + slot * MAXS;
+      for (int r = 0; r < rec.npre; ++r) {
+        const uint2 x = rr[r];
+        feed((int)(x.x & 0x7fffffffu), x.y, x.x >> 31);
+      }
+      if (rec.dir_pos >= 0) {  // long list: walk the rest of the directory here
+        const int32_t* dir = st.dir_arena + st.dir_off[rec.l];
+        for (int j0 = rec.dir_pos; j0 < rec.len; j0 += 32) {
+          const int j = j0 + lane;
+          int s = 0;
+          uint32_t bm = 0u, fl = 0u;
+          if (j < rec.len) {
+            s = dir[j];
+            bm = st.bitmap[s];
+            if (bm) fl = st.slab_flag[s] & 1u;
           }
-          ++i;
+          unsigned live = __ballot_sync(kFull, bm != 0u);
+          while (live) {
+            const int src = __ffs(live) - 1;
+            live &= live - 1;
+            feed(__shfl_sync(kFull, s, src), __shfl_sync(kFull, bm, src), __shfl_sync(kFull, fl, src));
+          }
         }
       }
-      if (lane == 0) {
-        for (; i < ngroups * GS; ++i) {  // pad the last group
-          const uint32_t seq = gg * GS + (uint32_t)i;
-          const int pos = (int)(seq % NST);
-          const uint32_t use = seq / NST;
-          mbar_wait(&empty[pos], (use & 1u) ^ 1u);
-          smeta[pos].slab = -1;
-          mbar_arrive(&full[pos]);
-        }
+      if (cnt > 0) {
+        if (has_pend) emit(4, GS, 0);
+        emit(0, cnt, 1);
+      } else if (has_pend) {
+        emit(4, GS, 1);
+      } else {
+        emit(0, 0, 1);  // no live slab: one fully masked group keeps the roles in step
       }
-    } else if (warp == W_MMA) {
-      if (lane == 0) {
-        for (int G = 0; G < ngroups; ++G) {
-          const uint32_t u = gg + (uint32_t)G, b = u & 1u;
-          PW(2, mbar_wait(ib_full, u & 1u));
-          mbar_wait(&grp_free[b], ((u >> 1) & 1u) ^ 1u);  // epilogue done reading D[b] (group u-2)
+    }
+  } else if (warp == W_MMA) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc = umma_idesc_tf32(TM, GN);
+    uint32_t gseq = 0;
+    for (uint32_t i = 0;; ++i) {
+      const int slot = (int)(i % NITEM);
+      mbar_wait_sleep(&item_full[slot], (i / NITEM) & 1u);
+      const ItemRec rec = items[slot];
+      if (rec.l < 0) break;
+      const uint32_t ab = i & 1u;
+      PW(1, mbar_wait_sleep(&a_full[ab], (i >> 1) & 1u));
+      for (;;) {
+        const int stg = (int)(gseq % (uint32_t)nst);
+        const uint32_t b = gseq & 1u;
+        mbar_wait_sleep(&meta_full[stg], (gseq / (uint32_t)nst) & 1u);
+        const StageMeta& sm = smeta[stg];
+        float xnv[GS];
+        uint32_t idv[GS];
+#pragma unroll
+        for (int j = 0; j < GS; ++j) {  // slot norms and ids: their latency hides behind the payload's
+          const size_t o = (size_t)(sm.slab[j] >= 0 ? sm.slab[j] : 0) * kSlot + lane;
+          xnv[j] = __ldg(st.slab_norm + o);
+          idv[j] = __ldg(st.slab_ids + o);
+        }
+        PW(2, mbar_wait_sleep(&full[stg], (gseq / (uint32_t)nst) & 1u));
+        if (lane == 0) TR(1, gseq, clock64());
+        PW(3, mbar_wait_sleep(&grp_free[b], ((gseq >> 1) & 1u) ^ 1u));
+        if (lane == 0) TR(2, gseq, clock64());
+        GroupMeta& g = gm[b];
+#pragma unroll
+        for (int j = 0; j < GS; ++j) {
+          const bool v = ((sm.bm[j] >> lane) & 1u) != 0u;
+          const float xn = xnv[j];
+          g.xnm[j * kSlot + lane] = v ? xn : __int_as_float(0x7fc00000);
+          g.id[j * kSlot + lane] = idv[j];
+          const uint32_t mx = __reduce_max_sync(kFull, v ? __float_as_uint(fmaxf(xn, 0.f)) : 0u);
+          if (lane == 0) {
+            g.xnmax[j] = __uint_as_float(mx);
+            g.flag[j] = sm.flag[j];
+            g.slab[j] = sm.slab[j];
+          }
+        }
+        const int last = sm.last;
+        if (lane == 0) g.last = last;
+        __syncwarp();
+        if (lane == 0) {
           tc_fence_after();
-          const uint32_t bsm = smem_u32(ib);
-          const uint32_t dt = tbase + dcol0 + b * GN;
-          for (int kk = 0; kk < (Dp >> 3); ++kk)
-            umma_tf32_ts(dt, tbase + (uint32_t)(8 * kk),
+          const uint32_t bsm = smem_u32(stage_x(stg));
+          const uint32_t dt = tbase + 256u + b * 128u, at = tbase + ab * 128u;
+          for (int kk = 0; kk < ((a.dbg & 4) ? 0 : (Dp >> 3)); ++kk)
+            umma_tf32_ts(dt, at + (uint32_t)(8 * kk),
                          umma_sdesc(bsm + (uint32_t)kk * 2u * GN * 16u, (uint32_t)GN * 16u, 128u), idesc,
                          kk > 0 ? 1u : 0u);
-          umma_commit(ib_free);      // interleave buffer may be refilled
-          umma_commit(&d_full[b]);
+          umma_commit(&empty[stg]);   // stage may be refilled once these MMAs have read it
+          umma_commit(&d_full[b]);    // accumulator ready
+          mbar_arrive(&d_full[b]);    // group metadata written
+          if (last) umma_commit(&a_free[ab]);
         }
-      }
-    } else if (warp < W_EPI0) {
-      // transposers: warp t handles group positions 2t, 2t+1
-      const int t = warp - W_TR0;
-      for (int G = 0; G < ngroups; ++G) {
-        const uint32_t u = gg + (uint32_t)G, b = u & 1u;
-        PW(2, mbar_wait(ib_free, (u & 1u) ^ 1u));               // MMA of the previous group has read the buffer
-        mbar_wait(&grp_free[b], ((u >> 1) & 1u) ^ 1u);           // epilogue done with gm[b] (group u-2)
-        float* dst = ib;
-        GroupMeta& m = gm[b];
-        for (int pp = 0; pp < 2; ++pp) {
-          const int gpos = 2 * t + pp;                          // position within the group
-          const uint32_t seq = u * GS + (uint32_t)gpos;
-          const int pos = (int)(seq % NST);                     // stage
-          PW(3, mbar_wait(&full[pos], (seq / NST) & 1u));
-          const StageMeta sm = smeta[pos];
-          const float* src = stage_x + (size_t)pos * kSlot * Dp;
-          if (sm.slab >= 0) {
-#pragma unroll 8
-            for (int q = 0; q < nquad; ++q)
-              *reinterpret_cast<float4*>(dst + ((size_t)q * GN + gpos * kSlot + lane) * 4) =
-                  *reinterpret_cast<const float4*>(src + ((size_t)q * kSlot + lane) * 4);
-            m.id[gpos * kSlot + lane] = stage_id[pos * kSlot + lane];
-            m.xn[gpos * kSlot + lane] = stage_nrm[pos * kSlot + lane];
-          }
-          if (lane == 0) {
-            m.bm[gpos] = sm.slab >= 0 ? sm.bitmap : 0u;
-            m.flag[gpos] = sm.slab >= 0 ? sm.flag : 0u;
-            m.slab[gpos] = sm.slab;
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[pos]);
-        }
-        fence_proxy_async_smem();  // generic smem writes -> visible to the tensor core (async proxy)
         __syncwarp();
-        if (lane == 0) mbar_arrive(ib_full);
+        ++gseq;
+        if (last) break;
       }
-    } else {
-      // ------------------------------------------------ epilogue
-      const int pair = qpair[row];
-      const int qglob = pair >= 0 ? pair / a.nprobe : -1;
-      const bool rv = row < nqt;
-      const float h0 = qn_half[row], h1 = qn_half[TM + row];
-      const bool qint = h0 >= 0.f && h1 >= 0.f;
-      const float qn = (h0 >= 0.f ? h0 : -1.f - h0) + (h1 >= 0.f ? h1 : -1.f - h1);
-      float thr = fminf(thr_sh[row], thr_sh[TM + row]);
-      u64 keys[KP];
-#pragma unroll
-      for (int i = 0; i < KP; ++i) keys[i] = i < KP - k ? 0ull : kPadKey;  // k-th = keys[KP-1]
-      u64 kth = kPadKey;
-      const float eps1 = 0x1p-9f + 0x1p-19f + (float)Dp * 0x1p-23f;
-      const float eps2 = (float)(2 * Dp + 8) * 0x1p-24f;
-      const bool exact_q = qint && qn < 8388608.f;
-      for (int G = 0; G < ngroups; ++G) {
-        const uint32_t u = gg + (uint32_t)G, b = u & 1u;
-        thr = fminf(thr, thr_sh[(1 - h) * TM + row]);  // partner half's bound
-        PW(2, mbar_wait(&d_full[b], (u >> 1) & 1u));
-        tc_fence_after();
-        const GroupMeta& m = gm[b];
+    }
+  } else if (warp < W_EPI0) {
+    // ------------------------------------------------------------ query loaders
+    // thread = query row (TMEM lane); rows are loaded 64 dims at a time, the
+    // first half before the A buffer is free (its latency hides behind the
+    // wait), then ||q||^2, an integrality flag and tcgen05.st into A[ab]
+    const int qw = warp & 3, row = 32 * qw + lane;
+    const bool vec = (st.D & 3) == 0;
+    const int nc8 = Dp >> 3;
+    for (uint32_t i = 0;; ++i) {
+      const int slot = (int)(i % NITEM);
+      mbar_wait_sleep(&item_full[slot], (i / NITEM) & 1u);
+      const ItemRec rec = items[slot];
+      if (rec.l < 0) break;
+      const uint32_t ab = i & 1u;
+      const bool rv = row < rec.nqt;
+      const bool wv = 32 * qw < rec.nqt && !(a.dbg & 16);  // warp-uniform: the warp has a real row
+      const int pair = rv ? a.inv_pairs[rec.p0 + row] : -1;
+      const float* qr = a.Q + (int64_t)(rv ? pair / a.nprobe : 0) * st.D;
+      const uint32_t ta = tbase + ((uint32_t)(32 * qw) << 16) + ab * 128u;
+      float nrm = 0.f;
+      uint32_t integ = 1u;
 #ifdef SIVF_TC_PROF
-        ngrp++;
-        long long _tg = clock64();
+      long long _tl0 = clock64();
 #endif
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          const int col0 = 64 * h + 16 * c;  // group column = pos * 32 + slot
-          const int pos = col0 >> 5, sb = col0 & 31;
-          uint32_t v[16];
-#ifdef SIVF_TC_PROF
-          long long _tl = clock64();
-#endif
-          tmem_ld16(tbase + ((uint32_t)(32 * g4) << 16) + dcol0 + b * GN + (uint32_t)col0, v);
-          tmem_ld_wait();
-#ifdef SIVF_TC_PROF
-          pw[6] += clock64() - _tl;
-#endif
-          const uint32_t bm = rv ? (m.bm[pos] >> sb) & 0xFFFFu : 0u;
-          if (!bm) continue;
-          const float4* nrm4 = reinterpret_cast<const float4*>(m.xn + col0);
-          const bool sint = exact_q && (m.flag[pos] & 1u) != 0u;
-          uint32_t pm = 0u, exm = 0u;
-          float dtc[16];
-          if (sint) {
+      for (int h0 = 0; h0 < nc8; h0 += 8) {
+        uint32_t v[8][8];
 #pragma unroll
-            for (int j4 = 0; j4 < 4; ++j4) {
-              const float4 xn = nrm4[j4];
-              const float xa[4] = {xn.x, xn.y, xn.z, xn.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int j = 4 * j4 + e;
-                const float sn = qn + xa[e];
-                dtc[j] = fmaf(-2.f, __uint_as_float(v[j]), sn);
-                const bool ex = sn < 16777216.f;  // every sum an integer < 2^24: exact
-                pm |= (dtc[j] <= thr && ex ? 1u : 0u) << j;
-                exm |= (ex ? 1u : 0u) << j;
-              }
-            }
-            const uint32_t fb = ~exm & 0xFFFFu;
-            if (fb) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const float xn = m.xn[col0 + j];
-                const float cs = sqrtf(qn * xn), sn = qn + xn;
-                const float E = 2.f * (2.f * eps1 * cs + eps2 * (sn + 2.f * cs));
-                if ((fb >> j) & 1u) pm |= (dtc[j] - E <= thr ? 1u : 0u) << j;
-              }
-            }
+        for (int u = 0; u < 8; ++u) {
+          const int d0 = 8 * (h0 + u);
+          float x[8];
+          if (wv && rv && vec && d0 + 7 < st.D) {
+            const float4 lo = __ldg(reinterpret_cast<const float4*>(qr + d0));
+            const float4 hi = __ldg(reinterpret_cast<const float4*>(qr + d0 + 4));
+            x[0] = lo.x, x[1] = lo.y, x[2] = lo.z, x[3] = lo.w, x[4] = hi.x, x[5] = hi.y, x[6] = hi.z, x[7] = hi.w;
           } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const float xn = m.xn[col0 + j];
-              const float sn = qn + xn;
-              dtc[j] = fmaf(-2.f, __uint_as_float(v[j]), sn);
-              const float cs = sqrtf(qn * xn);
-              const float E = 2.f * (2.f * eps1 * cs + eps2 * (sn + 2.f * cs));
-              pm |= (dtc[j] - E <= thr ? 1u : 0u) << j;
-            }
+            for (int e = 0; e < 8; ++e) x[e] = (rv && d0 + e < st.D) ? __ldg(qr + d0 + e) : 0.f;
           }
-          pm &= bm;
-#ifdef SIVF_TC_PROF
-          long long _ts = clock64();
-          pw[3] += __popc(pm);
-#endif
-          while (pm) {  // survivors: exact re-rank if needed, then the register top-k
-            const int j = __ffs(pm) - 1;
-            pm &= pm - 1;
-            float d = 0.f;
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) d = (jj == j) ? dtc[jj] : d;
-            if (!((exm >> j) & 1u)) {
-              const float* qr = a.Q + (int64_t)qglob * st.D;
-              const float* xs = st.payload + (size_t)m.slab[pos] * kSlot * Dp;
-              const int slot = sb + j;
-              float acc = 0.f;
-              for (int i4 = 0; i4 < nquad; ++i4) {
-                const float4 xv = __ldg(reinterpret_cast<const float4*>(xs + (i4 * kSlot + slot) * 4));
-                float qv[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) qv[e] = 4 * i4 + e < st.D ? __ldg(qr + 4 * i4 + e) : 0.f;
-                float tt;
-                tt = qv[0] - xv.x; acc = fmaf(tt, tt, acc);
-                tt = qv[1] - xv.y; acc = fmaf(tt, tt, acc);
-                tt = qv[2] - xv.z; acc = fmaf(tt, tt, acc);
-                tt = qv[3] - xv.w; acc = fmaf(tt, tt, acc);
-              }
-              d = acc;
-            }
-            if (!(d <= thr)) continue;
-            const u64 key = make_key(d, m.id[col0 + j]);
-            if (key >= kth) continue;
-            topk_reg_insert<KP>(keys, key);
-            kth = keys[KP - 1];
-            if (kth != kPadKey) thr = fminf(thr, key_dist(kth));
-#ifdef SIVF_TC_PROF
-            pw[4]++;
-#endif
-          }
-#ifdef SIVF_TC_PROF
-          pw[7] += clock64() - _ts;
-#endif
+          for (int e = 0; e < 8; ++e) v[u][e] = __float_as_uint(x[e]);
         }
-        thr_sh[h * TM + row] = thr;
+        if (h0 == 0) {
+          PW(4, mbar_wait_sleep(&a_free[ab], ((i >> 1) & 1u) ^ 1u));
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (h0 + u < nc8) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float x = __uint_as_float(v[u][e]);
+              nrm = fmaf(x, x, nrm);
+              integ &= (x == rintf(x) ? 1u : 0u) & (fabsf(x) <= 2048.f ? 1u : 0u);
+            }
+            if (wv) tmem_st8(ta + (uint32_t)(8 * (h0 + u)), v[u]);
+          }
+        }
+      }
+#ifdef SIVF_TC_PROF
+      pw[1] += clock64() - _tl0;
+      _tl0 = clock64();
+#endif
+      tmem_st_wait();
+#ifdef SIVF_TC_PROF
+      pw[2] += clock64() - _tl0;
+#endif
+      qinfo[ab * TM + row] = QInfo{nrm, pair, integ, 0u};
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[ab]);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    // thread = (query row, slab half h): slabs 2h, 2h+1 of every group; the two
+    // halves of a row keep separate top-k lists (merged at the item's end) and
+    // share their k-th distance bounds through shared memory every group
+    const int qw = warp & 3, row = 32 * qw + lane, h = (warp - W_EPI0) >> 2;
+    const float eps1 = 0x1p-9f + 0x1p-19f + (float)Dp * 0x1p-23f;
+    const float eps2 = (float)(2 * Dp + 10) * 0x1p-24f;
+    uint32_t gseq = 0;
+    for (uint32_t i = 0;; ++i) {
+      const int slot = (int)(i % NITEM);
+      mbar_wait_sleep(&item_full[slot], (i / NITEM) & 1u);
+      const ItemRec rec = items[slot];
+      if (rec.l < 0) break;
+      const uint32_t ab = i & 1u;
+      PW(1, mbar_wait_sleep(&a_full[ab], (i >> 1) & 1u));
+      const QInfo qi = qinfo[ab * TM + row];
+      const bool rv = row < rec.nqt;
+      const bool wact = 32 * qw < rec.nqt;
+      const int qglob = rv ? qi.pair / a.nprobe : 0;
+      const float qn = qi.qn, sqn = sqrtf(qn);
+      float thr = rv ? __uint_as_float(__ldcg(a.gthr + qglob)) : -INFINITY;
+      float gnext = thr, tpub = thr;
+      u64 keys[KP];
+#pragma unroll
+      for (int t = 0; t < KP; ++t) keys[t] = t < KP - k ? 0ull : kPadKey;  // k-th = keys[KP-1]
+      u64 kth = kPadKey;
+      for (;;) {
+        const uint32_t b = gseq & 1u;
+        PW(5, mbar_wait_sleep(&d_full[b], (gseq >> 1) & 1u));
+        if (lane == 0 && warp == W_EPI0 + 2) TR(3, gseq, clock64());
+        if (lane == 0 && warp == W_EPI0 + 6) TR(5, gseq, clock64());
+        tc_fence_after();
+        const GroupMeta& g = gm[b];
+        if (wact) {
+          const u64 ps = thr_sh[(1 - h) * TM + row];  // partner half's bound, tagged with its item
+          if ((uint32_t)(ps >> 32) == i) thr = fminf(thr, __uint_as_float((uint32_t)ps));
+          thr = fminf(thr, gnext);  // other items of the same query (read one group ago)
+          if (rv) gnext = __uint_as_float(__ldcg(a.gthr + qglob));
+          // one chunk = one slab = 32 TMEM columns of this row
+          auto chunk = [&](const int j, const uint32_t(&v)[32]) {
+            const float xm = g.xnmax[j], sxm = sqrtf(xm);
+            const float rs = sqn + sxm;
+            const bool ex = qi.qint != 0u && (g.flag[j] & 1u) != 0u && rs * rs < 16000000.f;
+            float E = 0.f;
+            if (!ex) {
+              const float cs = sqn * sxm;
+              E = 2.f * (2.f * eps1 * cs + eps2 * (qn + xm + 2.f * cs));
+            }
+            float tadj = ex ? __fsub_ru(thr, qn) : __fadd_ru(__fsub_ru(thr, qn), E);
+            const float4* x4 = reinterpret_cast<const float4*>(g.xnm + 32 * j);
+            float m8[8];
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const float4 xx = x4[c4];
+              const float t0 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 0]), xx.x);
+              const float t1 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 1]), xx.y);
+              const float t2 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 2]), xx.z);
+              const float t3 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 3]), xx.w);
+              m8[c4] = fminf(fminf(t0, t1), fminf(t2, t3));
+            }
+            const float mn = fminf(fminf(fminf(m8[0], m8[1]), fminf(m8[2], m8[3])),
+                                   fminf(fminf(m8[4], m8[5]), fminf(m8[6], m8[7])));
+            if (!(mn <= tadj) || (a.dbg & 1)) return;
+            // slow path (per lane): survivors of this slab, exact distance, register top-k
+#ifdef SIVF_TC_PROF
+            long long _ts = clock64();
+#endif
+            uint32_t pm = 0u;
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const float4 xx = x4[c4];
+              pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 0]), xx.x) <= tadj ? 1u : 0u) << (4 * c4);
+              pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 1]), xx.y) <= tadj ? 1u : 0u) << (4 * c4 + 1);
+              pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 2]), xx.z) <= tadj ? 1u : 0u) << (4 * c4 + 2);
+              pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 3]), xx.w) <= tadj ? 1u : 0u) << (4 * c4 + 3);
+            }
+            while (pm) {
+              const int c = __ffs(pm) - 1;
+              pm &= pm - 1;
+              const float t = fmaf(-2.f, __uint_as_float(pick32(v, c)), g.xnm[32 * j + c]);
+              if (!(t <= tadj)) continue;  // the threshold may have tightened
+              float d;
+              if (ex) {
+                d = qn + t;  // exact: every term an integer < 2^24
+              } else {
+                const float* xs = st.payload + (size_t)g.slab[j] * kSlot * Dp;
+                const float* qr = a.Q + (int64_t)qglob * st.D;
+                float acc = 0.f;
+                for (int i4 = 0; i4 < nq4; ++i4) {
+                  const float4 xv = __ldg(reinterpret_cast<const float4*>(xs + (i4 * kSlot + c) * 4));
+                  float qv[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) qv[e] = 4 * i4 + e < st.D ? __ldg(qr + 4 * i4 + e) : 0.f;
+                  float tt;
+                  tt = qv[0] - xv.x; acc = fmaf(tt, tt, acc);
+                  tt = qv[1] - xv.y; acc = fmaf(tt, tt, acc);
+                  tt = qv[2] - xv.z; acc = fmaf(tt, tt, acc);
+                  tt = qv[3] - xv.w; acc = fmaf(tt, tt, acc);
+                }
+                d = acc;
+              }
+              d = fmaxf(d, 0.f);
+              if (!(d <= thr)) continue;
+              const u64 key = make_key(d, g.id[32 * j + c]);
+              if (key >= kth) continue;
+              topk_reg_insert<KP>(keys, key);
+              kth = keys[KP - 1];
+              if (kth != kPadKey) {
+                thr = fminf(thr, key_dist(kth));
+                tadj = ex ? __fsub_ru(thr, qn) : __fadd_ru(__fsub_ru(thr, qn), E);
+              }
+#ifdef SIVF_TC_PROF
+              pw[7]++;
+#endif
+            }
+#ifdef SIVF_TC_PROF
+            pw[6] += clock64() - _ts;
+#endif
+          };
+          const uint32_t dcol = tbase + ((uint32_t)(32 * qw) << 16) + 256u + b * 128u + (uint32_t)(64 * h);
+#ifdef SIVF_TC_PROF
+          long long _tg = clock64();
+#endif
+#pragma unroll 1
+          for (int jj = 0; jj < 2; ++jj) {
+            uint32_t v[32];
+#ifdef SIVF_TC_PROF
+            long long _tq = clock64();
+#endif
+            tmem_ld32(dcol + 32u * (uint32_t)jj, v);
+            tmem_ld_wait();
+#ifdef SIVF_TC_PROF
+            pw[3] += clock64() - _tq;
+#endif
+            if (!(a.dbg & 2)) chunk(2 * h + jj, v);
+          }
+#ifdef SIVF_TC_PROF
+          pw[0] += clock64() - _tg;
+#endif
+          thr_sh[h * TM + row] = ((u64)i << 32) | __float_as_uint(thr);
+          if (rv && thr < tpub) {  // share the bound with the query's other items right away
+            atomicMin(a.gthr + qglob, __float_as_uint(thr));
+            tpub = thr;
+          }
+        }
+        const int last = g.last;
+        if (lane == 0 && warp == W_EPI0 + 2) TR(4, gseq, clock64());
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&grp_free[b]);
-#ifdef SIVF_TC_PROF
-        pw[5] += clock64() - _tg;
-#endif
+        ++gseq;
+        if (last) break;
       }
-      // merge the two half lists of each row (the group buffers are idle now)
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * TEPI));
+      // merge the two halves of each row: h = 1 hands its list over in smem
+      if (h == 1 && rv) {
 #pragma unroll
-      for (int i = 0; i < KP; ++i) mrg[((size_t)row * 2 + h) * KP + i] = keys[i];
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * TEPI));
+        for (int t = 0; t < KP; ++t) mrg[row * KP + t] = keys[t];
+      }
+      PW(2, named_bar_sync(1 + qw, 64));
       if (h == 0 && rv) {
-        const u64* A0 = mrg + (size_t)row * 2 * KP + (KP - k);
-        const u64* A1 = A0 + KP;
-        int i0 = 0, i1 = 0;
-        u64 last = kPadKey;
-        for (int j = 0; j < k; ++j) {
-          const u64 x0 = A0[i0], x1 = A1[i1];
-          const u64 x = x0 < x1 ? x0 : x1;
-          if (x0 < x1) ++i0; else ++i1;
-          a.partial[(size_t)pair * k + j] = x;
-          last = x;
+        for (int t = KP - k; t < KP; ++t) {
+          const u64 key = mrg[row * KP + t];
+          if (key >= kth) break;  // sorted: the rest cannot enter
+          topk_reg_insert<KP>(keys, key);
+          kth = keys[KP - 1];
         }
-        if (last != kPadKey) atomicMin(&a.gthr[qglob], __float_as_uint(key_dist(last)));
+#pragma unroll
+        for (int t = 0; t < KP; ++t)
+          if (t >= KP - k) a.partial[(size_t)qi.pair * k + (t - (KP - k))] = keys[t];
+        if (kth != kPadKey) atomicMin(&a.gthr[qglob], __float_as_uint(key_dist(kth)));
+      }
+      named_bar_sync(1 + qw, 64);
+      if (lane == 0) {
+        mbar_arrive(&a_free[ab]);
+        mbar_arrive(&item_empty[slot]);
       }
     }
-    gg += (uint32_t)ngroups;
-#ifdef SIVF_TC_PROF
-    nitems++;
-#endif
-    __syncthreads();
   }
 #ifdef SIVF_TC_PROF
-  if (blockIdx.x < 2 && lane == 0 && (warp <= W_TR0 || warp == W_EPI0))
-    printf("blk %d warp %d total %lld items %lld grp %lld | staging %lld setupsync %lld wait %lld surv %lld ins %lld groupbody %lld tmemld %lld survloop %lld\n",
-           blockIdx.x, warp, clock64() - tstart, nitems, ngrp, pw[0], pw[1], pw[2], pw[3], pw[4], pw[5], pw[6], pw[7]);
+  if (blockIdx.x < 2 && lane == 0)
+    printf("blk %d warp %d total %lld | p0 %lld p1 %lld p2 %lld p3 %lld p4 %lld p5 %lld slow %lld ins %lld\n",
+           blockIdx.x, warp, clock64() - tstart, pw[0], pw[1], pw[2], pw[3], pw[4], pw[5], pw[6], pw[7]);
 #endif
   tc_fence_before();
   __syncthreads();
@@ -522,38 +701,134 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   if (warp == W_MMA) tmem_dealloc(tbase, 512);
 }
 
+
+// Seed of the per-query bound gthr[q] on its final k-th distance: exact
+// distances from q to the live slots of the first `nseed` live slabs of its
+// nearest probed list (probes are sorted, rank 0 first).  Any k real
+// candidates bound the final k-th distance from above, so the bound only
+// prunes work, never results.  The difference form here and the scan's
+// distances may round differently (each within (Dp+2) 2^-24 relative of the
+// exact value), so the bound is inflated by (1 + (Dp+2) 2^-23), rounded up.
+// Warp per query; lane = slot; slab payload loads are 512-B coalesced.
+__global__ void __launch_bounds__(128) k_seed_bound(DevState st, const float* __restrict__ Q, int64_t nq,
+                                                    int nprobe, const int32_t* __restrict__ probes, int nseed,
+                                                    int k, uint32_t* __restrict__ gthr) {
+  __shared__ __align__(16) float qs[4][128];
+  __shared__ u64 tops[4][64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.x * 4 + w;
+  if (q >= nq) return;  // warp-uniform
+  const int Dp = st.Dp, nq4 = Dp >> 2;
+  for (int d = lane; d < Dp; d += 32) qs[w][d] = d < st.D ? __ldg(Q + q * st.D + d) : 0.f;
+  u64* top = tops[w];
+  u64* tmp = top + 32;
+  warp_topk_init(top, k);
+  const int l = probes[q * nprobe];
+  const int len = st.dir_len[l];
+  const int32_t* dir = st.dir_arena + st.dir_off[l];
+  const float infl = 1.f + (float)(Dp + 2) * 0x1p-23f;
+  int used = 0;
+  for (int j = 0; j < len && used < nseed; ++j) {
+    const int s = dir[j];
+    const uint32_t bm = st.bitmap[s];
+    if (!bm) continue;
+    ++used;
+    const float4* xs = reinterpret_cast<const float4*>(st.payload + (size_t)s * kSlot * Dp);
+    const float4* q4 = reinterpret_cast<const float4*>(qs[w]);
+    float acc = 0.f;
+#pragma unroll 8
+    for (int c4 = 0; c4 < nq4; ++c4) {
+      const float4 xv = __ldg(xs + c4 * kSlot + lane);
+      const float4 qv = q4[c4];
+      float t;
+      t = qv.x - xv.x; acc = fmaf(t, t, acc);
+      t = qv.y - xv.y; acc = fmaf(t, t, acc);
+      t = qv.z - xv.z; acc = fmaf(t, t, acc);
+      t = qv.w - xv.w; acc = fmaf(t, t, acc);
+    }
+    const bool valid = (bm >> lane) & 1u;
+    warp_topk_insert(top, tmp, k, valid ? make_key(__fmul_ru(acc, infl), st.slab_ids[(size_t)s * kSlot + lane])
+                                        : kPadKey);
+  }
+  const u64 kth = top[k - 1];
+  if (lane == 0 && kth != kPadKey) atomicMin(&gthr[q], __float_as_uint(key_dist(kth)));
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int tc_stages(const Index& ix, int KP) {
+  const size_t sb = tc_plan(ix.st.Dp, 0, KP).stage_bytes;
+  const size_t fixed = tc_plan(ix.st.Dp, 0, KP).total;
+  if (ix.smem_optin < fixed) return 0;
+  int n = (int)((ix.smem_optin - fixed) / sb);
+  return n > MAXST ? MAXST : n;
+}
+
 }  // namespace
 
 bool scan_tc_supported(const Index& ix, int k) {
-  if (ix.st.Dp > 128 || k > 32) return false;
-  const int KP = k <= 16 ? 16 : 32;
-  return tc_smem_plan(ix.st.Dp, KP).total <= ix.smem_optin;
+  return ix.st.Dp <= 128 && k <= 32 && ix.payload_tmap_ok && tc_stages(ix, k <= 16 ? 16 : 32) >= 2;
 }
 
 cudaError_t setup_scan_tc(Index& ix) {
   if (ix.st.Dp > 128) return cudaSuccess;
-  for (int KP : {16, 32}) {
-    const size_t need = tc_smem_plan(ix.st.Dp, KP).total;
-    if (need > ix.smem_optin) continue;
-    cudaError_t e = KP == 16
-                        ? cudaFuncSetAttribute(k_scan_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need)
-                        : cudaFuncSetAttribute(k_scan_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
-    if (e != cudaSuccess) return e;
+  if (tc_stages(ix, 32) < 2) return cudaSuccess;
+  // TMA descriptor of the payload as [num_slabs * Dp/4] rows x 128 floats (512 B)
+  EncodeTiledFn enc = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q) !=
+          cudaSuccess ||
+      enc == nullptr) {
+    cudaGetLastError();
+    return cudaSuccess;  // no TMA descriptor: the CUDA-core scan serves every search
   }
-  return cudaSuccess;
+  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+  const cuuint64_t gdim[2] = {128, (cuuint64_t)ix.st.num_slabs * (cuuint64_t)(ix.st.Dp >> 2)};
+  const cuuint64_t gstr[1] = {512};
+  const cuuint32_t box[2] = {128, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(ix.payload_tmap);
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ix.st.payload, gdim, gstr, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  ix.payload_tmap_ok = r == CUDA_SUCCESS;
+  if (!ix.payload_tmap_ok) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_scan_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tc_plan(ix.st.Dp, tc_stages(ix, 16), 16).total);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_scan_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc_plan(ix.st.Dp, tc_stages(ix, 32), 32).total);
+  return e;
 }
 
 cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s) {
   Scratch& sc = ix.sc;
-  TcArgs a{ix.st, d_q, nprobe, k, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr};
   const int KP = k <= 16 ? 16 : 32;
-  const size_t smem = tc_smem_plan(ix.st.Dp, KP).total;
-  if (KP == 16) k_scan_tc<16><<<ix.num_sms, TTHREADS, smem, s>>>(a);
-  else k_scan_tc<32><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+  const int nst = tc_stages(ix, KP);
+  TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, ix.dbg};
+  const size_t smem = tc_plan(ix.st.Dp, nst, KP).total;
+  const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(ix.payload_tmap);
+  if (k <= 16) k_scan_tc<16><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);
+  else k_scan_tc<32><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);
   ix.launches += 1;
   return cudaGetLastError();
 }
 
 int scan_tc_tile() { return TM; }
 
+cudaError_t launch_seed_bound(Index& ix, const float* d_q, int64_t nq, int k, int nprobe, cudaStream_t s) {
+  if (ix.seed_slabs <= 0 || nq <= 0 || ix.st.Dp > 128 || k > 32) return cudaSuccess;
+  k_seed_bound<<<ceil_div(nq, 4), 128, 0, s>>>(ix.st, d_q, nq, nprobe, ix.sc.probes, ix.seed_slabs, k, ix.sc.gthr);
+  ix.launches += 1;
+  return cudaGetLastError();
+}
+
 }  // namespace sivf
+
+#ifdef SIVF_TC_PROF
+extern "C" int sivf_debug_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, sivf::g_tr, sizeof(long long) * 6 * 1024);
+}
+#endif

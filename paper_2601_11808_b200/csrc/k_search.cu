@@ -214,13 +214,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
 // probed list (rank 0) and bucket 1 the rest; work items are laid out bucket-
 // major, so each query's nearest list is scanned first and the per-query bound
 // on its k-th distance is already in place for its other lists.
-__global__ void k_inv_count(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int nb, int nlist,
-                            int32_t* __restrict__ cnt, uint32_t* __restrict__ gthr) {
+__global__ void k_inv_count(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int nb, int r0,
+                            int nlist, int32_t* __restrict__ cnt, uint32_t* __restrict__ gthr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npairs) return;
   const int p = (int)(i % nprobe);
   if (p == 0) gthr[i / nprobe] = 0x7F800000u;  // per-query bound = +inf
-  const int b = (nb == 2 && p > 0) ? 1 : 0;
+  const int b = (nb == 2 && p >= r0) ? 1 : 0;
   atomicAdd(&cnt[b * nlist + probes[i]], 1);
 }
 
@@ -286,12 +286,12 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
   }
 }
 
-__global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int nb, int nlist,
-                              int32_t* __restrict__ cursor, int32_t* __restrict__ pairs) {
+__global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int nb, int r0,
+                              int nlist, int32_t* __restrict__ cursor, int32_t* __restrict__ pairs) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npairs) return;
   const int p = (int)(i % nprobe);
-  const int b = (nb == 2 && p > 0) ? 1 : 0;
+  const int b = (nb == 2 && p >= r0) ? 1 : 0;
   pairs[atomicAdd(&cursor[b * nlist + probes[i]], 1)] = (int32_t)i;
 }
 
@@ -409,15 +409,28 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   if (e != cudaSuccess) return e;
   const int64_t npairs = nq * nprobe;
   if (d_probes) cudaMemcpyAsync(d_probes, sc.probes, sizeof(int32_t) * npairs, cudaMemcpyDeviceToDevice, s);
-  // Tensor-core path: probe-rank buckets (nearest list first), one scan launch.
-  const int nb = (tc && nprobe > 1 && ix.tc_two_phase) ? 2 : 1;
+  // Tensor-core path: probe-rank buckets, one scan launch.  Work items are laid
+  // out bucket-major, so with nb = 2 every query's r0 nearest lists are scanned
+  // first and its k-th distance bound is tight before the other lists are
+  // reached (far fewer survivors of the tensor-core filter).  Split only when
+  // the lists are long enough in queries that it adds no tiles on average.
+  int nb = 1, r0 = nprobe;
+  if (tc && nprobe >= 8) {
+    const int64_t per_list = npairs / nlist;
+    const int rr = ix.tc_two_phase ? 1 : nprobe / 4;
+    const int64_t ta = ceil_div(per_list * rr / nprobe, QT), tb = ceil_div(per_list - per_list * rr / nprobe, QT);
+    if (ix.tc_two_phase || (ix.rank_split && ta + tb <= ceil_div(per_list, QT))) {
+      nb = 2;
+      r0 = rr;
+    }
+  }
   const int nent = nb * nlist;
   {
     PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
     cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * nent, s);
-    k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, nlist, sc.inv_cnt, sc.gthr);
+    k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, r0, nlist, sc.inv_cnt, sc.gthr);
     k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr);
-    k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, nlist, sc.inv_cursor,
+    k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, r0, nlist, sc.inv_cursor,
                                                          sc.inv_pairs);
     k_work_fill<<<ceil_div(nent, 256), 256, 0, s>>>(sc.tile_off, sc.inv_off, nent, nlist, QT, sc.work_l,
                                                     sc.work_p0, sc.work_n);
@@ -427,11 +440,16 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   const int grid = ix.num_sms;  // persistent: one CTA per SM
   {
     PhaseTimer pt(ix, SIVF_PH_SCAN, s);
-    if (tc) e = launch_scan_tc(ix, d_q, k, nprobe, s);
+    if (tc) {
+      e = launch_seed_bound(ix, d_q, nq, k, nprobe, s);  // after k_inv_count reset gthr to +inf
+      if (e == cudaSuccess) e = launch_scan_tc(ix, d_q, k, nprobe, s);
+    }
     else if (nw == 8) k_scan<8><<<grid, 32 * 9, smem, s>>>(a);
     else if (nw == 4) k_scan<4><<<grid, 32 * 5, smem, s>>>(a);
     else k_scan<2><<<grid, 32 * 3, smem, s>>>(a);
     if (!tc) ix.launches += 1;
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return e;  // a failed scan launch must not be masked by the merge below
   }
   PhaseTimer pt(ix, SIVF_PH_MERGE, s);
   const int wpb = 4;

@@ -81,7 +81,15 @@ struct Index {
   bool use_tc_scan = true;
   bool use_tc_coarse = true;  // tcgen05 coarse quantisation (k_coarse_tc.cu); false = exact SIMT k_dist_exact
   bool tc_two_phase = false;  // nearest-list-first scan phase (SIVF_OPT_TC_TWO_PHASE)  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
+  bool rank_split = true;     // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT)
+  int dbg = 0;                // experiment switches (SIVF_OPT_DEBUG)
+  int seed_slabs = 8;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS)
   int64_t launches = 0;
+  // TMA descriptor (CUtensorMap, 128 B) of the payload viewed as rows of 512 B
+  // (row = slab * Dp/4 + c4), box 128 floats x 1 row: the tile::gather4 source
+  // of k_scan_tc (encoded once in setup_scan_tc; the payload never moves).
+  alignas(64) unsigned char payload_tmap[128] = {};
+  bool payload_tmap_ok = false;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
   // phase profiling (sivf_profile_*)
@@ -150,6 +158,7 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
 // k_search.cu
 cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
                           int64_t* d_ids, int32_t* d_probes, cudaStream_t s);
+cudaError_t launch_seed_bound(Index& ix, const float* d_q, int64_t nq, int k, int nprobe, cudaStream_t s);
 cudaError_t launch_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int32_t G, int64_t nq, int32_t k,
                               float* d_dist, int64_t* d_ids, cudaStream_t s, int64_t* launches);
 // k_train.cu

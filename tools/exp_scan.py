@@ -15,11 +15,14 @@ for b in range(0, N, 65536):
 Q = torch.from_numpy(gen.queries(0, NQ)).cuda()
 two = int(os.environ.get("TWO_PHASE", "0"))
 ix.set_option(2, two)
-for npb in (8, 32):
+ix.set_option(99, int(os.environ.get("DBG", "0")))
+seeds = [int(v) for v in os.environ.get("SEEDS", "8").split(",")]
+for seed, npb in [(sd, npb) for sd in seeds for npb in (8, 32)]:
+    ix.set_option(4, seed)
     ix.search(Q, 10, npb); torch.cuda.synchronize()
     ix.profile(True); ix.profile_read()
     for _ in range(5): ix.search(Q, 10, npb)
     torch.cuda.synchronize()
     p = ix.profile_read(); ix.profile(False)
     tot = {k: v[0] / 5 for k, v in p.items() if v[1]}
-    print(os.path.basename(S.LIB_PATH), "two" if two else "one", "nprobe", npb, {k: round(v, 4) for k, v in tot.items()}, flush=True)
+    print(os.path.basename(S.LIB_PATH), "two" if two else "one", "nprobe", npb, "seed", seed, {k: round(v, 4) for k, v in tot.items()}, flush=True)
