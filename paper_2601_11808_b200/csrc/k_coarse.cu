@@ -115,10 +115,10 @@ __global__ void k_select_probes(const float* __restrict__ dist, int64_t nq, int6
 
 }  // namespace
 
-cudaError_t launch_assign_exact(Index& ix, const float* d_x, int64_t n, cudaStream_t s) {
+cudaError_t launch_assign_exact(Index& ix, const float* d_x, int64_t n, cudaStream_t s, bool need_dist) {
   if (n <= 0) return cudaSuccess;
   PhaseTimer pt(ix, SIVF_PH_ASSIGN, s);
-  if (coarse_tc_supported(ix, 1)) return launch_coarse_tc(ix, d_x, n, 1, ix.sc.row_best, nullptr, s);
+  if (coarse_tc_supported(ix, 1)) return launch_coarse_tc(ix, d_x, n, 1, ix.sc.row_best, nullptr, s, need_dist);
   cudaMemsetAsync(ix.sc.row_best, 0xff, sizeof(unsigned long long) * n, s);
   dim3 grid(ceil_div(ix.st.nlist, BN), ceil_div(n, BM));
   k_dist_exact<0><<<grid, 256, 0, s>>>(d_x, n, ix.st.D, ix.st.centroids, ix.st.Dp, ix.st.nlist, ix.sc.row_best,

@@ -37,18 +37,23 @@
 // <= its dist32 <= U_(m) <= U, hence is a candidate, and the re-rank orders
 // candidates by the exact key.  A row whose buffer overflows re-ranks all lists.
 //
-// Error bound (u = 2^-10 tf32 operand truncation, w = 2^-23 = 2x the fp32
+// Split tf32 products: x = xh + xl, c = ch + cl with xh, ch tf32-exact (low 13
+// mantissa bits cleared) and |xl| < u|x|, |cl| < u|c|; the tensor cores compute
+// xh.ch + xh.cl + xl.ch (3 MMAs per K step into one fp32 accumulator).
+// Error bound (u = 2^-10 tf32 operand precision, w = 2^-23 = 2x the fp32
 // unit roundoff, S = ||x|| ||c|| >= sum |x_k c_k|):
-//   |2 x.c_tc - 2 x.c|   <= 2 [(2u + u^2) + (Dp + 2) w] S        (operands, fp32 accumulation)
+//   |2 x.c_tc - 2 x.c|   <= 2 [3u^2(1+u) + (3 Dp + 2) w] S       (operands, fp32 accumulation)
 //   norms + the 2 roundings of A            <= (D + 6) w (||x||^2 + ||c||^2) + 4 w S
 //   |dist32 - d|                            <= (D + 2) w/2 d       (Higham, non-negative terms)
 // E = 2 (E0 + e3 (max(A,0) + E0)),  E0 = e1 S + e2 (||x||^2 + ||c||^2),
-// e1 = 2(2u+u^2) + 2(Dp+4)w, e2 = (D+6)w, e3 = (D+3)w (safety factor 2); with
+// e1 = 2(3u^2+4u^3) + 2(3Dp+4)w, e2 = (D+6)w, e3 = (D+3)w (safety factor 2); with
 // max(A,0) <= ||x||^2 + ||c||^2 + 2S + E0 this is <= ka S + kb (||x||^2 + ||c||^2),
 // ka = 2(1+2e3)e1 + 4e3, kb = 2(1+2e3)e2 + 2e3 (both rounded up), the form
 // evaluated per element.  A violation could only show up as a wrong assignment or
 // probe set; the GPU tests compare both with the oracle bit for bit, including
 // adversarial 1-ulp near-ties.
+#include <cuda.h>
+
 #include "sivf_host.h"
 
 namespace sivf {
@@ -57,17 +62,17 @@ namespace {
 
 constexpr int TM = 128;        // rows per tile (UMMA M, TMEM lanes)
 constexpr int TN = 256;        // centroids per N-tile (UMMA N)
-constexpr int KC = 32;         // dims per pipeline stage
+constexpr int KC = 16;         // dims per pipeline stage (hi and lo halves of each operand)
 constexpr int NSTG = 4;        // stage ring depth
 constexpr int W_PROD = 0, W_MMA = 1, W_EPI0 = 2, NEPI = 8;
 constexpr int CTHREADS = 32 * (W_EPI0 + NEPI);
-constexpr size_t kStageA = (size_t)TM * KC * 4;  // 16 KB
-constexpr size_t kStageB = (size_t)TN * KC * 4;  // 32 KB
+constexpr size_t kStageA = (size_t)2 * TM * KC * 4;  // 16 KB: [hi | lo]
+constexpr size_t kStageB = (size_t)2 * TN * KC * 4;  // 32 KB: [hi | lo]
 
 struct CoarseArgs {
-  const float* x_tiles;   // [ntile][Dp/4][128][4]
+  const float* x_tiles;   // [ntile][hi, lo][Dp/4][128][4]
   const float* xnorm;     // [n]
-  const float* c_tiles;   // [nct][Dp/4][256][4]
+  const float* c_tiles;   // [nct][hi, lo][Dp/4][256][4]
   const float* cnorm;     // [nct*256] ||c||^2 (NaN for padding columns)
   const float* ccsa;      // [nct*256] ka * ||c||
   const float* ccnb;      // [nct*256] kb * ||c||^2
@@ -77,14 +82,20 @@ struct CoarseArgs {
   unsigned long long* cand;  // [n][cap] lower-bound keys (bits(max(A-E,0)) << 32 | list)
   float* cand_ub;            // [n][cap] upper bounds A+E
   int32_t* cand_cnt;         // [n] appended candidates (> cap: overflow)
+  float* mat;                // KP == 0: A = ||x||^2 + ||c||^2 - 2 x.c_tc, [n][nlist] row-major
+  int ntpc;                  // N-tiles per CTA (blockIdx.y selects the range); KP != 0: all
 };
 
-__host__ __device__ constexpr size_t coarse_smem_bytes() {
-  return (size_t)NSTG * (kStageA + kStageB)  // operand ring
+__host__ __device__ constexpr int coarse_nstg(int KP) { return KP == 0 ? 3 : NSTG; }
+__host__ __device__ constexpr size_t coarse_xchg_bytes(int KP) {
+  return KP == 0 ? (size_t)NEPI * 32 * 32 * 4 : (size_t)TM * 32 * 4;  // store tiles | half-row top-32
+}
+__host__ __device__ constexpr size_t coarse_smem_bytes(int KP = 1) {
+  return (size_t)coarse_nstg(KP) * (kStageA + kStageB)  // operand ring
          + 2 * 3 * TN * 4                    // per-N-tile column constants (double buffered)
-         + TM * 32 * 4                       // half-row top-32 exchange
+         + coarse_xchg_bytes(KP)             // exchange area
          + TM * 4 + 2 * TM * 4               // candidate counters, half-row bounds
-         + 256;                              // barriers, TMEM base
+         + 256 + 1024;                       // barriers, TMEM base, alignment slack
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -140,17 +151,19 @@ __device__ __forceinline__ void merge_lower32(float (&keys)[32], const float* c)
 // columns), the halves merge them, and U = the m-th smallest over the row;
 // pass 2 recomputes the products and appends exactly the lists with A-E <= U.
 template <int KP>
-__global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(CoarseArgs a) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  float* sA = reinterpret_cast<float*>(smem);                                  // [NSTG][16 KB]
-  float* sB = reinterpret_cast<float*>(smem + NSTG * kStageA);                 // [NSTG][32 KB]
-  float* colc = reinterpret_cast<float*>(smem + NSTG * (kStageA + kStageB));   // [2][3][TN]
-  float* xchg = colc + 2 * 3 * TN;                                             // [TM][32]
-  int* cnt_sm = reinterpret_cast<int*>(xchg + TM * 32);                        // [TM]
+__global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(const __grid_constant__ CUtensorMap tmat, CoarseArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 128B-swizzle tiles
+  constexpr int NS = coarse_nstg(KP);
+  float* sA = reinterpret_cast<float*>(smem);                                  // [NS][16 KB]
+  float* sB = reinterpret_cast<float*>(smem + NS * kStageA);                   // [NS][32 KB]
+  float* colc = reinterpret_cast<float*>(smem + NS * (kStageA + kStageB));     // [2][3][TN]
+  float* xchg = colc + 2 * 3 * TN;                                             // see coarse_xchg_bytes
+  int* cnt_sm = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(xchg) + coarse_xchg_bytes(KP));  // [TM]
   float* thr_sh = reinterpret_cast<float*>(cnt_sm + TM);                       // [2][TM]
   uint64_t* full = reinterpret_cast<uint64_t*>(thr_sh + 2 * TM);
-  uint64_t* empty = full + NSTG;
-  uint64_t* acc_full = empty + NSTG;   // [2]
+  uint64_t* empty = full + NS;
+  uint64_t* acc_full = empty + NS;     // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint32_t* tmem_base_sm = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -158,11 +171,12 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(CoarseArgs a) {
   const int tile = blockIdx.x;
   const int Dp = a.Dp, nq4 = Dp >> 2;
   const int nchunk = (Dp + KC - 1) / KC;
-  const int ntn = (a.nlist + TN - 1) / TN;
-  constexpr int NPASS = KP == 1 ? 1 : 2;
+  const int jbeg = blockIdx.y * a.ntpc;
+  const int ntn = min((a.nlist + TN - 1) / TN - jbeg, a.ntpc);  // N-tiles of this CTA: [jbeg, jbeg + ntn)
+  constexpr int NPASS = KP <= 1 ? 1 : 2;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NSTG; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -185,18 +199,22 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(CoarseArgs a) {
 
   if (warp == W_PROD) {
     if (lane == 0) {
-      const float* xa = a.x_tiles + (size_t)tile * nq4 * TM * 4;
+      const float* xa = a.x_tiles + (size_t)tile * 2 * nq4 * TM * 4;
       uint32_t seq = 0;
       for (int t = 0; t < NPASS * ntn; ++t) {
-        const float* cb = a.c_tiles + (size_t)(t % ntn) * nq4 * TN * 4;
+        const float* cb = a.c_tiles + (size_t)(jbeg + t % ntn) * 2 * nq4 * TN * 4;
         for (int c = 0; c < nchunk; ++c, ++seq) {
-          const int st = (int)(seq % NSTG);
-          mbar_wait(&empty[st], ((seq / NSTG) & 1u) ^ 1u);
+          const int st = (int)(seq % NS);
+          mbar_wait(&empty[st], ((seq / NS) & 1u) ^ 1u);
           const int kc = min(KC, Dp - c * KC);
           const uint32_t ba = (uint32_t)kc * TM * 4, bb = (uint32_t)kc * TN * 4;
-          mbar_arrive_expect_tx(&full[st], ba + bb);
-          bulk_g2s(sA + (size_t)st * (kStageA / 4), xa + (size_t)c * KC * TM, ba, &full[st]);
-          bulk_g2s(sB + (size_t)st * (kStageB / 4), cb + (size_t)c * KC * TN, bb, &full[st]);
+          mbar_arrive_expect_tx(&full[st], 2 * (ba + bb));
+          float* da = sA + (size_t)st * (kStageA / 4);
+          float* db = sB + (size_t)st * (kStageB / 4);
+          bulk_g2s(da, xa + (size_t)c * KC * TM, ba, &full[st]);                                  // x hi
+          bulk_g2s(da + TM * KC, xa + (size_t)nq4 * TM * 4 + (size_t)c * KC * TM, ba, &full[st]);   // x lo
+          bulk_g2s(db, cb + (size_t)c * KC * TN, bb, &full[st]);                                  // c hi
+          bulk_g2s(db + TN * KC, cb + (size_t)nq4 * TN * 4 + (size_t)c * KC * TN, bb, &full[st]);   // c lo
         }
       }
     }
@@ -210,16 +228,21 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(CoarseArgs a) {
         tc_fence_after();
         const uint32_t dt = tbase + b * TN;
         for (int c = 0; c < nchunk; ++c, ++seq) {
-          const int st = (int)(seq % NSTG);
-          mbar_wait(&full[st], (seq / NSTG) & 1u);
+          const int st = (int)(seq % NS);
+          mbar_wait(&full[st], (seq / NS) & 1u);
           tc_fence_after();
           const int kc = min(KC, Dp - c * KC);
           const uint32_t a0 = smem_u32(sA + (size_t)st * (kStageA / 4));
           const uint32_t b0 = smem_u32(sB + (size_t)st * (kStageB / 4));
-          for (int kk = 0; kk < (kc >> 3); ++kk)
-            umma_tf32_ss(dt, umma_sdesc(a0 + (uint32_t)kk * 2u * TM * 16u, TM * 16u, 128u),
-                         umma_sdesc(b0 + (uint32_t)kk * 2u * TN * 16u, TN * 16u, 128u), idesc,
+          // split tf32 ("3xTF32"): x.c ~ xh.ch + xh.cl + xl.ch (the bound E below)
+          for (int kk = 0; kk < (kc >> 3); ++kk) {
+            const uint32_t ah = a0 + (uint32_t)kk * 2u * TM * 16u, al = ah + (uint32_t)(TM * KC * 4);
+            const uint32_t bh = b0 + (uint32_t)kk * 2u * TN * 16u, bl = bh + (uint32_t)(TN * KC * 4);
+            umma_tf32_ss(dt, umma_sdesc(ah, TM * 16u, 128u), umma_sdesc(bh, TN * 16u, 128u), idesc,
                          (c > 0 || kk > 0) ? 1u : 0u);
+            umma_tf32_ss(dt, umma_sdesc(ah, TM * 16u, 128u), umma_sdesc(bl, TN * 16u, 128u), idesc, 1u);
+            umma_tf32_ss(dt, umma_sdesc(al, TM * 16u, 128u), umma_sdesc(bh, TN * 16u, 128u), idesc, 1u);
+          }
           umma_commit(&empty[st]);  // stage reusable once these MMAs have read it
         }
         umma_commit(&acc_full[b]);
@@ -236,14 +259,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(CoarseArgs a) {
     const bool rv = row < a.n;
     const float qn = rv ? a.xnorm[row] : 0.f;
     const float sq = sqrtf(qn), qnb = a.kb * qn;
-    float keys[KP];
+    float keys[KP > 0 ? KP : 1];
 #pragma unroll
     for (int i = 0; i < KP; ++i) keys[i] = i < KP - a.m ? -INFINITY : INFINITY;
     float Uo = INFINITY;  // KP == 1: running min upper bound; KP == 32: final U (after pass 1)
     unsigned long long* crow = a.cand + (size_t)(rv ? row : 0) * a.cap;
     float* urow = a.cand_ub + (size_t)(rv ? row : 0) * a.cap;
     for (int t = 0; t < NPASS * ntn; ++t) {
-      const int j = t % ntn;
+      const int j = jbeg + t % ntn;
       const bool append_pass = NPASS == 1 || t >= ntn;
       if constexpr (NPASS == 2) {
         if (t == ntn) {
@@ -283,6 +306,32 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(CoarseArgs a) {
         __syncwarp();
         tmem_ld32(tbase + ((uint32_t)(32 * q) << 16) + b * TN + (uint32_t)cb, v);
         tmem_ld_wait();
+        if constexpr (KP == 0) {
+          // store A = ||x||^2 + ||c||^2 - 2 x.c_tc for the per-row selection: the
+          // warp's 32 rows x 32 columns go to a 128B-swizzled shared tile (conflict-free
+          // 16-B stores), then one TMA tensor store (rows >= n land in unused scratch
+          // rows; columns >= nlist are clipped by the tensor map)
+          float* T = xchg + (size_t)ew * 32 * 32;
+#pragma unroll
+          for (int c16 = 0; c16 < 8; ++c16) {
+            const float4 cn = *reinterpret_cast<const float4*>(cc + cb + 4 * c16);
+            float4 o;
+            o.x = fmaf(-2.f, __uint_as_float(v[4 * c16 + 0]), qn + cn.x);
+            o.y = fmaf(-2.f, __uint_as_float(v[4 * c16 + 1]), qn + cn.y);
+            o.z = fmaf(-2.f, __uint_as_float(v[4 * c16 + 2]), qn + cn.z);
+            o.w = fmaf(-2.f, __uint_as_float(v[4 * c16 + 3]), qn + cn.w);
+            *reinterpret_cast<float4*>(T + lane * 32 + ((c16 ^ (lane & 7)) * 4)) = o;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmat, T, j * TN + cb, tile * TM + 32 * q);
+            bulk_commit();
+            bulk_wait_read0();  // the tile may be rewritten by the next chunk
+          }
+          __syncwarp();
+          continue;
+        }
         if constexpr (NPASS == 2) {
           if (!append_pass) {
           // pass 1 (KP == 32): exact per-half top-32 of the upper bounds
@@ -339,25 +388,42 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(CoarseArgs a) {
       if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
     asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI));
-    if (h == 0 && rv) a.cand_cnt[row] = cnt_sm[r];
+    if (KP != 0 && h == 0 && rv) a.cand_cnt[row] = cnt_sm[r];
   }
+  if (KP == 0 && warp >= W_EPI0 && lane == 0) bulk_wait0();  // stores complete before exit
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == W_MMA) tmem_dealloc(tbase, 512);
 }
 
-// X [n][D] row-major -> [n/128][Dp/4][128][4] zero padded; ||x||^2 (fp32, any order).
-__global__ void __launch_bounds__(TM) k_rows_tiles(const float* __restrict__ X, int64_t n, int D, int Dp,
-                                                   float* __restrict__ out, float* __restrict__ norm) {
-  const int r = threadIdx.x;
+// The tf32 part of x (low 13 mantissa bits cleared): exactly representable in tf32,
+// so the tensor core takes it unchanged whether it truncates or rounds; x - hi is
+// exact in fp32 and |x - hi| < 2^-10 |x|.
+__device__ __forceinline__ float4 tf32_hi(float4 v) {
+  return make_float4(__uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u),
+                     __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u),
+                     __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u),
+                     __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
+}
+
+// X [n][D] row-major -> [n/128][hi, lo][Dp/4][128][4] zero padded; ||x||^2 (fp32, any order).
+// 4 threads per row (quarters of the row, loads issued 8 ahead), partial norms
+// combined through shared memory.
+__global__ void __launch_bounds__(4 * TM) k_rows_tiles(const float* __restrict__ X, int64_t n, int D, int Dp,
+                                                       float* __restrict__ out, float* __restrict__ norm) {
+  __shared__ float part[4][TM];
+  const int r = threadIdx.x & (TM - 1), qt = threadIdx.x >> 7;
   const int64_t row = (int64_t)blockIdx.x * TM + r;
   const int nq4 = Dp >> 2;
-  float4* o = reinterpret_cast<float4*>(out) + (size_t)blockIdx.x * nq4 * TM + r;
+  const int c0 = (nq4 * qt) >> 2, c1 = (nq4 * (qt + 1)) >> 2;
+  float4* o = reinterpret_cast<float4*>(out) + (size_t)blockIdx.x * 2 * nq4 * TM + r;
+  float4* ol = o + (size_t)nq4 * TM;
   const float* xr = X + (row < n ? row : 0) * (int64_t)D;
   const bool vec = (D & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
   float nrm = 0.f;
-  for (int c4 = 0; c4 < nq4; ++c4) {
+#pragma unroll 8
+  for (int c4 = c0; c4 < c1; ++c4) {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (row < n) {
       if (vec && 4 * c4 + 3 < D) {
@@ -369,10 +435,14 @@ __global__ void __launch_bounds__(TM) k_rows_tiles(const float* __restrict__ X, 
         v = make_float4(t[0], t[1], t[2], t[3]);
       }
     }
-    o[(size_t)c4 * TM] = v;
+    const float4 hi = tf32_hi(v);
+    o[(size_t)c4 * TM] = hi;
+    ol[(size_t)c4 * TM] = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);  // exact
     nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nrm))));
   }
-  if (row < n) norm[row] = nrm;
+  part[qt][r] = nrm;
+  __syncthreads();
+  if (qt == 0 && row < n) norm[row] = (part[0][r] + part[1][r]) + (part[2][r] + part[3][r]);
 }
 
 // centroids [nlist][Dp] -> [nlist/256][Dp/4][256][4] zero padded; per column
@@ -383,12 +453,15 @@ __global__ void __launch_bounds__(TN) k_cent_tiles(const float* __restrict__ C, 
   const int r = threadIdx.x;
   const int l = blockIdx.x * TN + r;
   const int nq4 = Dp >> 2;
-  float4* o = reinterpret_cast<float4*>(out) + (size_t)blockIdx.x * nq4 * TN + r;
+  float4* o = reinterpret_cast<float4*>(out) + (size_t)blockIdx.x * 2 * nq4 * TN + r;
+  float4* ol = o + (size_t)nq4 * TN;
   const float4* cr = reinterpret_cast<const float4*>(C + (size_t)(l < nlist ? l : 0) * Dp);
   float nrm = 0.f;
   for (int c4 = 0; c4 < nq4; ++c4) {
     const float4 v = l < nlist ? cr[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
-    o[(size_t)c4 * TN] = v;
+    const float4 hi = tf32_hi(v);
+    o[(size_t)c4 * TN] = hi;
+    ol[(size_t)c4 * TN] = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);  // exact
     nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nrm))));
   }
   cnorm[l] = l < nlist ? nrm : __int_as_float(0x7fc00000);
@@ -424,6 +497,44 @@ __device__ __forceinline__ float dist32_rows(const float* __restrict__ xs, const
     s = __fadd_rn(s, __fmul_rn(t, t));
   }
   return s;
+}
+
+// Two canonical dist32 chains interleaved (independent sequential sums: the
+// latency of one 128-long add chain hides the other's).
+__device__ __forceinline__ void dist32_rows2(const float* __restrict__ xs, const float* __restrict__ c0,
+                                             const float* __restrict__ c1, int D, bool vec, float& d0, float& d1) {
+  float s0 = 0.f, s1 = 0.f;
+  int k = 0;
+  if (vec) {
+    for (; k + 16 <= D; k += 16) {
+      float4 a[4], b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a[j] = __ldg(reinterpret_cast<const float4*>(c0 + k) + j);
+        b[j] = __ldg(reinterpret_cast<const float4*>(c1 + k) + j);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 xv = *reinterpret_cast<const float4*>(xs + k + 4 * j);
+        float t, u;
+        t = __fsub_rn(xv.x, a[j].x); u = __fsub_rn(xv.x, b[j].x);
+        s0 = __fadd_rn(s0, __fmul_rn(t, t)); s1 = __fadd_rn(s1, __fmul_rn(u, u));
+        t = __fsub_rn(xv.y, a[j].y); u = __fsub_rn(xv.y, b[j].y);
+        s0 = __fadd_rn(s0, __fmul_rn(t, t)); s1 = __fadd_rn(s1, __fmul_rn(u, u));
+        t = __fsub_rn(xv.z, a[j].z); u = __fsub_rn(xv.z, b[j].z);
+        s0 = __fadd_rn(s0, __fmul_rn(t, t)); s1 = __fadd_rn(s1, __fmul_rn(u, u));
+        t = __fsub_rn(xv.w, a[j].w); u = __fsub_rn(xv.w, b[j].w);
+        s0 = __fadd_rn(s0, __fmul_rn(t, t)); s1 = __fadd_rn(s1, __fmul_rn(u, u));
+      }
+    }
+  }
+  for (; k < D; ++k) {
+    const float t = __fsub_rn(xs[k], __ldg(c0 + k)), u = __fsub_rn(xs[k], __ldg(c1 + k));
+    s0 = __fadd_rn(s0, __fmul_rn(t, t));
+    s1 = __fadd_rn(s1, __fmul_rn(u, u));
+  }
+  d0 = s0;
+  d1 = s1;
 }
 
 __host__ __device__ inline size_t rerank_smem_per_warp(int m, int cap, int Dp) {
@@ -517,13 +628,234 @@ __global__ void __launch_bounds__(128) k_coarse_rerank(const float* __restrict__
   }
 }
 
+
+// Per-row selection over the stored A matrix (warp per row; lane owns the
+// columns lane + 32 i).  With E the certified bound of the file comment:
+//   U = the m-th smallest upper bound max(A + E, 0) (m = 1: the minimum; else a
+//       bisection on the fp32 bit pattern: the smallest t with #{ub <= t} >= m),
+//   candidates = {l : A_l - E_l <= U} (every member of the exact top-m, ties
+//       included, has lower bound <= its dist32 <= U),
+// then the canonical dist32 of each candidate and the exact top-m by
+// (dist32, l).  MODE 0: best[row] = smallest key (assignment); MODE 1:
+// probes[row][0..m) sorted.  More than CCAP candidates: every list is re-ranked.
+constexpr int CCAP = 256;
+#ifdef SIVF_TC_PROF
+__device__ unsigned g_selhist[2][64];
+__device__ unsigned long long g_selclk[2][8];
+#define SELCLK(i)                                                             \
+  do {                                                                        \
+    const long long _t = clock64();                                           \
+    if (lane == 0) atomicAdd(&g_selclk[MODE][i], (unsigned long long)(_t - _t0)); \
+    _t0 = _t;                                                                 \
+  } while (0)
+#else
+#define SELCLK(i) \
+  do {            \
+  } while (0)
+#endif
+constexpr int SELW = 8;  // rows (warps) per block
+__host__ __device__ inline size_t select_smem_per_warp(int Dp) {
+  return (size_t)Dp * 4 + 2 * CCAP * 4 + 2 * 32 * 8;
+}
+__host__ __device__ inline size_t select_smem(int Dp, int nlist) {
+  return SELW * select_smem_per_warp(Dp) + (size_t)2 * nlist * 4;
+}
+template <int NPL, int MODE>
+__global__ void __launch_bounds__(32 * SELW) k_coarse_select(const float* __restrict__ mat,
+                                                             const float* __restrict__ X, int64_t n, int D,
+                                                             int nlist, int m, const float* __restrict__ xnorm,
+                                                             const float* __restrict__ ccsa,
+                                                             const float* __restrict__ ccnb, float kb,
+                                                             const float* __restrict__ C, int Dp,
+                                                             unsigned long long* __restrict__ best,
+                                                             int32_t* __restrict__ probes, int probes_ld,
+                                                             int need_dist) {
+  extern __shared__ __align__(16) unsigned char sm_sel[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* csa_s = reinterpret_cast<float*>(sm_sel + SELW * select_smem_per_warp(Dp));
+  float* cnb_s = csa_s + nlist;
+  for (int c = threadIdx.x; c < nlist; c += blockDim.x) {
+    csa_s[c] = __ldg(ccsa + c);
+    cnb_s[c] = __ldg(ccnb + c);
+  }
+  __syncthreads();
+  const int64_t row = (int64_t)blockIdx.x * SELW + w;
+  if (row >= n) return;  // warp-uniform
+#ifdef SIVF_TC_PROF
+  long long _t0 = clock64();
+#endif
+  unsigned char* base = sm_sel + (size_t)w * select_smem_per_warp(Dp);
+  float* xs = reinterpret_cast<float*>(base);
+  int32_t* cand = reinterpret_cast<int32_t*>(xs + Dp);
+  float* capx = reinterpret_cast<float*>(cand + CCAP);  // approximate distance of each candidate
+  unsigned long long* top = reinterpret_cast<unsigned long long*>(capx + CCAP);
+  unsigned long long* tmp = top + 32;
+  // lane owns the columns lane + 32 i (coalesced 128-B row segments)
+  const float* arow = mat + (size_t)row * nlist;
+  float A[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) A[i] = lane + 32 * i < nlist ? __ldcs(arow + lane + 32 * i) : INFINITY;
+  const float qn = xnorm[row], sq = sqrtf(qn), qnb = kb * qn;
+  float lbv[NPL];
+  uint32_t ubb[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int c = lane + 32 * i;
+    lbv[i] = INFINITY;
+    ubb[i] = 0x7F800000u;
+    if (c < nlist) {
+      const float E = fmaf(sq, csa_s[c], qnb + cnb_s[c]);
+      lbv[i] = A[i] - E;
+      ubb[i] = __float_as_uint(fmaxf(A[i] + E, 0.f));
+    }
+  }
+  const float* xr = X + row * (int64_t)D;
+  for (int k = lane; k < Dp; k += 32) xs[k] = k < D ? __ldg(xr + k) : 0.f;
+  SELCLK(0);
+  uint32_t Ub;
+  if (MODE == 0 || m == 1) {
+    uint32_t mn = 0x7F800000u;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) mn = min(mn, ubb[i]);
+    Ub = __reduce_min_sync(kFull, mn);
+  } else {
+    // hi = the largest of the lanes' minima: >= 32 >= m upper bounds are <= hi, so
+    // U lies among the values <= hi; those are compacted (shared memory) and the
+    // m-th smallest found by bisection on the fp32 bit pattern
+    uint32_t mn = 0x7F800000u;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) mn = min(mn, ubb[i]);
+    uint32_t hi = m <= 32 ? __reduce_max_sync(kFull, mn) : 0x7F800000u;
+    uint32_t lo = __reduce_min_sync(kFull, mn);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(cand);  // scratch, reused for candidates below
+    int ns = 0;
+    const unsigned ltm = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const bool keep = ubb[i] <= hi;
+      const unsigned pm = __ballot_sync(kFull, keep);
+      const int pos = ns + __popc(pm & ltm);
+      if (keep && pos < CCAP) sv[pos] = ubb[i];
+      ns += __popc(pm);
+    }
+    __syncwarp();
+    if (ns <= CCAP) {
+      uint32_t u[CCAP / 32];
+#pragma unroll
+      for (int t = 0; t < CCAP / 32; ++t) u[t] = lane + 32 * t < ns ? sv[lane + 32 * t] : 0xFFFFFFFFu;
+      while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        int c = 0;
+#pragma unroll
+        for (int t = 0; t < CCAP / 32; ++t) c += u[t] <= mid ? 1 : 0;
+        if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) hi = mid;
+        else lo = mid + 1;
+      }
+    } else {
+      while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) c += ubb[i] <= mid ? 1 : 0;
+        if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) hi = mid;
+        else lo = mid + 1;
+      }
+    }
+    __syncwarp();
+    Ub = hi;
+  }
+  SELCLK(1);
+  const float U = __uint_as_float(Ub);
+  // candidates: lower bound <= U (columns beyond nlist have A = +inf)
+  int nc = 0;
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const bool pass = lbv[i] <= U;
+    const unsigned pm = __ballot_sync(kFull, pass);
+    const int pos = nc + __popc(pm & lt);
+    if (pass && pos < CCAP) {
+      cand[pos] = lane + 32 * i;
+      capx[pos] = fmaxf(0.5f * (lbv[i] + __uint_as_float(ubb[i])), 0.f);
+    }
+    nc += __popc(pm);
+  }
+  __syncwarp();
+#ifdef SIVF_TC_PROF
+  if (lane == 0) atomicAdd(&g_selhist[MODE][nc < 63 ? nc : 63], 1u);
+#endif
+  SELCLK(2);
+  const bool all = nc > CCAP;
+  const int total = all ? nlist : nc;
+  const bool vec = (Dp & 3) == 0;
+  unsigned long long bestk = ~0ull;
+  if (MODE == 0 && nc == 1 && !need_dist) {
+    // a single candidate is certainly the argmin; the insert path needs only the list
+    if (lane == 0) best[row] = (unsigned long long)(uint32_t)cand[0];
+    return;
+  }
+  if (MODE == 1 && nc == m) {
+    // exactly m candidates: the probe SET is certain (reading C3); order by the
+    // approximate distance (nearest-first only steers the scan's work order)
+    unsigned long long k0 = lane < nc ? make_key(capx[lane], (uint32_t)cand[lane]) : kPadKey;
+    k0 = warp_sort32(k0);
+    if (lane < m) probes[row * probes_ld + lane] = (int32_t)key_id(k0);
+    SELCLK(3);
+    return;
+  }
+  if (MODE == 1 && total <= 64) {
+    // <= 64 candidates: exact keys, two warp sorts and one bitonic merge
+    unsigned long long k0 = kPadKey, k1 = kPadKey;
+    if (lane < total) {
+      const int l0 = cand[lane], l1 = lane + 32 < total ? cand[lane + 32] : l0;
+      float d0, d1;
+      dist32_rows2(xs, C + (size_t)l0 * Dp, C + (size_t)l1 * Dp, D, vec, d0, d1);
+      k0 = make_key(d0, (uint32_t)l0);
+      if (lane + 32 < total) k1 = make_key(d1, (uint32_t)l1);
+    }
+    k0 = warp_sort32(k0);
+    if (total > 32) {
+      k1 = warp_sort32(k1);
+      k0 = umin64(k0, __shfl_sync(kFull, k1, 31 - lane));  // bitonic: the 32 smallest of both
+#pragma unroll
+      for (int j = 16; j > 0; j >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, k0, j);
+        k0 = (lane & j) ? umax64(k0, o) : umin64(k0, o);
+      }
+    }
+    if (lane < m) probes[row * probes_ld + lane] = (int32_t)key_id(k0);
+    SELCLK(4);
+    return;
+  }
+  if (MODE == 1) warp_topk_init(top, m);
+  for (int i0 = 0; i0 < total; i0 += 32) {
+    const int i = i0 + lane;
+    unsigned long long key = kPadKey;
+    if (i < total) {
+      const int l = all ? i : cand[i];
+      key = make_key(dist32_rows(xs, C + (size_t)l * Dp, D, vec), (uint32_t)l);
+    }
+    if (MODE == 0) bestk = umin64(bestk, key);
+    else warp_topk_insert(top, tmp, m, key);
+  }
+  if (MODE == 0) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) bestk = umin64(bestk, __shfl_xor_sync(kFull, bestk, off));
+    if (lane == 0) best[row] = bestk;
+  } else {
+    for (int j = lane; j < m; j += 32) probes[row * probes_ld + j] = (int32_t)key_id(top[j]);
+  }
+}
+
 struct Bound {
   float ka, kb;
 };
 
 Bound coarse_bound(int D, int Dp) {
   const double u = 0x1p-10, w = 0x1p-23;
-  const double e1 = 2.0 * (2.0 * u + u * u) + 2.0 * (Dp + 4) * w;
+  // split tf32: per product |err| <= 3 u^2 (1 + u) |x_k c_k| (x_h c_l, x_l c_h through one
+  // more tf32 conversion each, x_l c_l dropped); 3 Dp products accumulated in fp32
+  const double e1 = 2.0 * (3.0 * u * u + 4.0 * u * u * u) + 2.0 * (3 * Dp + 4) * w;
   const double e2 = (D + 6) * w, e3 = (D + 3) * w;
   const double ka = 2.0 * (1.0 + 2.0 * e3) * e1 + 4.0 * e3;
   const double kb = 2.0 * (1.0 + 2.0 * e3) * e2 + 2.0 * e3;
@@ -540,8 +872,44 @@ bool coarse_tc_supported(const Index& ix, int m) {
          4 * rerank_smem_per_warp(m, cap, ix.st.Dp) <= 48 * 1024;
 }
 
+typedef CUresult (*EncodeTiledFn2)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
 cudaError_t setup_coarse_tc(Index& ix) {
-  cudaError_t e = cudaFuncSetAttribute(k_coarse_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // TMA descriptor of the coarse matrix [coarse_rows][nlist] fp32 (store box 32 x 32, 128B swizzle)
+  ix.coarse_tmap_ok = false;
+  if ((ix.st.nlist & 3) == 0 && ix.sc.coarse_rows >= TM) {
+    EncodeTiledFn2 enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        enc) {
+      const cuuint64_t gdim[2] = {(cuuint64_t)ix.st.nlist, (cuuint64_t)ix.sc.coarse_rows};
+      const cuuint64_t gstr[1] = {(cuuint64_t)ix.st.nlist * 4};
+      const cuuint32_t box[2] = {32, 32};
+      const cuuint32_t estr[2] = {1, 1};
+      ix.coarse_tmap_ok =
+          enc(reinterpret_cast<CUtensorMap*>(ix.coarse_tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ix.sc.coarse, gdim,
+              gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  cudaError_t e = cudaFuncSetAttribute(k_coarse_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)coarse_smem_bytes(0));
+  {
+    const int sel = (int)select_smem(ix.st.Dp, 1024);  // nlist <= 1024 on this path
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_select<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_select<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_select<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_select<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_select<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_select<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel);
+  }
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_coarse_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)coarse_smem_bytes());
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_coarse_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -565,25 +933,67 @@ int coarse_tc_tile_cols() { return TN; }
 // assignment (m == 1) into best[i]; else probes[i * m + j].  Rows are
 // processed in chunks of sc.tc_rows.
 cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsigned long long* best,
-                             int32_t* probes, cudaStream_t s) {
+                             int32_t* probes, cudaStream_t s, bool need_dist) {
   Scratch& sc = ix.sc;
   const DevState& st = ix.st;
   const int D = st.D, Dp = st.Dp;
   const Bound bd = coarse_bound(D, Dp);
   // capacity per row: assignment calls (up to max(batch, queries) rows) get the small cap
   const int cap = probes == nullptr ? sc.cand_cap_assign : sc.cand_cap_probe;
+  const int ntn = (int)ceil_div(st.nlist, TN);
+  // Fast path: store A, then a per-row selection (k_coarse_select) — nlist <= 1024
+  // and chunks of >= 128 rows of the coarse scratch matrix.
+  const int64_t R = sc.tc_rows < sc.coarse_rows / TM * TM ? sc.tc_rows : sc.coarse_rows / TM * TM;
+  if (ix.coarse_select && ix.coarse_tmap_ok && st.nlist <= 1024 && R >= TM) {
+    const size_t ssm = select_smem(Dp, st.nlist);
+    for (int64_t r0 = 0; r0 < n; r0 += R) {
+      const int64_t nr = n - r0 < R ? n - r0 : R;
+      const float* xr = d_x + r0 * D;
+      const int64_t ntile = ceil_div(nr, TM);
+      k_rows_tiles<<<ntile, 4 * TM, 0, s>>>(xr, nr, D, Dp, sc.x_tiles, sc.x_norm);
+      // split the N-tiles over CTAs until every SM has a CTA
+      int ncg = ntile >= ix.num_sms ? 1 : (int)ceil_div(ix.num_sms, ntile);
+      if (ncg > ntn) ncg = ntn;
+      const int ntpc = (int)ceil_div(ntn, ncg);
+      CoarseArgs a{sc.x_tiles, sc.x_norm, sc.c_tiles, sc.c_norm, sc.c_csa, sc.c_cnb, nr, Dp, st.nlist, m, 0,
+                   bd.kb, nullptr, nullptr, nullptr, sc.coarse, ntpc};
+      k_coarse_gemm<0><<<dim3((unsigned)ntile, (unsigned)ceil_div(ntn, ntpc)), CTHREADS, coarse_smem_bytes(0), s>>>(
+          *reinterpret_cast<const CUtensorMap*>(ix.coarse_tmap), a);
+      const dim3 g((unsigned)ceil_div(nr, SELW));
+#define SIVF_SEL(NPL)                                                                                          \
+  if (probes == nullptr)                                                                                       \
+    k_coarse_select<NPL, 0><<<g, 32 * SELW, ssm, s>>>(sc.coarse, xr, nr, D, st.nlist, m, sc.x_norm, sc.c_csa,  \
+                                                       sc.c_cnb, bd.kb, st.centroids, Dp, best + r0, nullptr, 0,  \
+                                                       need_dist);                                                \
+  else                                                                                                         \
+    k_coarse_select<NPL, 1><<<g, 32 * SELW, ssm, s>>>(sc.coarse, xr, nr, D, st.nlist, m, sc.x_norm, sc.c_csa,  \
+                                                       sc.c_cnb, bd.kb, st.centroids, Dp, nullptr, probes + r0 * m, m, 1);
+      if (st.nlist <= 256) {
+        SIVF_SEL(8)
+      } else if (st.nlist <= 512) {
+        SIVF_SEL(16)
+      } else {
+        SIVF_SEL(32)
+      }
+#undef SIVF_SEL
+      ix.launches += 3;
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   const size_t rsm = 4 * rerank_smem_per_warp(m, cap, Dp);
   for (int64_t r0 = 0; r0 < n; r0 += sc.tc_rows) {
     const int64_t nr = n - r0 < sc.tc_rows ? n - r0 : sc.tc_rows;
     const float* xr = d_x + r0 * D;
     const int64_t ntile = ceil_div(nr, TM);
-    k_rows_tiles<<<ntile, TM, 0, s>>>(xr, nr, D, Dp, sc.x_tiles, sc.x_norm);
+    k_rows_tiles<<<ntile, 4 * TM, 0, s>>>(xr, nr, D, Dp, sc.x_tiles, sc.x_norm);
     CoarseArgs a{sc.x_tiles, sc.x_norm, sc.c_tiles, sc.c_norm, sc.c_csa, sc.c_cnb, nr, Dp, st.nlist, m, cap,
-                 bd.kb, sc.cand, sc.cand_ubv, sc.cand_cnt};
+                 bd.kb, sc.cand, sc.cand_ubv, sc.cand_cnt, nullptr, ntn};
     if (m == 1)
-      k_coarse_gemm<1><<<ntile, CTHREADS, coarse_smem_bytes(), s>>>(a);
+      k_coarse_gemm<1><<<ntile, CTHREADS, coarse_smem_bytes(), s>>>(*reinterpret_cast<const CUtensorMap*>(ix.coarse_tmap), a);
     else
-      k_coarse_gemm<32><<<ntile, CTHREADS, coarse_smem_bytes(), s>>>(a);
+      k_coarse_gemm<32><<<ntile, CTHREADS, coarse_smem_bytes(), s>>>(*reinterpret_cast<const CUtensorMap*>(ix.coarse_tmap), a);
     if (probes == nullptr)
       k_coarse_rerank<0><<<ceil_div(nr, 4), 128, rsm, s>>>(xr, nr, D, st.centroids, Dp, st.nlist, m, sc.cand,
                                                           sc.cand_ubv, sc.cand_cnt, cap, best + r0, nullptr, 0);
@@ -599,3 +1009,12 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
 }
 
 }  // namespace sivf
+
+#ifdef SIVF_TC_PROF
+extern "C" int sivf_debug_selhist(unsigned* host) {
+  return (int)cudaMemcpyFromSymbol(host, sivf::g_selhist, sizeof(unsigned) * 128);
+}
+extern "C" int sivf_debug_selclk(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, sivf::g_selclk, sizeof(unsigned long long) * 16);
+}
+#endif

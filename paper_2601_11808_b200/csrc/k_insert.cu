@@ -360,7 +360,7 @@ cudaError_t launch_insert(Index& ix, const int64_t* d_ids, const float* d_x, int
   k_claim<<<ceil_div(n, 256), 256, 0, s>>>(st, d_ids, n, sc.row_status, sc.row_lid);
   ix.launches += 1;
   }
-  cudaError_t e = launch_assign_exact(ix, d_x, n, s);
+  cudaError_t e = launch_assign_exact(ix, d_x, n, s, /*need_dist=*/false);  // the list is all insert needs
   if (e != cudaSuccess) return e;
   PhaseTimer pt(ix, SIVF_PH_APPEND, s);
   e = launch_stable_ranks(ix, n, 1, s);

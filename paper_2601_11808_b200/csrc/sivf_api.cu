@@ -58,8 +58,13 @@ Layout make_layout(const sivf_config* c) {
   L.max_chunks = (L.max_rows + 1023) / 1024;
   int64_t cr = ((int64_t)1 << 26) / nl;
   if (cr < 64) cr = 64;
-  L.coarse_rows = c->max_queries < cr ? c->max_queries : cr;
-  if (L.coarse_rows < 1) L.coarse_rows = 1;
+  {
+    // rows per coarse pass: a whole search batch or insert batch when it fits (whole 128-row tiles)
+    const int64_t want = c->max_queries > c->max_batch ? c->max_queries : c->max_batch;
+    L.coarse_rows = want < cr ? want : cr;
+    if (L.coarse_rows < 1) L.coarse_rows = 1;
+    L.coarse_rows = (L.coarse_rows + 127) / 128 * 128;
+  }
   const int64_t npairs = (int64_t)c->max_queries * c->max_nprobe;
   L.max_work = (npairs + 7) / 8 + 2 * nl + 1;
 
@@ -119,9 +124,9 @@ Layout make_layout(const sivf_config* c) {
   const int64_t cap_rows = L.tc_rows * L.cap_assign > (int64_t)c->max_queries * L.cap_probe
                                ? L.tc_rows * L.cap_assign
                                : (int64_t)c->max_queries * L.cap_probe;
-  L.x_tiles = take(L, (size_t)L.tc_rows * L.Dp * 4);
+  L.x_tiles = take(L, (size_t)2 * L.tc_rows * L.Dp * 4);  // hi and lo tf32 parts
   L.x_norm = take(L, (size_t)L.tc_rows * 4);
-  L.c_tiles = take(L, (size_t)nct * 256 * L.Dp * 4);
+  L.c_tiles = take(L, (size_t)2 * nct * 256 * L.Dp * 4);
   L.c_norm = take(L, (size_t)nct * 256 * 4);
   L.c_csa = take(L, (size_t)nct * 256 * 4);
   L.c_cnb = take(L, (size_t)nct * 256 * 4);
@@ -449,6 +454,7 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
     case SIVF_OPT_TC_SCAN: ix->use_tc_scan = value != 0; return SIVF_OK;
     case SIVF_OPT_TC_TWO_PHASE: ix->tc_two_phase = value != 0; return SIVF_OK;
     case SIVF_OPT_TC_COARSE: ix->use_tc_coarse = value != 0; return SIVF_OK;
+    case SIVF_OPT_COARSE_SELECT: ix->coarse_select = value != 0; return SIVF_OK;
     case SIVF_OPT_RANK_SPLIT: ix->rank_split = value != 0; return SIVF_OK;
     case 99: ix->dbg = (int)value; return SIVF_OK;  // SIVF_OPT_DEBUG: experiments only
     case SIVF_OPT_SEED_SLABS:

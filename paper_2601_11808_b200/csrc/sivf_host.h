@@ -30,7 +30,8 @@ struct Scratch {
   int32_t* list_newbase = nullptr;  // [nlist] index into free_stack of the list's first new slab
   int32_t* list_short = nullptr;    // [nlist] 1 if the list was not fully served
   // search (max_queries x max_nprobe)
-  float* coarse = nullptr;          // [coarse_rows][nlist]
+  float* coarse = nullptr;          // [coarse_rows][nlist] distance matrix (exact SIMT path) or the
+                                    // tensor-core approximation A (k_coarse_select path)
   int64_t coarse_rows = 0;
   int32_t* probes = nullptr;        // [max_queries][max_nprobe]
   int32_t* inv_cnt = nullptr;       // [2 nlist]   (probe-rank bucket, list)
@@ -81,6 +82,7 @@ struct Index {
   bool use_tc_scan = true;
   bool use_tc_coarse = true;  // tcgen05 coarse quantisation (k_coarse_tc.cu); false = exact SIMT k_dist_exact
   bool tc_two_phase = false;  // nearest-list-first scan phase (SIVF_OPT_TC_TWO_PHASE)  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
+  bool coarse_select = true;  // A-matrix + per-row selection coarse path (SIVF_OPT_COARSE_SELECT)
   bool rank_split = true;     // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT)
   int dbg = 0;                // experiment switches (SIVF_OPT_DEBUG)
   int seed_slabs = 8;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS)
@@ -90,6 +92,8 @@ struct Index {
   // of k_scan_tc (encoded once in setup_scan_tc; the payload never moves).
   alignas(64) unsigned char payload_tmap[128] = {};
   bool payload_tmap_ok = false;
+  alignas(64) unsigned char coarse_tmap[128] = {};  // TMA store descriptor of sc.coarse (k_coarse_tc.cu)
+  bool coarse_tmap_ok = false;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
   // phase profiling (sivf_profile_*)
@@ -145,7 +149,8 @@ cudaError_t launch_delete(Index& ix, const int64_t* d_ids, int64_t n, int64_t* d
 cudaError_t launch_reclaim(Index& ix, int64_t* d_nreclaimed, cudaStream_t s);
 cudaError_t launch_dump(Index& ix, int32_t* d_list_of_id, int64_t* d_live_per_list, int64_t* d_viol, cudaStream_t s);
 // k_coarse.cu (dispatch: tensor cores when supported, else exact SIMT)
-cudaError_t launch_assign_exact(Index& ix, const float* d_x, int64_t n, cudaStream_t s);  // -> sc.row_best
+// -> sc.row_best (list in the low word; the dist32 in the high word only when need_dist)
+cudaError_t launch_assign_exact(Index& ix, const float* d_x, int64_t n, cudaStream_t s, bool need_dist = true);
 cudaError_t launch_probe_exact(Index& ix, const float* d_q, int64_t nq, int32_t nprobe, cudaStream_t s); // -> sc.probes
 // k_coarse_tc.cu
 bool coarse_tc_supported(const Index& ix, int m);
@@ -154,7 +159,7 @@ cudaError_t refresh_centroid_tiles(Index& ix, cudaStream_t s);
 int coarse_tc_tile_rows();
 int coarse_tc_tile_cols();
 cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsigned long long* best,
-                             int32_t* probes, cudaStream_t s);
+                             int32_t* probes, cudaStream_t s, bool need_dist = true);
 // k_search.cu
 cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
                           int64_t* d_ids, int32_t* d_probes, cudaStream_t s);
