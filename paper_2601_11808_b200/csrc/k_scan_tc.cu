@@ -156,6 +156,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 
 #ifdef SIVF_TC_PROF
 __device__ long long g_tr[6][1024];
+__device__ unsigned long long g_scnt[4];  // slow-path entries, survivors, insertions, warp-level loop iterations
 #define TR(r, g, v) \
   do {              \
     if (blockIdx.x == 0 && (g) < 1024u) g_tr[r][g] = (v); \
@@ -579,15 +580,22 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
 #ifdef SIVF_TC_PROF
             long long _ts = clock64();
 #endif
+#ifdef SIVF_TC_PROF
+            atomicAdd(&g_scnt[0], 1ull);
+#endif
             uint32_t pm = 0u;
 #pragma unroll
             for (int c4 = 0; c4 < 8; ++c4) {
+              if (!(m8[c4] <= tadj)) continue;  // the quad's minimum already fails
               const float4 xx = x4[c4];
               pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 0]), xx.x) <= tadj ? 1u : 0u) << (4 * c4);
               pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 1]), xx.y) <= tadj ? 1u : 0u) << (4 * c4 + 1);
               pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 2]), xx.z) <= tadj ? 1u : 0u) << (4 * c4 + 2);
               pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 3]), xx.w) <= tadj ? 1u : 0u) << (4 * c4 + 3);
             }
+#ifdef SIVF_TC_PROF
+            atomicAdd(&g_scnt[1], (unsigned long long)__popc(pm));
+#endif
             while (pm) {
               const int c = __ffs(pm) - 1;
               pm &= pm - 1;
@@ -625,6 +633,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
               }
 #ifdef SIVF_TC_PROF
               pw[7]++;
+              atomicAdd(&g_scnt[2], 1ull);
 #endif
             }
 #ifdef SIVF_TC_PROF
@@ -758,6 +767,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+// register top-k width: the insertion network costs O(KP) per survivor
+inline int scan_kp(int k) { return k <= 12 ? 12 : k <= 16 ? 16 : 32; }
+
 int tc_stages(const Index& ix, int KP) {
   const size_t sb = tc_plan(ix.st.Dp, 0, KP).stage_bytes;
   const size_t fixed = tc_plan(ix.st.Dp, 0, KP).total;
@@ -769,7 +781,7 @@ int tc_stages(const Index& ix, int KP) {
 }  // namespace
 
 bool scan_tc_supported(const Index& ix, int k) {
-  return ix.st.Dp <= 128 && k <= 32 && ix.payload_tmap_ok && tc_stages(ix, k <= 16 ? 16 : 32) >= 2;
+  return ix.st.Dp <= 128 && k <= 32 && ix.payload_tmap_ok && tc_stages(ix, scan_kp(k)) >= 2;
 }
 
 cudaError_t setup_scan_tc(Index& ix) {
@@ -795,7 +807,10 @@ cudaError_t setup_scan_tc(Index& ix) {
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   ix.payload_tmap_ok = r == CUDA_SUCCESS;
   if (!ix.payload_tmap_ok) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_scan_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_scan_tc<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tc_plan(ix.st.Dp, tc_stages(ix, 12), 12).total);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_scan_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tc_plan(ix.st.Dp, tc_stages(ix, 16), 16).total);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_scan_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -805,12 +820,13 @@ cudaError_t setup_scan_tc(Index& ix) {
 
 cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s) {
   Scratch& sc = ix.sc;
-  const int KP = k <= 16 ? 16 : 32;
+  const int KP = scan_kp(k);
   const int nst = tc_stages(ix, KP);
   TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, ix.dbg};
   const size_t smem = tc_plan(ix.st.Dp, nst, KP).total;
   const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(ix.payload_tmap);
-  if (k <= 16) k_scan_tc<16><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);
+  if (KP == 12) k_scan_tc<12><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);
+  else if (KP == 16) k_scan_tc<16><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);
   else k_scan_tc<32><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);
   ix.launches += 1;
   return cudaGetLastError();
@@ -828,6 +844,14 @@ cudaError_t launch_seed_bound(Index& ix, const float* d_q, int64_t nq, int k, in
 }  // namespace sivf
 
 #ifdef SIVF_TC_PROF
+extern "C" int sivf_debug_scnt(unsigned long long* host, int reset) {
+  int rc = (int)cudaMemcpyFromSymbol(host, sivf::g_scnt, sizeof(unsigned long long) * 4);
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(sivf::g_scnt, z, sizeof(z));
+  }
+  return rc;
+}
 extern "C" int sivf_debug_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, sivf::g_tr, sizeof(long long) * 6 * 1024);
 }
