@@ -1,6 +1,7 @@
 # Build everything in-tree (the .so files travel to the GPU box with gpurun).
 #   make            -> datagen + oracle + libsivf
 #   make datagen    -> datagen/libsivfgen.so        (seeded input generator, host)
+#   make datagen_cuda -> datagen/libsivfgen_cuda.so (the same generator on the GPU; harness only)
 #   make oracle     -> oracle/libsivf_oracle.so     (CPU oracle: test infrastructure)
 #   make sivf       -> paper_2601_11808_b200/lib/libsivf.so (the product: sm_100a CUDA + C ABI)
 
@@ -17,14 +18,18 @@ HOSTFP    := -O2 -ffp-contract=off -fno-fast-math -fPIC
 SIVF_SRCS := $(wildcard $(CSRC)/*.cu)
 SIVF_HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/sivf.h
 
-all: datagen oracle sivf
+all: datagen datagen_cuda oracle sivf
 
 datagen: datagen/libsivfgen.so
+datagen_cuda: datagen/libsivfgen_cuda.so
 oracle: oracle/libsivf_oracle.so
 sivf: $(PKG)/lib/libsivf.so
 
 datagen/libsivfgen.so: datagen/datagen_host.c datagen/sivf_datagen.h
 	$(CC) $(HOSTFP) -std=c11 -shared -o $@ datagen/datagen_host.c -lpthread -lm
+
+datagen/libsivfgen_cuda.so: datagen/datagen_cuda.cu datagen/sivf_datagen.h
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -ffp-contract=off -fmad=false -shared -o $@ datagen/datagen_cuda.cu
 
 oracle/libsivf_oracle.so: oracle/sivf_oracle.cpp oracle/sivf_oracle.h
 	$(CXX) $(HOSTFP) -std=c++17 -shared -o $@ oracle/sivf_oracle.cpp
@@ -34,6 +39,6 @@ $(PKG)/lib/libsivf.so: $(SIVF_SRCS) $(SIVF_HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SIVF_SRCS) 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
 
 clean:
-	rm -f datagen/libsivfgen.so oracle/libsivf_oracle.so $(PKG)/lib/libsivf.so
+	rm -f datagen/libsivfgen.so datagen/libsivfgen_cuda.so oracle/libsivf_oracle.so $(PKG)/lib/libsivf.so
 
-.PHONY: all datagen oracle sivf clean
+.PHONY: all datagen datagen_cuda oracle sivf clean

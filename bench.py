@@ -50,10 +50,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="sivf", choices=["sivf", "reference"])
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the sliding-window (W) and GIST (G) legs")
+    ap.add_argument("--no-extra", action="store_true", help="skip the sliding-window (W), GIST (G) and H legs")
     ap.add_argument("--window-steps", type=int, default=1000)
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run only N steps, no extras")
+    ap.add_argument("--h-n", type=int, default=100_000_000, help="vectors of the id-sharded H leg (0: skip)")
     return ap.parse_args()
 
 
@@ -520,6 +521,8 @@ def run_sivf(args):
         torch.cuda.empty_cache()
         line["configs"]["G_gist1m"] = leg_gist(S, dev, log)
         torch.cuda.empty_cache()
+    if not args.no_extra and args.h_n > 0:
+        line.setdefault("configs", {})["H_sharded"] = leg_h(S, dev, log, G, rank, pg, args.h_n)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if pg is not None:
@@ -692,6 +695,150 @@ def leg_gist(S, dev, log):
            "train_s": t_train, "overhead_paper": st["overhead_paper"], "overhead_actual": st["overhead_actual"]}
     log(f"gist: delete p50 {res['delete_10k_ms_p50']:.4f} ms, insert10k {res['insert_10k_ms_p50']:.3f} ms, "
         f"qps@32 {sweep[32]['qps']:.0f} r={sweep[32]['recall10']:.3f}")
+    return res
+
+
+def leg_h(S, dev, log, G, rank, pg, n_total):
+    """BASELINE configs[4]: id-sharded SIFT-shaped n_total x 128 (default 100M), nlist=16384, owner(id) =
+    id mod G.  Vectors are generated on the device (datagen.DeviceGenerator, bit-identical to the host
+    generator).  Reports the build rate, routed 80k-id mutation batches (no collective) and search of
+    10k broadcast queries: local search -> NCCL all-gather of the per-shard top-k -> sivf_merge_topk,
+    timed on the device as the max over ranks; recall@10 on 100 queries against an exact top-10 kept
+    while building (fp32 GEMM over every generated batch, merged across ranks)."""
+    import torch
+
+    from datagen import TRAIN_BASE, QUERY_BASE, DeviceGenerator, sift_shape
+
+    NLH, NQH, NGT, MB = 16384, NQ, 100, 80_000
+    gen = DeviceGenerator(sift_shape(seed=0x100A))
+    local_n = len(range(rank, n_total, G))
+    cap = n_total + MB + 64
+    ix = S.Index(DIM, NLH, cap, S.num_slabs_for(local_n + MB // G + 1, NLH), max_batch=1 << 20, max_queries=NQH,
+                 max_k=K, max_nprobe=128, max_train=1 << 20, shard_rank=rank, shard_count=G, seed=0x100A, device=dev)
+
+    def dmax(ms):
+        if pg is None:
+            return ms
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    t0 = time.time()
+    Xt = torch.empty(1 << 20, DIM, dtype=torch.float32, device=dev)
+    gen.range_into(Xt, TRAIN_BASE, 1)  # identical sample on every rank
+    ix.train(Xt, niter=N_ITER)
+    if pg is not None:
+        C = ix.get_centroids()
+        pg.broadcast(C, src=0)
+        ix.set_centroids(C)
+    torch.cuda.synchronize()
+    t_train = time.time() - t0
+    del Xt
+    Qg = torch.empty(NQH, DIM, dtype=torch.float32, device=dev)
+    gen.range_into(Qg, QUERY_BASE, 1)
+    Qs = Qg[:NGT]
+    qn = (Qs * Qs).sum(1)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    gt_d = torch.full((NGT, 10), float("inf"), device=dev)
+    gt_i = torch.full((NGT, 10), -1, dtype=torch.int64, device=dev)
+    B = 1 << 20
+    Xb = torch.empty(B, DIM, dtype=torch.float32, device=dev)
+    ins_ms = 0.0
+    t0 = time.time()
+    for j0 in range(0, local_n, B):
+        nb = min(B, local_n - j0)
+        gen.range_into(Xb[:nb], rank + j0 * G, G)
+        ids = rank + G * torch.arange(j0, j0 + nb, device=dev, dtype=torch.int64)
+        a, b = _ev(), _ev()
+        a.record()
+        ix.insert(ids, Xb[:nb])
+        b.record()
+        x = Xb[:nb]
+        d = qn[:, None] + (x * x).sum(1)[None, :] - 2.0 * (Qs @ x.T)
+        dd, ii = torch.topk(torch.cat([gt_d, d], 1), 10, dim=1, largest=False)
+        gt_i = torch.gather(torch.cat([gt_i, ids[None, :].expand(NGT, -1)], 1), 1, ii)
+        gt_d = dd
+        b.synchronize()
+        ins_ms += a.elapsed_time(b)
+    torch.cuda.synchronize()
+    t_build = time.time() - t0
+    build_rate = n_total / (dmax(ins_ms) / 1e3)
+    del Xb
+    if pg is not None:
+        ad = [torch.empty_like(gt_d) for _ in range(G)]
+        ai = [torch.empty_like(gt_i) for _ in range(G)]
+        pg.all_gather(ad, gt_d)
+        pg.all_gather(ai, gt_i)
+        dd, ii = torch.topk(torch.cat(ad, 1), 10, dim=1, largest=False)
+        gt_i = torch.gather(torch.cat(ai, 1), 1, ii)
+    gt = gt_i.cpu().numpy()
+    st = ix.stats()
+    assert st["live"] == local_n and st["device_errors"] == 0, st
+    log(f"H: train {t_train:.1f}s build {t_build:.1f}s ({build_rate / 1e6:.1f} M/s device-timed)")
+
+    gd = torch.empty(G, NQH, K, dtype=torch.float32, device=dev)
+    gi = torch.empty(G, NQH, K, dtype=torch.int64, device=dev)
+
+    def search(npb):
+        d, i = ix.search(Qg, K, npb)
+        if pg is not None:
+            pg.all_gather_into_tensor(gd.view(-1), d.reshape(-1))
+            pg.all_gather_into_tensor(gi.view(-1), i.reshape(-1))
+            d, i = S.merge_topk(gd, gi)
+        return d, i
+
+    sweep, qps_at_09, np_at_09 = {}, None, None
+    for npb in (8, 16, 32, 64):
+        search(npb)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(3):
+            if pg is not None:
+                pg.barrier()
+            a, b = _ev(), _ev()
+            a.record()
+            _, ii = search(npb)
+            b.record()
+            torch.cuda.synchronize()
+            times.append(dmax(a.elapsed_time(b)))
+        res = ii[:NGT, :10].cpu().numpy()
+        rec = float(np.mean([len(set(r) & set(g)) / 10 for r, g in zip(res, gt)]))
+        ms = statistics.median(times)
+        sweep[npb] = {"recall10": rec, "qps": NQH / (ms / 1e3), "ms": ms}
+        if qps_at_09 is None and rec >= 0.9:
+            qps_at_09, np_at_09 = NQH / (ms / 1e3), npb
+    # routed mutations: a global batch of 80k random live ids deleted and 80k new ids inserted
+    rng = np.random.default_rng(0x100A)
+    dids = rng.choice(n_total, MB, replace=False).astype(np.int64)
+    nids = np.arange(n_total, n_total + MB, dtype=np.int64)
+    dl = torch.from_numpy(dids[dids % G == rank]).to(dev)
+    nl = torch.from_numpy(nids[nids % G == rank]).to(dev)
+    Xn = torch.empty(nl.shape[0], DIM, dtype=torch.float32, device=dev)
+    gen.range_into(Xn, n_total + rank, G)
+    if pg is not None:
+        pg.barrier()
+    a, b, c = _ev(), _ev(), _ev()
+    a.record()
+    nd = ix.delete(dl)
+    b.record()
+    ix.insert(nl, Xn)
+    c.record()
+    torch.cuda.synchronize()
+    del_ms, ins80_ms = dmax(a.elapsed_time(b)), dmax(b.elapsed_time(c))
+    st = ix.stats()
+    assert st["live"] == local_n and st["device_errors"] == 0, st
+    res = {"workload": f"BASELINE configs[4]: id-sharded SIFT-shaped {n_total // 1_000_000}M x 128, nlist=16384, "
+                       f"G={G} (owner = id mod G), 10k broadcast queries k=10, per-shard top-k all-gather + merge",
+           "n_total": n_total, "gpus": G, "build_inserts_per_s": build_rate, "train_s": t_train,
+           "deletes_per_s_80k_routed": MB / (del_ms / 1e3), "inserts_per_s_80k_routed": MB / (ins80_ms / 1e3),
+           "delete_80k_ms": del_ms, "insert_80k_ms": ins80_ms,
+           "qps_nprobe32": sweep[32]["qps"], "recall10_nprobe32": sweep[32]["recall10"],
+           "qps_at_recall10_0.9": qps_at_09, "nprobe_at_recall10_0.9": np_at_09, "sweep": sweep,
+           "recall_truth": f"exact top-10 of {NGT} queries (fp32 GEMM over every generated batch)",
+           "scaling": "strong (the global index is fixed; each rank holds n/G)"}
+    log(f"H: qps@32 {sweep[32]['qps']:.0f} r={sweep[32]['recall10']:.3f}; delete80k {del_ms:.3f} ms")
+    del ix
+    torch.cuda.empty_cache()
     return res
 
 

@@ -132,6 +132,45 @@ class Generator:
         return self.range(TRAIN_BASE, n)
 
 
+class DeviceGenerator:
+    """The same (seed, g) -> vector map evaluated on the GPU (libsivfgen_cuda.so;
+    harness code).  Outputs are bit-identical to Generator (tests/test_datagen.py)."""
+
+    def __init__(self, shape: Shape):
+        path = os.path.join(_HERE, "libsivfgen_cuda.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `make -C {os.path.dirname(_HERE)} datagen_cuda`")
+        self._L = ctypes.CDLL(path)
+        self._L.sivfgen_cuda_model_new.restype = ctypes.c_void_p
+        self._L.sivfgen_cuda_model_new.argtypes = [ctypes.POINTER(_Params)]
+        self._L.sivfgen_cuda_model_free.argtypes = [ctypes.c_void_p]
+        self._L.sivfgen_cuda_range.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
+                                               ctypes.c_void_p, ctypes.c_void_p]
+        self.shape = shape
+        self._p = shape._params()
+        self._m = self._L.sivfgen_cuda_model_new(ctypes.byref(self._p))
+        if not self._m:
+            raise RuntimeError("sivfgen_cuda_model_new failed")
+
+    def __del__(self):
+        try:
+            if self._m:
+                self._L.sivfgen_cuda_model_free(self._m)
+        except Exception:
+            pass
+
+    def range_into(self, out, g0: int, gstride: int = 1, stream=None):
+        """out: a CUDA float32 tensor [n][dim]; row i = vector(g0 + i * gstride)."""
+        import torch
+
+        assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.shape[1] == self.shape.dim
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        rc = self._L.sivfgen_cuda_range(self._m, g0, gstride, out.shape[0], out.data_ptr(), st)
+        if rc != 0:
+            raise RuntimeError(f"sivfgen_cuda_range: CUDA error {rc}")
+        return out
+
+
 def mix64(z: int) -> int:
     return int(lib().sivfgen_mix64_x(z))
 

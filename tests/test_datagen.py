@@ -2,6 +2,7 @@
 import os
 
 import numpy as np
+import pytest
 
 import datagen as G
 
@@ -44,3 +45,16 @@ def test_delete_order_is_permutation():
     live = np.arange(1000, 1100)
     p = G.delete_order(1, 3, live)
     assert sorted(p.tolist()) == live.tolist() and not np.array_equal(p, live)
+
+
+@pytest.mark.gpu
+def test_device_generator_bit_identical():
+    import torch
+
+    for shape in (G.sift_shape(seed=0x100A), G.gist_shape(dim=960)):
+        host = G.Generator(shape)
+        dev = G.DeviceGenerator(shape)
+        out = torch.empty(300, shape.dim, dtype=torch.float32, device="cuda")
+        dev.range_into(out, 12345, 3)  # ids 12345 + 3 i (rank-local ids of an id-sharded index)
+        ref = host.take(12345 + 3 * np.arange(300))
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
