@@ -80,6 +80,7 @@ struct TcArgs {
   unsigned long long* partial;
   uint32_t* gthr;
   int dbg;  // experiments only (SIVF_OPT_DEBUG): bit0 skip the slow path, bit1 skip the fast path
+  int copy_mode;  // 0: TMA tile::gather4 builds the B operand; 1: cp.async by the 4 loader warps
 };
 
 struct ItemRec {
@@ -114,7 +115,7 @@ struct TcPlan {
 };
 __host__ __device__ inline TcPlan tc_plan(int Dp, int nst, int KP) {
   TcPlan p;
-  p.stage_bytes = ((size_t)GN * Dp * 4 + 1023) & ~(size_t)1023;
+  p.stage_bytes = ((size_t)GN * Dp * 4 + 2 * GN * 4 + 1023) & ~(size_t)1023;  // payload + slot norms + ids
   p.off_meta = (size_t)nst * p.stage_bytes;
   p.off_gm = p.off_meta + MAXST * sizeof(StageMeta);
   p.off_q = p.off_gm + 2 * sizeof(GroupMeta);
@@ -203,6 +204,12 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
   uint64_t* item_empty = item_full + NITEM;                        // [NITEM] epilogue -> scheduler
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(item_empty + NITEM);
   auto stage_x = [&](int s) { return reinterpret_cast<float*>(smem + (size_t)s * p.stage_bytes); };
+  auto stage_nrm = [&](int s) {
+    return reinterpret_cast<float*>(smem + (size_t)s * p.stage_bytes + (size_t)GN * Dp * 4);
+  };
+  auto stage_id = [&](int s) {
+    return reinterpret_cast<uint32_t*>(smem + (size_t)s * p.stage_bytes + (size_t)GN * Dp * 4 + GN * 4);
+  };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef SIVF_TC_PROF
   long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
 #endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < MAXST; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], a.copy_mode ? 32 * NLD : 1);
       mbar_init(&empty[i], 1);
       mbar_init(&meta_full[i], 1);
     }
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     const unsigned lt = (1u << lane) - 1u;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      if (lane == 0) PW(0, mbar_wait_sleep(&item_empty[slot], ((i / NITEM) & 1u) ^ 1u));
+      if (lane == 0) PW(0, mbar_wait(&item_empty[slot], ((i / NITEM) & 1u) ^ 1u));
       int w = 0;
       if (lane == 0) w = atomicAdd(&st.ictr[I_WORK], 1);
       w = __shfl_sync(kFull, w, 0);
@@ -287,7 +294,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     uint32_t my_bm = 0u, my_fl = 0u;
     auto emit = [&](int base, int nvalid, int last) {
       const int stg = (int)(gseq % (uint32_t)nst);
-      if (lane == 0) PW(1, mbar_wait_sleep(&empty[stg], ((gseq / (uint32_t)nst) & 1u) ^ 1u));
+      if (lane == 0) PW(1, mbar_wait(&empty[stg], ((gseq / (uint32_t)nst) & 1u) ^ 1u));
       if (lane == 0) TR(0, gseq, clock64());
       __syncwarp();
       const int sl = __shfl_sync(kFull, my_s, base + (lane & 3));
@@ -308,10 +315,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&meta_full[stg]);  // the MMA warp fetches the slot norms while the payload is in flight
-        mbar_arrive_expect_tx(&full[stg], (uint32_t)nq4 * 2048u);
+        if (!a.copy_mode) mbar_arrive_expect_tx(&full[stg], (uint32_t)nq4 * 2048u);
       }
       __syncwarp();
-      if (lane < nq4)
+      if (!a.copy_mode && lane < nq4)
         tma_gather4(stage_x(stg) + lane * 512, &tmap, 0, sj[0] * nq4 + lane, sj[1] * nq4 + lane,
                     sj[2] * nq4 + lane, sj[3] * nq4 + lane, &full[stg]);
       ++gseq;
@@ -340,7 +347,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     };
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      mbar_wait_sleep(&item_full[slot], (i / NITEM) & 1u);
+      mbar_wait(&item_full[slot], (i / NITEM) & 1u);
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       cnt = 0;
@@ -384,27 +391,36 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     uint32_t gseq = 0;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      mbar_wait_sleep(&item_full[slot], (i / NITEM) & 1u);
+      mbar_wait(&item_full[slot], (i / NITEM) & 1u);
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       const uint32_t ab = i & 1u;
-      PW(1, mbar_wait_sleep(&a_full[ab], (i >> 1) & 1u));
+      PW(1, mbar_wait(&a_full[ab], (i >> 1) & 1u));
       for (;;) {
         const int stg = (int)(gseq % (uint32_t)nst);
         const uint32_t b = gseq & 1u;
-        mbar_wait_sleep(&meta_full[stg], (gseq / (uint32_t)nst) & 1u);
+        mbar_wait(&meta_full[stg], (gseq / (uint32_t)nst) & 1u);
         const StageMeta& sm = smeta[stg];
         float xnv[GS];
         uint32_t idv[GS];
+        if (!a.copy_mode) {
 #pragma unroll
-        for (int j = 0; j < GS; ++j) {  // slot norms and ids: their latency hides behind the payload's
-          const size_t o = (size_t)(sm.slab[j] >= 0 ? sm.slab[j] : 0) * kSlot + lane;
-          xnv[j] = __ldg(st.slab_norm + o);
-          idv[j] = __ldg(st.slab_ids + o);
+          for (int j = 0; j < GS; ++j) {  // slot norms and ids: their latency hides behind the payload's
+            const size_t o = (size_t)(sm.slab[j] >= 0 ? sm.slab[j] : 0) * kSlot + lane;
+            xnv[j] = __ldg(st.slab_norm + o);
+            idv[j] = __ldg(st.slab_ids + o);
+          }
         }
-        PW(2, mbar_wait_sleep(&full[stg], (gseq / (uint32_t)nst) & 1u));
+        PW(2, mbar_wait(&full[stg], (gseq / (uint32_t)nst) & 1u));
         if (lane == 0) TR(1, gseq, clock64());
-        PW(3, mbar_wait_sleep(&grp_free[b], ((gseq >> 1) & 1u) ^ 1u));
+        if (a.copy_mode) {  // staged with the payload by the copy warps
+#pragma unroll
+          for (int j = 0; j < GS; ++j) {
+            xnv[j] = stage_nrm(stg)[j * kSlot + lane];
+            idv[j] = stage_id(stg)[j * kSlot + lane];
+          }
+        }
+        PW(3, mbar_wait(&grp_free[b], ((gseq >> 1) & 1u) ^ 1u));
         if (lane == 0) TR(2, gseq, clock64());
         GroupMeta& g = gm[b];
 #pragma unroll
@@ -425,6 +441,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
         __syncwarp();
         if (lane == 0) {
           tc_fence_after();
+          if (a.copy_mode) fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05.mma (async proxy)
           const uint32_t bsm = smem_u32(stage_x(stg));
           const uint32_t dt = tbase + 256u + b * 128u, at = tbase + ab * 128u;
           for (int kk = 0; kk < ((a.dbg & 4) ? 0 : (Dp >> 3)); ++kk)
@@ -449,9 +466,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     const int qw = warp & 3, row = 32 * qw + lane;
     const bool vec = (st.D & 3) == 0;
     const int nc8 = Dp >> 3;
+    uint32_t cseq = 0;  // group sequence (copy mode)
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      mbar_wait_sleep(&item_full[slot], (i / NITEM) & 1u);
+      mbar_wait(&item_full[slot], (i / NITEM) & 1u);
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       const uint32_t ab = i & 1u;
@@ -483,7 +501,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
           for (int e = 0; e < 8; ++e) v[u][e] = __float_as_uint(x[e]);
         }
         if (h0 == 0) {
-          PW(4, mbar_wait_sleep(&a_free[ab], ((i >> 1) & 1u) ^ 1u));
+          PW(4, mbar_wait(&a_free[ab], ((i >> 1) & 1u) ^ 1u));
           tc_fence_after();
         }
 #pragma unroll
@@ -511,6 +529,38 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_full[ab]);
+      if (a.copy_mode) {
+        // B operand of this item's groups: warp qw copies group position qw (one slab),
+        // lane = slot, one 16-B cp.async per 4 dims into the interleaved layout
+        // [Dp/4][4 slabs][32 slots][4]; completion arrives on full[stg] (no tx count)
+        for (;;) {
+          const int stg = (int)(cseq % (uint32_t)nst);
+          mbar_wait(&meta_full[stg], (cseq / (uint32_t)nst) & 1u);
+          const StageMeta& sm = smeta[stg];
+          const int sl = sm.slab[qw];
+          const int last = sm.last;
+          if (sl >= 0) {
+            const float* src = st.payload + (size_t)sl * kSlot * Dp + lane * 4;
+            const uint32_t dst = smem_u32(stage_x(stg)) + (uint32_t)(qw * 512 + lane * 16);
+#pragma unroll 8
+            for (int c4 = 0; c4 < nq4; ++c4)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (uint32_t)c4 * 2048u),
+                           "l"(src + (size_t)c4 * 128)
+                           : "memory");
+            if (lane < 16) {  // the slab's 32 slot norms (lanes 0-7) and ids (lanes 8-15)
+              const uint32_t nd = lane < 8 ? smem_u32(stage_nrm(stg) + qw * kSlot + 4 * lane)
+                                           : smem_u32(stage_id(stg) + qw * kSlot + 4 * (lane - 8));
+              const void* ns = lane < 8 ? (const void*)(st.slab_norm + (size_t)sl * kSlot + 4 * lane)
+                                        : (const void*)(st.slab_ids + (size_t)sl * kSlot + 4 * (lane - 8));
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(nd), "l"(ns) : "memory");
+            }
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[stg]))
+                       : "memory");
+          ++cseq;
+          if (last) break;
+        }
+      }
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -523,11 +573,11 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     uint32_t gseq = 0;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      mbar_wait_sleep(&item_full[slot], (i / NITEM) & 1u);
+      mbar_wait(&item_full[slot], (i / NITEM) & 1u);
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       const uint32_t ab = i & 1u;
-      PW(1, mbar_wait_sleep(&a_full[ab], (i >> 1) & 1u));
+      PW(1, mbar_wait(&a_full[ab], (i >> 1) & 1u));
       const QInfo qi = qinfo[ab * TM + row];
       const bool rv = row < rec.nqt;
       const bool wact = 32 * qw < rec.nqt;
@@ -541,7 +591,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
       u64 kth = kPadKey;
       for (;;) {
         const uint32_t b = gseq & 1u;
-        PW(5, mbar_wait_sleep(&d_full[b], (gseq >> 1) & 1u));
+        PW(5, mbar_wait(&d_full[b], (gseq >> 1) & 1u));
         if (lane == 0 && warp == W_EPI0 + 2) TR(3, gseq, clock64());
         if (lane == 0 && warp == W_EPI0 + 6) TR(5, gseq, clock64());
         tc_fence_after();
@@ -822,7 +872,8 @@ cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaS
   Scratch& sc = ix.sc;
   const int KP = scan_kp(k);
   const int nst = tc_stages(ix, KP);
-  TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, ix.dbg};
+  TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, ix.dbg,
+            ix.scan_copy_mode};
   const size_t smem = tc_plan(ix.st.Dp, nst, KP).total;
   const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(ix.payload_tmap);
   if (KP == 12) k_scan_tc<12><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);

@@ -89,25 +89,26 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
 
 // one warp per CTA copies each group with cp.async (16 B per lane, L2-only),
 // writing the interleaved layout directly: lane = slot, dst = c4*2048 + j*512 + slot*16
-__global__ void __launch_bounds__(64, 1) k_stream_cpasync(const float* payload, int nslabs, int ngroups, int nst,
-                                                        unsigned* sink) {
+template <int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1) k_stream_cpasync(const float* payload, int nslabs, int ngroups,
+                                                                  int nst, unsigned* sink) {
   extern __shared__ __align__(1024) unsigned char smem[];
   float* st = reinterpret_cast<float*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nst * GB);
   uint64_t* empty = full + nst;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < nst; ++i) { mbar_init(&full[i], 32); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < nst; ++i) { mbar_init(&full[i], 32 * NW); mbar_init(&empty[i], 1); }
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == 0) {
+  if (warp < NW) {
     for (int g = 0; g < ngroups; ++g) {
       const int s = g % nst;
       mbar_wait(&empty[s], ((g / nst) & 1u) ^ 1u);
       const uint32_t dst = smem_u32(st + (size_t)s * (GB / 4));
 #pragma unroll 1
-      for (int j = 0; j < 4; ++j) {
+      for (int j = warp; j < 4; j += NW) {
         const int sl = (int)(((unsigned)(blockIdx.x * 7919 + g * 4 + j) * 2654435761u) % (unsigned)nslabs);
         const float* src = payload + (size_t)sl * 4096 + lane * 4;
 #pragma unroll 8
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(64, 1) k_stream_cpasync(const float* payload, 
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
     }
-  } else if (warp == 1) {
+  } else if (warp == NW) {
     unsigned acc = 0;
     for (int g = 0; g < ngroups; ++g) {
       const int s = g % nst;
@@ -178,9 +179,11 @@ int main() {
       const size_t sm = (size_t)nst * GB + 256;
       cudaFuncSetAttribute(k_stream<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       cudaFuncSetAttribute(k_stream<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      cudaFuncSetAttribute(k_stream_cpasync, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(k_stream_cpasync<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(k_stream_cpasync<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(k_stream_cpasync<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       const int ng = 200;
-      for (int gather = 0; gather < 3; ++gather) {
+      for (int gather = 0; gather < 5; ++gather) {
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
@@ -188,14 +191,16 @@ int main() {
           cudaEventRecord(a);
           if (gather == 1) k_stream<true><<<148, 64, sm>>>(tm, d, ns, ng, nst, sink);
           else if (gather == 0) k_stream<false><<<148, 64, sm>>>(tm, d, ns, ng, nst, sink);
-          else k_stream_cpasync<<<148, 64, sm>>>(d, ns, ng, nst, sink);
+          else if (gather == 2) k_stream_cpasync<1><<<148, 64, sm>>>(d, ns, ng, nst, sink);
+          else if (gather == 3) k_stream_cpasync<2><<<148, 96, sm>>>(d, ns, ng, nst, sink);
+          else k_stream_cpasync<4><<<148, 160, sm>>>(d, ns, ng, nst, sink);
           cudaEventRecord(b);
           cudaEventSynchronize(b);
           float ms;
           cudaEventElapsedTime(&ms, a, b);
           if (rep == 2)
             printf("  nst %d slabs %d %s: %.3f ms  %.0f GB/s  (err %s)\n", nst, ns,
-                   gather == 1 ? "gather4" : gather == 0 ? "bulk16K" : "cpasync", ms,
+                   gather == 1 ? "gather4" : gather == 0 ? "bulk16K" : gather == 2 ? "cpasync1w" : gather == 3 ? "cpasync2w" : "cpasync4w", ms,
                    148.0 * ng * GB / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
         }
       }
