@@ -200,7 +200,7 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
  *                      on tcgen05 tensor cores with a certified band and exact
  *                      dist32 re-rank (bit-identical result); 0 = exact CUDA-core
  *                      distance matrix.
- *   SIVF_OPT_SEED_SLABS (default 8): before the tensor-core scan, each query's
+ *   SIVF_OPT_SEED_SLABS (default 0): before the tensor-core scan, each query's
  *                      bound on its k-th distance is seeded with exact distances
  *                      to the first `value` live slabs of its nearest probed list
  *                      (any k real candidates bound the final k-th distance from

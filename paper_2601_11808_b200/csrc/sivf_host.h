@@ -86,7 +86,7 @@ struct Index {
   bool rank_split = true;     // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT)
   int scan_copy_mode = 0;     // k_scan_tc B operand: 0 TMA gather4 (default), 1 cp.async by the loader warps
   int dbg = 0;                // experiment switches (SIVF_OPT_DEBUG)
-  int seed_slabs = 8;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS)
+  int seed_slabs = 0;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS; off: it costs more than it saves)
   int64_t launches = 0;
   // TMA descriptor (CUtensorMap, 128 B) of the payload viewed as rows of 512 B
   // (row = slab * Dp/4 + c4), box 128 floats x 1 row: the tile::gather4 source

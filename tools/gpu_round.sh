@@ -17,12 +17,12 @@ for w in $WHAT; do
       echo "bench rc=$?"; tail -c 1500 gpurun_out/${TAG}_bench.json; tail -5 gpurun_out/${TAG}_bench.err ;;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
-        --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-sweep --no-cpu \
+        --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-sweep --no-cpu --no-extra \
         > gpurun_out/${TAG}_launches_bench.json 2> gpurun_out/${TAG}_launches.err
       echo "launches rc=$?" ;;
     full)
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_scan -s 1 -c 1 \
-        -o gpurun_out/${TAG}_scan python bench.py --steps 1 --warmup 1 --no-sweep --no-cpu \
+        -o gpurun_out/${TAG}_scan python bench.py --steps 1 --warmup 1 --no-sweep --no-cpu --no-extra \
         > gpurun_out/${TAG}_full_bench.json 2> gpurun_out/${TAG}_full.err
       echo "full rc=$?" ;;
   esac
