@@ -661,7 +661,7 @@ __host__ __device__ inline size_t select_smem(int Dp, int nlist) {
   return SELW * select_smem_per_warp(Dp) + (size_t)2 * nlist * 4;
 }
 template <int NPL, int MODE>
-__global__ void __launch_bounds__(32 * SELW) k_coarse_select(const float* __restrict__ mat,
+__global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __restrict__ mat,
                                                              const float* __restrict__ X, int64_t n, int D,
                                                              int nlist, int m, const float* __restrict__ xnorm,
                                                              const float* __restrict__ ccsa,
@@ -696,19 +696,13 @@ __global__ void __launch_bounds__(32 * SELW) k_coarse_select(const float* __rest
 #pragma unroll
   for (int i = 0; i < NPL; ++i) A[i] = lane + 32 * i < nlist ? __ldcs(arow + lane + 32 * i) : INFINITY;
   const float qn = xnorm[row], sq = sqrtf(qn), qnb = kb * qn;
-  float lbv[NPL];
-  uint32_t ubb[NPL];
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) {
+  // the certified half-width E of column lane + 32 i (recomputed where needed: keeping
+  // only A in registers doubles the resident warps of this latency-bound kernel)
+  auto Eat = [&](int i) {
     const int c = lane + 32 * i;
-    lbv[i] = INFINITY;
-    ubb[i] = 0x7F800000u;
-    if (c < nlist) {
-      const float E = fmaf(sq, csa_s[c], qnb + cnb_s[c]);
-      lbv[i] = A[i] - E;
-      ubb[i] = __float_as_uint(fmaxf(A[i] + E, 0.f));
-    }
-  }
+    return c < nlist ? fmaf(sq, csa_s[c], qnb + cnb_s[c]) : 0.f;
+  };
+  auto ubat = [&](int i) { return __float_as_uint(fmaxf(A[i] + Eat(i), 0.f)); };  // +inf beyond nlist
   const float* xr = X + row * (int64_t)D;
   for (int k = lane; k < Dp; k += 32) xs[k] = k < D ? __ldg(xr + k) : 0.f;
   SELCLK(0);
@@ -716,7 +710,7 @@ __global__ void __launch_bounds__(32 * SELW) k_coarse_select(const float* __rest
   if (MODE == 0 || m == 1) {
     uint32_t mn = 0x7F800000u;
 #pragma unroll
-    for (int i = 0; i < NPL; ++i) mn = min(mn, ubb[i]);
+    for (int i = 0; i < NPL; ++i) mn = min(mn, ubat(i));
     Ub = __reduce_min_sync(kFull, mn);
   } else {
     // hi = the largest of the lanes' minima: >= 32 >= m upper bounds are <= hi, so
@@ -724,7 +718,7 @@ __global__ void __launch_bounds__(32 * SELW) k_coarse_select(const float* __rest
     // m-th smallest found by bisection on the fp32 bit pattern
     uint32_t mn = 0x7F800000u;
 #pragma unroll
-    for (int i = 0; i < NPL; ++i) mn = min(mn, ubb[i]);
+    for (int i = 0; i < NPL; ++i) mn = min(mn, ubat(i));
     uint32_t hi = m <= 32 ? __reduce_max_sync(kFull, mn) : 0x7F800000u;
     uint32_t lo = __reduce_min_sync(kFull, mn);
     uint32_t* sv = reinterpret_cast<uint32_t*>(cand);  // scratch, reused for candidates below
@@ -732,10 +726,11 @@ __global__ void __launch_bounds__(32 * SELW) k_coarse_select(const float* __rest
     const unsigned ltm = (1u << lane) - 1u;
 #pragma unroll
     for (int i = 0; i < NPL; ++i) {
-      const bool keep = ubb[i] <= hi;
+      const uint32_t ub = ubat(i);
+      const bool keep = ub <= hi;
       const unsigned pm = __ballot_sync(kFull, keep);
       const int pos = ns + __popc(pm & ltm);
-      if (keep && pos < CCAP) sv[pos] = ubb[i];
+      if (keep && pos < CCAP) sv[pos] = ub;
       ns += __popc(pm);
     }
     __syncwarp();
@@ -756,7 +751,7 @@ __global__ void __launch_bounds__(32 * SELW) k_coarse_select(const float* __rest
         const uint32_t mid = lo + ((hi - lo) >> 1);
         int c = 0;
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) c += ubb[i] <= mid ? 1 : 0;
+        for (int i = 0; i < NPL; ++i) c += ubat(i) <= mid ? 1 : 0;
         if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) hi = mid;
         else lo = mid + 1;
       }
@@ -771,12 +766,12 @@ __global__ void __launch_bounds__(32 * SELW) k_coarse_select(const float* __rest
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
   for (int i = 0; i < NPL; ++i) {
-    const bool pass = lbv[i] <= U;
+    const bool pass = A[i] - Eat(i) <= U;  // lower bound (+inf beyond nlist)
     const unsigned pm = __ballot_sync(kFull, pass);
     const int pos = nc + __popc(pm & lt);
     if (pass && pos < CCAP) {
       cand[pos] = lane + 32 * i;
-      capx[pos] = fmaxf(0.5f * (lbv[i] + __uint_as_float(ubb[i])), 0.f);
+      capx[pos] = fmaxf(A[i], 0.f);  // the midpoint of the band
     }
     nc += __popc(pm);
   }

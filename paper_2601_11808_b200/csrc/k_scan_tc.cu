@@ -80,7 +80,7 @@ struct TcArgs {
   unsigned long long* partial;
   uint32_t* gthr;
   int dbg;  // experiments only (SIVF_OPT_DEBUG): bit0 skip the slow path, bit1 skip the fast path
-  int copy_mode;  // 0: TMA tile::gather4 builds the B operand; 1: cp.async by the 4 loader warps
+  int copy_mode;  // B operand: 0 TMA tile::gather4; 1 cp.async by the 4 loader warps; 2 both (c4 halves)
 };
 
 struct ItemRec {
@@ -185,6 +185,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const DevState& st = a.st;
   const int Dp = st.Dp, nq4 = Dp >> 2, nst = a.nst, k = a.k;
+  // dims [0, 4 c4_tma) of each group are gathered by TMA, the rest copied by the loader warps
+  const int c4_tma = a.copy_mode == 0 ? nq4 : a.copy_mode == 1 ? 0 : nq4 / 2;
   const TcPlan p = tc_plan(Dp, nst, KP);
   StageMeta* smeta = reinterpret_cast<StageMeta*>(smem + p.off_meta);
   GroupMeta* gm = reinterpret_cast<GroupMeta*>(smem + p.off_gm);
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
 #endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < MAXST; ++i) {
-      mbar_init(&full[i], a.copy_mode ? 32 * NLD : 1);
+      mbar_init(&full[i], a.copy_mode == 0 ? 1 : a.copy_mode == 1 ? 32 * NLD : 32 * NLD + 1);
       mbar_init(&empty[i], 1);
       mbar_init(&meta_full[i], 1);
     }
@@ -315,10 +317,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&meta_full[stg]);  // the MMA warp fetches the slot norms while the payload is in flight
-        if (!a.copy_mode) mbar_arrive_expect_tx(&full[stg], (uint32_t)nq4 * 2048u);
+        if (a.copy_mode != 1) mbar_arrive_expect_tx(&full[stg], (uint32_t)c4_tma * 2048u);
       }
       __syncwarp();
-      if (!a.copy_mode && lane < nq4)
+      if (a.copy_mode != 1 && lane < c4_tma)
         tma_gather4(stage_x(stg) + lane * 512, &tmap, 0, sj[0] * nq4 + lane, sj[1] * nq4 + lane,
                     sj[2] * nq4 + lane, sj[3] * nq4 + lane, &full[stg]);
       ++gseq;
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
             const float* src = st.payload + (size_t)sl * kSlot * Dp + lane * 4;
             const uint32_t dst = smem_u32(stage_x(stg)) + (uint32_t)(qw * 512 + lane * 16);
 #pragma unroll 8
-            for (int c4 = 0; c4 < nq4; ++c4)
+            for (int c4 = c4_tma; c4 < nq4; ++c4)
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (uint32_t)c4 * 2048u),
                            "l"(src + (size_t)c4 * 128)
                            : "memory");

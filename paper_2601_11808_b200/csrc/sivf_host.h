@@ -84,7 +84,7 @@ struct Index {
   bool tc_two_phase = false;  // nearest-list-first scan phase (SIVF_OPT_TC_TWO_PHASE)  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
   bool coarse_select = true;  // A-matrix + per-row selection coarse path (SIVF_OPT_COARSE_SELECT)
   bool rank_split = true;     // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT)
-  int scan_copy_mode = 0;     // k_scan_tc B operand: 0 TMA gather4 (default), 1 cp.async by the loader warps
+  int scan_copy_mode = 2;     // k_scan_tc B operand: 0 TMA gather4, 1 cp.async by the loader warps, 2 both (c4 halves)
   int dbg = 0;                // experiment switches (SIVF_OPT_DEBUG)
   int seed_slabs = 0;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS; off: it costs more than it saves)
   int64_t launches = 0;

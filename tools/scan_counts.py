@@ -14,11 +14,12 @@ for b in range(0, N, 65536):
     ix.insert(ids[b:b+65536], X[b:b+65536])
 Q = torch.from_numpy(gen.queries(0, NQ)).cuda()
 c = np.zeros(4, np.uint64)
-for split in (1, 0):
+for split, seed in ((1, 0), (1, 1), (1, 4)):
     for npb in (8, 32):
         ix.set_option(5, split)
+        ix.set_option(4, seed)
         ix.search(Q, 10, npb); torch.cuda.synchronize()
         S.lib().sivf_debug_scnt(c.ctypes.data_as(ctypes.c_void_p), 1)
         ix.search(Q, 10, npb); torch.cuda.synchronize()
         S.lib().sivf_debug_scnt(c.ctypes.data_as(ctypes.c_void_p), 1)
-        print(f"split {split} nprobe {npb}: slow entries/query {c[0]/NQ:.1f} survivors/query {c[1]/NQ:.1f} insertions/query {c[2]/NQ:.1f}")
+        print(f"seed {seed} split {split} nprobe {npb}: slow entries/query {c[0]/NQ:.1f} survivors/query {c[1]/NQ:.1f} insertions/query {c[2]/NQ:.1f}")

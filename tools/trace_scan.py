@@ -16,7 +16,7 @@ for b in range(0, N, 65536):
 Q = torch.from_numpy(gen.queries(0, NQ)).cuda()
 ix.set_option(4, 0)
 ix.set_option(99, int(os.environ.get("DBG", "0")))
-ix.set_option(98, int(os.environ.get("COPY", "0")))
+ix.set_option(98, int(os.environ.get("COPY", "2")))
 for _ in range(3):
     ix.search(Q, 10, npb)
 torch.cuda.synchronize()
