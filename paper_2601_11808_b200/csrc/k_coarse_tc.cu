@@ -639,6 +639,19 @@ __global__ void __launch_bounds__(128) k_coarse_rerank(const float* __restrict__
 // (dist32, l).  MODE 0: best[row] = smallest key (assignment); MODE 1:
 // probes[row][0..m) sorted.  More than CCAP candidates: every list is re-ranked.
 constexpr int CCAP = 256;
+// Fused first step of the search's inverse probe map (k_search.cu k_inv_count): per
+// probe rank j of a row, one count in bucket (j >= r0) of its list; the row's k-th
+// distance bound reset to +inf.  cnt == nullptr: not fused.
+struct InvCount {
+  int32_t* cnt;
+  uint32_t* gthr;
+  int nb, r0;
+};
+__device__ __forceinline__ void inv_count_row(const InvCount& ic, int nlist, int64_t row, int j, int32_t l) {
+  if (!ic.cnt) return;
+  atomicAdd(&ic.cnt[((ic.nb == 2 && j >= ic.r0) ? nlist : 0) + l], 1);
+  if (j == 0) ic.gthr[row] = 0x7F800000u;
+}
 #ifdef SIVF_TC_PROF
 __device__ unsigned g_selhist[2][64];
 __device__ unsigned long long g_selclk[2][8];
@@ -669,7 +682,7 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
                                                              const float* __restrict__ C, int Dp,
                                                              unsigned long long* __restrict__ best,
                                                              int32_t* __restrict__ probes, int probes_ld,
-                                                             int need_dist) {
+                                                             int need_dist, InvCount ic) {
   extern __shared__ __align__(16) unsigned char sm_sel[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* csa_s = reinterpret_cast<float*>(sm_sel + SELW * select_smem_per_warp(Dp));
@@ -794,7 +807,10 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
     // approximate distance (nearest-first only steers the scan's work order)
     unsigned long long k0 = lane < nc ? make_key(capx[lane], (uint32_t)cand[lane]) : kPadKey;
     k0 = warp_sort32(k0);
-    if (lane < m) probes[row * probes_ld + lane] = (int32_t)key_id(k0);
+    if (lane < m) {
+      probes[row * probes_ld + lane] = (int32_t)key_id(k0);
+      inv_count_row(ic, nlist, row, lane, (int32_t)key_id(k0));
+    }
     SELCLK(3);
     return;
   }
@@ -818,7 +834,10 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
         k0 = (lane & j) ? umax64(k0, o) : umin64(k0, o);
       }
     }
-    if (lane < m) probes[row * probes_ld + lane] = (int32_t)key_id(k0);
+    if (lane < m) {
+      probes[row * probes_ld + lane] = (int32_t)key_id(k0);
+      inv_count_row(ic, nlist, row, lane, (int32_t)key_id(k0));
+    }
     SELCLK(4);
     return;
   }
@@ -838,7 +857,10 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
     for (int off = 16; off; off >>= 1) bestk = umin64(bestk, __shfl_xor_sync(kFull, bestk, off));
     if (lane == 0) best[row] = bestk;
   } else {
-    for (int j = lane; j < m; j += 32) probes[row * probes_ld + j] = (int32_t)key_id(top[j]);
+    for (int j = lane; j < m; j += 32) {
+      probes[row * probes_ld + j] = (int32_t)key_id(top[j]);
+      inv_count_row(ic, nlist, row, j, (int32_t)key_id(top[j]));
+    }
   }
 }
 
@@ -959,10 +981,11 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
   if (probes == nullptr)                                                                                       \
     k_coarse_select<NPL, 0><<<g, 32 * SELW, ssm, s>>>(sc.coarse, xr, nr, D, st.nlist, m, sc.x_norm, sc.c_csa,  \
                                                        sc.c_cnb, bd.kb, st.centroids, Dp, best + r0, nullptr, 0,  \
-                                                       need_dist);                                                \
+                                                       need_dist, InvCount{nullptr, nullptr, 1, 0});              \
   else                                                                                                         \
     k_coarse_select<NPL, 1><<<g, 32 * SELW, ssm, s>>>(sc.coarse, xr, nr, D, st.nlist, m, sc.x_norm, sc.c_csa,  \
-                                                       sc.c_cnb, bd.kb, st.centroids, Dp, nullptr, probes + r0 * m, m, 1);
+                                                       sc.c_cnb, bd.kb, st.centroids, Dp, nullptr, probes + r0 * m, m, 1, \
+                                                       InvCount{ix.fuse_inv_cnt, ix.sc.gthr + r0, ix.fuse_nb, ix.fuse_r0});
       if (st.nlist <= 256) {
         SIVF_SEL(8)
       } else if (st.nlist <= 512) {
@@ -975,6 +998,7 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
+    if (ix.fuse_inv_cnt) ix.fuse_inv_done = true;
     return cudaSuccess;
   }
   const size_t rsm = 4 * rerank_smem_per_warp(m, cap, Dp);

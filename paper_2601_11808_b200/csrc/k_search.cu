@@ -226,7 +226,9 @@ __global__ void k_inv_count(const int32_t* __restrict__ probes, int64_t npairs, 
 
 __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ cnt, int nent, int QT,
                                                    int32_t* __restrict__ off, int32_t* __restrict__ cursor,
-                                                   int32_t* __restrict__ tile_off, int32_t* __restrict__ ictr) {
+                                                   int32_t* __restrict__ tile_off, int32_t* __restrict__ ictr,
+                                                   int nlist, int32_t* __restrict__ work_l,
+                                                   int32_t* __restrict__ work_p0, int32_t* __restrict__ work_n) {
   __shared__ int32_t ws[2][32];
   __shared__ int32_t carry[2];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -284,6 +286,16 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
     ictr[I_NTILES] = carry[1];
     ictr[I_WORK] = 0;
   }
+  __syncthreads();  // the block's offsets are visible to all of its threads
+  // work items (list, first pair, number of pairs), bucket-major (k_work_fill fused)
+  for (int e = t; e < nent; e += blockDim.x) {
+    const int c = off[e + 1] - off[e];
+    for (int tt = tile_off[e], j = 0; tt < tile_off[e + 1]; ++tt, ++j) {
+      work_l[tt] = e % nlist;
+      work_p0[tt] = off[e] + j * QT;
+      work_n[tt] = min(QT, c - j * QT);
+    }
+  }
 }
 
 __global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int nb, int r0,
@@ -295,17 +307,36 @@ __global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs
   pairs[atomicAdd(&cursor[b * nlist + probes[i]], 1)] = (int32_t)i;
 }
 
-// Materialise the work items: (list, first pair, number of pairs).
-__global__ void k_work_fill(const int32_t* __restrict__ tile_off, const int32_t* __restrict__ off, int nent,
-                            int nlist, int QT, int32_t* __restrict__ work_l, int32_t* __restrict__ work_p0,
-                            int32_t* __restrict__ work_n) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= nent) return;
-  const int c = off[e + 1] - off[e];
-  for (int t = tile_off[e], j = 0; t < tile_off[e + 1]; ++t, ++j) {
-    work_l[t] = e % nlist;
-    work_p0[t] = off[e] + j * QT;
-    work_n[t] = min(QT, c - j * QT);
+// Warp per query, nprobe <= 32, k <= KM: lane p holds probe p's sorted partial list in
+// registers; k rounds of a warp-wide minimum over the list heads, the winning lane
+// shifts its list (static register moves, no local memory).  Same result as k_merge.
+template <int KM>
+__global__ void __launch_bounds__(128) k_merge_regs(const unsigned long long* __restrict__ partial, int64_t nq,
+                                                    int nprobe, int k, float* __restrict__ dist,
+                                                    int64_t* __restrict__ ids) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.x * 4 + w;
+  if (q >= nq) return;  // warp-uniform
+  unsigned long long h[KM];
+  const unsigned long long* src = partial + ((size_t)q * nprobe + lane) * k;
+#pragma unroll
+  for (int j = 0; j < KM; ++j) h[j] = (lane < nprobe && j < k) ? src[j] : kPadKey;
+  unsigned long long out = kPadKey;
+  for (int r = 0; r < k; ++r) {
+    unsigned long long m = h[0];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) m = umin64(m, __shfl_xor_sync(kFull, m, off));
+    if (lane == r) out = m;
+    if (h[0] == m) {  // keys are unique (ids), so exactly one lane advances
+#pragma unroll
+      for (int j = 0; j < KM - 1; ++j) h[j] = h[j + 1];
+      h[KM - 1] = kPadKey;
+    }
+  }
+  if (lane < k) {
+    const bool pad = out == kPadKey;
+    dist[q * k + lane] = pad ? __int_as_float(0x7f800000) : key_dist(out);
+    ids[q * k + lane] = pad ? -1 : (int64_t)key_id(out);
   }
 }
 
@@ -405,10 +436,7 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   const size_t smem = tc ? 0 : scan_smem_for(ix, k, &nw);
   if (!tc && !nw) return cudaErrorInvalidConfiguration;
   const int QT = tc ? scan_tc_tile() : kQPW * nw;
-  cudaError_t e = launch_probe_exact(ix, d_q, nq, nprobe, s);
-  if (e != cudaSuccess) return e;
   const int64_t npairs = nq * nprobe;
-  if (d_probes) cudaMemcpyAsync(d_probes, sc.probes, sizeof(int32_t) * npairs, cudaMemcpyDeviceToDevice, s);
   // Tensor-core path: probe-rank buckets, one scan launch.  Work items are laid
   // out bucket-major, so with nb = 2 every query's r0 nearest lists are scanned
   // first and its k-th distance bound is tight before the other lists are
@@ -424,17 +452,31 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
       r0 = rr;
     }
   }
+  // the coarse selection may count the inverse map on the fly (k_inv_count fused)
+  cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * nb * nlist, s);
+  ix.fuse_inv_cnt = sc.inv_cnt;
+  ix.fuse_nb = nb;
+  ix.fuse_r0 = r0;
+  ix.fuse_inv_done = false;
+  cudaError_t e = launch_probe_exact(ix, d_q, nq, nprobe, s);
+  const bool counted = ix.fuse_inv_done;
+  ix.fuse_inv_cnt = nullptr;
+  ix.fuse_inv_done = false;
+  if (e != cudaSuccess) return e;
+  if (d_probes) cudaMemcpyAsync(d_probes, sc.probes, sizeof(int32_t) * npairs, cudaMemcpyDeviceToDevice, s);
   const int nent = nb * nlist;
   {
     PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
-    cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * nent, s);
-    k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, r0, nlist, sc.inv_cnt, sc.gthr);
-    k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr);
+    if (!counted) {
+      k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, r0, nlist, sc.inv_cnt, sc.gthr);
+      ix.launches += 1;
+    }
+    k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr, nlist,
+                                  sc.work_l, sc.work_p0, sc.work_n);
     k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, r0, nlist, sc.inv_cursor,
                                                          sc.inv_pairs);
-    k_work_fill<<<ceil_div(nent, 256), 256, 0, s>>>(sc.tile_off, sc.inv_off, nent, nlist, QT, sc.work_l,
-                                                    sc.work_p0, sc.work_n);
-    ix.launches += 4;
+
+    ix.launches += 2;
   }
   ScanArgs a{ix.st, d_q, nprobe, k, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial};
   const int grid = ix.num_sms;  // persistent: one CTA per SM
@@ -453,8 +495,13 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   }
   PhaseTimer pt(ix, SIVF_PH_MERGE, s);
   const int wpb = 4;
-  k_merge<<<ceil_div(nq, wpb), 32 * wpb, sizeof(unsigned long long) * 2 * k * wpb, s>>>(sc.partial, nq, nprobe, k,
-                                                                                        d_dist, d_ids);
+  if (nprobe <= 32 && k <= 16) {
+    if (k <= 10) k_merge_regs<10><<<ceil_div(nq, 4), 128, 0, s>>>(sc.partial, nq, nprobe, k, d_dist, d_ids);
+    else k_merge_regs<16><<<ceil_div(nq, 4), 128, 0, s>>>(sc.partial, nq, nprobe, k, d_dist, d_ids);
+  } else {
+    k_merge<<<ceil_div(nq, wpb), 32 * wpb, sizeof(unsigned long long) * 2 * k * wpb, s>>>(sc.partial, nq, nprobe, k,
+                                                                                          d_dist, d_ids);
+  }
   ix.launches += 1;
   return cudaGetLastError();
 }

@@ -82,6 +82,11 @@ struct Index {
   bool use_tc_scan = true;
   bool use_tc_coarse = true;  // tcgen05 coarse quantisation (k_coarse_tc.cu); false = exact SIMT k_dist_exact
   bool tc_two_phase = false;  // nearest-list-first scan phase (SIVF_OPT_TC_TWO_PHASE)  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
+  // search -> coarse hand-off: when set, k_coarse_select also counts the inverse probe map
+  // (k_inv_count fused) into fuse_inv_cnt and sets fuse_inv_done
+  int32_t* fuse_inv_cnt = nullptr;
+  int fuse_nb = 1, fuse_r0 = 0;
+  bool fuse_inv_done = false;
   bool coarse_select = true;  // A-matrix + per-row selection coarse path (SIVF_OPT_COARSE_SELECT)
   bool rank_split = true;     // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT)
   int scan_copy_mode = 2;     // k_scan_tc B operand: 0 TMA gather4, 1 cp.async by the loader warps, 2 both (c4 halves)
