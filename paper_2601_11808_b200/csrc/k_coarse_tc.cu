@@ -910,6 +910,14 @@ cudaError_t setup_coarse_tc(Index& ix) {
           enc(reinterpret_cast<CUtensorMap*>(ix.coarse_tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ix.sc.coarse, gdim,
               gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      ix.qcoarse_tmap_ok = false;
+      if (ix.coarse_tmap_ok && ix.sc.q_rows >= TM) {
+        const cuuint64_t qdim[2] = {(cuuint64_t)ix.st.nlist, (cuuint64_t)ix.sc.q_rows};
+        ix.qcoarse_tmap_ok =
+            enc(reinterpret_cast<CUtensorMap*>(ix.qcoarse_tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ix.sc.qcoarse,
+                qdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      }
     } else {
       cudaGetLastError();
     }
@@ -943,6 +951,13 @@ cudaError_t refresh_centroid_tiles(Index& ix, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// The search front (probe selection) may overlap an insert's assignment when it takes the
+// k_coarse_select path on its own scratch set.
+bool coarse_front_concurrent_ok(const Index& ix, int32_t nprobe) {
+  return coarse_tc_supported(ix, nprobe) && ix.coarse_select && ix.coarse_tmap_ok && ix.qcoarse_tmap_ok &&
+         ix.st.nlist <= 1024 && ix.sc.q_rows >= TM;
+}
+
 int coarse_tc_tile_rows() { return TM; }
 int coarse_tc_tile_cols() { return TN; }
 
@@ -960,30 +975,38 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
   const int ntn = (int)ceil_div(st.nlist, TN);
   // Fast path: store A, then a per-row selection (k_coarse_select) — nlist <= 1024
   // and chunks of >= 128 rows of the coarse scratch matrix.
-  const int64_t R = sc.tc_rows < sc.coarse_rows / TM * TM ? sc.tc_rows : sc.coarse_rows / TM * TM;
+  // the search front may run concurrently with an insert's assignment: it then uses
+  // its own scratch set (q*), sized for max_queries rows
+  const bool alt = ix.coarse_alt;
+  float* const xt = alt ? sc.qx_tiles : sc.x_tiles;
+  float* const xn = alt ? sc.qx_norm : sc.x_norm;
+  float* const mat = alt ? sc.qcoarse : sc.coarse;
+  const void* const tmat = alt ? (const void*)ix.qcoarse_tmap : (const void*)ix.coarse_tmap;
+  const int64_t R = alt ? sc.q_rows
+                        : (sc.tc_rows < sc.coarse_rows / TM * TM ? sc.tc_rows : sc.coarse_rows / TM * TM);
   if (ix.coarse_select && ix.coarse_tmap_ok && st.nlist <= 1024 && R >= TM) {
     const size_t ssm = select_smem(Dp, st.nlist);
     for (int64_t r0 = 0; r0 < n; r0 += R) {
       const int64_t nr = n - r0 < R ? n - r0 : R;
       const float* xr = d_x + r0 * D;
       const int64_t ntile = ceil_div(nr, TM);
-      k_rows_tiles<<<ntile, 4 * TM, 0, s>>>(xr, nr, D, Dp, sc.x_tiles, sc.x_norm);
+      k_rows_tiles<<<ntile, 4 * TM, 0, s>>>(xr, nr, D, Dp, xt, xn);
       // split the N-tiles over CTAs until every SM has a CTA
       int ncg = ntile >= ix.num_sms ? 1 : (int)ceil_div(ix.num_sms, ntile);
       if (ncg > ntn) ncg = ntn;
       const int ntpc = (int)ceil_div(ntn, ncg);
-      CoarseArgs a{sc.x_tiles, sc.x_norm, sc.c_tiles, sc.c_norm, sc.c_csa, sc.c_cnb, nr, Dp, st.nlist, m, 0,
-                   bd.kb, nullptr, nullptr, nullptr, sc.coarse, ntpc};
+      CoarseArgs a{xt, xn, sc.c_tiles, sc.c_norm, sc.c_csa, sc.c_cnb, nr, Dp, st.nlist, m, 0,
+                   bd.kb, nullptr, nullptr, nullptr, mat, ntpc};
       k_coarse_gemm<0><<<dim3((unsigned)ntile, (unsigned)ceil_div(ntn, ntpc)), CTHREADS, coarse_smem_bytes(0), s>>>(
-          *reinterpret_cast<const CUtensorMap*>(ix.coarse_tmap), a);
+          *reinterpret_cast<const CUtensorMap*>(tmat), a);
       const dim3 g((unsigned)ceil_div(nr, SELW));
 #define SIVF_SEL(NPL)                                                                                          \
   if (probes == nullptr)                                                                                       \
-    k_coarse_select<NPL, 0><<<g, 32 * SELW, ssm, s>>>(sc.coarse, xr, nr, D, st.nlist, m, sc.x_norm, sc.c_csa,  \
+    k_coarse_select<NPL, 0><<<g, 32 * SELW, ssm, s>>>(mat, xr, nr, D, st.nlist, m, xn, sc.c_csa,  \
                                                        sc.c_cnb, bd.kb, st.centroids, Dp, best + r0, nullptr, 0,  \
                                                        need_dist, InvCount{nullptr, nullptr, 1, 0});              \
   else                                                                                                         \
-    k_coarse_select<NPL, 1><<<g, 32 * SELW, ssm, s>>>(sc.coarse, xr, nr, D, st.nlist, m, sc.x_norm, sc.c_csa,  \
+    k_coarse_select<NPL, 1><<<g, 32 * SELW, ssm, s>>>(mat, xr, nr, D, st.nlist, m, xn, sc.c_csa,  \
                                                        sc.c_cnb, bd.kb, st.centroids, Dp, nullptr, probes + r0 * m, m, 1, \
                                                        InvCount{ix.fuse_inv_cnt, ix.sc.gthr + r0, ix.fuse_nb, ix.fuse_r0});
       if (st.nlist <= 256) {

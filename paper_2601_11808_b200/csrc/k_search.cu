@@ -426,37 +426,45 @@ cudaError_t setup_search_kernels(Index& ix) {
   return cudaSuccess;
 }
 
-cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
-                          int64_t* d_ids, int32_t* d_probes, cudaStream_t s) {
-  if (nq <= 0) return cudaSuccess;
-  Scratch& sc = ix.sc;
+SearchPlan plan_search(const Index& ix, int64_t nq, int32_t k, int32_t nprobe) {
+  SearchPlan p{};
   const int nlist = ix.st.nlist;
-  const bool tc = ix.use_tc_scan && scan_tc_supported(ix, k);
-  int nw = 0;
-  const size_t smem = tc ? 0 : scan_smem_for(ix, k, &nw);
-  if (!tc && !nw) return cudaErrorInvalidConfiguration;
-  const int QT = tc ? scan_tc_tile() : kQPW * nw;
-  const int64_t npairs = nq * nprobe;
+  p.tc = ix.use_tc_scan && scan_tc_supported(ix, k);
+  p.smem = p.tc ? 0 : scan_smem_for(ix, k, &p.nw);
+  p.ok = p.tc || p.nw != 0;
+  p.QT = p.tc ? scan_tc_tile() : kQPW * p.nw;
   // Tensor-core path: probe-rank buckets, one scan launch.  Work items are laid
   // out bucket-major, so with nb = 2 every query's r0 nearest lists are scanned
   // first and its k-th distance bound is tight before the other lists are
   // reached (far fewer survivors of the tensor-core filter).  Split only when
   // the lists are long enough in queries that it adds no tiles on average.
-  int nb = 1, r0 = nprobe;
-  if (tc && nprobe >= 8) {
-    const int64_t per_list = npairs / nlist;
+  p.nb = 1;
+  p.r0 = nprobe;
+  if (p.tc && nprobe >= 8) {
+    const int64_t per_list = nq * nprobe / nlist;
     const int rr = ix.tc_two_phase ? 1 : nprobe / 4;
-    const int64_t ta = ceil_div(per_list * rr / nprobe, QT), tb = ceil_div(per_list - per_list * rr / nprobe, QT);
-    if (ix.tc_two_phase || (ix.rank_split && ta + tb <= ceil_div(per_list, QT))) {
-      nb = 2;
-      r0 = rr;
+    const int64_t ta = ceil_div(per_list * rr / nprobe, p.QT),
+                  tb = ceil_div(per_list - per_list * rr / nprobe, p.QT);
+    if (ix.tc_two_phase || (ix.rank_split && ta + tb <= ceil_div(per_list, p.QT))) {
+      p.nb = 2;
+      p.r0 = rr;
     }
   }
+  return p;
+}
+
+// Coarse quantisation + inverse probe map: reads only the centroids and the
+// queries (never the index state), so it may run concurrently with mutations.
+cudaError_t launch_search_front(Index& ix, const SearchPlan& p, const float* d_q, int64_t nq, int32_t nprobe,
+                                int32_t* d_probes, cudaStream_t s) {
+  Scratch& sc = ix.sc;
+  const int nlist = ix.st.nlist;
+  const int64_t npairs = nq * nprobe;
   // the coarse selection may count the inverse map on the fly (k_inv_count fused)
-  cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * nb * nlist, s);
+  cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * p.nb * nlist, s);
   ix.fuse_inv_cnt = sc.inv_cnt;
-  ix.fuse_nb = nb;
-  ix.fuse_r0 = r0;
+  ix.fuse_nb = p.nb;
+  ix.fuse_r0 = p.r0;
   ix.fuse_inv_done = false;
   cudaError_t e = launch_probe_exact(ix, d_q, nq, nprobe, s);
   const bool counted = ix.fuse_inv_done;
@@ -464,32 +472,41 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   ix.fuse_inv_done = false;
   if (e != cudaSuccess) return e;
   if (d_probes) cudaMemcpyAsync(d_probes, sc.probes, sizeof(int32_t) * npairs, cudaMemcpyDeviceToDevice, s);
-  const int nent = nb * nlist;
-  {
-    PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
-    if (!counted) {
-      k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, r0, nlist, sc.inv_cnt, sc.gthr);
-      ix.launches += 1;
-    }
-    k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr, nlist,
-                                  sc.work_l, sc.work_p0, sc.work_n);
-    k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, nb, r0, nlist, sc.inv_cursor,
-                                                         sc.inv_pairs);
-
-    ix.launches += 2;
+  const int nent = p.nb * nlist;
+  PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
+  if (!counted) {
+    k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, p.nb, p.r0, nlist, sc.inv_cnt,
+                                                       sc.gthr);
+    ix.launches += 1;
   }
+  k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, p.QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr, nlist,
+                                sc.work_l, sc.work_p0, sc.work_n);
+  k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, p.nb, p.r0, nlist, sc.inv_cursor,
+                                                       sc.inv_pairs);
+  ix.launches += 2;
+  return cudaGetLastError();
+}
+
+// Slab scan + per-query merge (reads the index state).
+cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q, int64_t nq, int32_t k,
+                               int32_t nprobe, float* d_dist, int64_t* d_ids, cudaStream_t s) {
+  Scratch& sc = ix.sc;
+  cudaError_t e = cudaSuccess;
   ScanArgs a{ix.st, d_q, nprobe, k, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial};
   const int grid = ix.num_sms;  // persistent: one CTA per SM
   {
     PhaseTimer pt(ix, SIVF_PH_SCAN, s);
-    if (tc) {
-      e = launch_seed_bound(ix, d_q, nq, k, nprobe, s);  // after k_inv_count reset gthr to +inf
+    if (p.tc) {
+      e = launch_seed_bound(ix, d_q, nq, k, nprobe, s);  // after the front reset gthr to +inf
       if (e == cudaSuccess) e = launch_scan_tc(ix, d_q, k, nprobe, s);
+    } else if (p.nw == 8) {
+      k_scan<8><<<grid, 32 * 9, p.smem, s>>>(a);
+    } else if (p.nw == 4) {
+      k_scan<4><<<grid, 32 * 5, p.smem, s>>>(a);
+    } else {
+      k_scan<2><<<grid, 32 * 3, p.smem, s>>>(a);
     }
-    else if (nw == 8) k_scan<8><<<grid, 32 * 9, smem, s>>>(a);
-    else if (nw == 4) k_scan<4><<<grid, 32 * 5, smem, s>>>(a);
-    else k_scan<2><<<grid, 32 * 3, smem, s>>>(a);
-    if (!tc) ix.launches += 1;
+    if (!p.tc) ix.launches += 1;
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return e;  // a failed scan launch must not be masked by the merge below
   }
@@ -504,6 +521,16 @@ cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, in
   }
   ix.launches += 1;
   return cudaGetLastError();
+}
+
+cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
+                          int64_t* d_ids, int32_t* d_probes, cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  const SearchPlan p = plan_search(ix, nq, k, nprobe);
+  if (!p.ok) return cudaErrorInvalidConfiguration;
+  cudaError_t e = launch_search_front(ix, p, d_q, nq, nprobe, d_probes, s);
+  if (e != cudaSuccess) return e;
+  return launch_search_back(ix, p, d_q, nq, k, nprobe, d_dist, d_ids, s);
 }
 
 cudaError_t launch_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int32_t G, int64_t nq, int32_t k,

@@ -21,6 +21,8 @@ struct Layout {
       list_granted, list_newbase, list_short;
   size_t coarse, probes, inv_cnt, inv_off, inv_cursor, inv_pairs, tile_off, work_l, work_p0, work_n, partial;
   size_t train_perm, train_members, train_off;
+  size_t qx_tiles, qx_norm, qcoarse;
+  int64_t q_rows;
   size_t x_tiles, x_norm, c_tiles, c_norm, c_csa, c_cnb, cand, cand_ubv, cand_cnt;
   int64_t tc_rows, cap_assign, cap_probe;
   int64_t Dp, cap_local, dir_arena_cap, max_rows, max_chunks, coarse_rows, max_work;
@@ -133,6 +135,11 @@ Layout make_layout(const sivf_config* c) {
   L.cand = take(L, (size_t)cap_rows * 8);
   L.cand_ubv = take(L, (size_t)cap_rows * 4);
   L.cand_cnt = take(L, (size_t)L.tc_rows * 4);
+  L.q_rows = (c->max_queries + 127) / 128 * 128;
+  if (nl > 1024) L.q_rows = 0;  // the concurrent search front needs the k_coarse_select path
+  L.qx_tiles = take(L, (size_t)2 * L.q_rows * L.Dp * 4);
+  L.qx_norm = take(L, (size_t)L.q_rows * 4);
+  L.qcoarse = take(L, (size_t)L.q_rows * nl * 4);
   return L;
 }
 
@@ -244,6 +251,10 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   sc.list_newbase = at<int32_t>(d_arena, L.list_newbase);
   sc.list_short = at<int32_t>(d_arena, L.list_short);
   sc.coarse = at<float>(d_arena, L.coarse);
+  sc.q_rows = L.q_rows;
+  sc.qx_tiles = at<float>(d_arena, L.qx_tiles);
+  sc.qx_norm = at<float>(d_arena, L.qx_norm);
+  sc.qcoarse = at<float>(d_arena, L.qcoarse);
   sc.coarse_rows = L.coarse_rows;
   sc.probes = at<int32_t>(d_arena, L.probes);
   sc.inv_cnt = at<int32_t>(d_arena, L.inv_cnt);
@@ -283,6 +294,9 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   if (m < 64) m = 64;
   k_init<<<ceil_div(m, 256), 256, 0, s>>>(st);
   ix->launches += 1;
+  cudaStreamCreateWithFlags(&ix->side, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&ix->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ix->ev_join, cudaEventDisableTiming);
   cudaError_t e = setup_search_kernels(*ix);
   if (e == cudaSuccess) e = setup_coarse_tc(*ix);
   if (e == cudaSuccess) {
@@ -386,9 +400,26 @@ sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const f
   }
   if (!ix->trained) return SIVF_E_NOT_TRAINED;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e = launch_insert(*ix, d_new_ids, d_new_x, n_new, d_status, nullptr, s);
+  // The search's coarse quantisation and inverse probe map read only centroids and
+  // queries, so they run on a side stream concurrently with insert + delete; the
+  // scan joins after the mutations (C22: the search sees the post-step window).
+  const SearchPlan sp = plan_search(*ix, nq, k, nprobe);
+  if (nq > 0 && !sp.ok) return SIVF_E_UNSUPPORTED;
+  const bool fork = nq > 0 && coarse_front_concurrent_ok(*ix, nprobe) && ix->side;
+  cudaError_t e = cudaSuccess;
+  if (fork) {
+    cudaEventRecord(ix->ev_fork, s);
+    cudaStreamWaitEvent(ix->side, ix->ev_fork, 0);
+    ix->coarse_alt = true;
+    e = launch_search_front(*ix, sp, d_q, nq, nprobe, nullptr, ix->side);
+    ix->coarse_alt = false;
+    cudaEventRecord(ix->ev_join, ix->side);
+  }
+  if (e == cudaSuccess) e = launch_insert(*ix, d_new_ids, d_new_x, n_new, d_status, nullptr, s);
   if (e == cudaSuccess) e = launch_delete(*ix, d_old_ids, n_old, d_ndeleted, s);
-  if (e == cudaSuccess && nq > 0) e = launch_search(*ix, d_q, nq, k, nprobe, d_dist, d_ids, nullptr, s);
+  if (fork) cudaStreamWaitEvent(s, ix->ev_join, 0);  // always join, even after an error
+  if (e == cudaSuccess && nq > 0 && !fork) e = launch_search_front(*ix, sp, d_q, nq, nprobe, nullptr, s);
+  if (e == cudaSuccess && nq > 0) e = launch_search_back(*ix, sp, d_q, nq, k, nprobe, d_dist, d_ids, s);
   if (e == cudaSuccess) e = launch_reclaim(*ix, nullptr, s);
   return cuda_rc(e);
 }

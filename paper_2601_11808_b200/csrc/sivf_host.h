@@ -67,6 +67,11 @@ struct Scratch {
   float* cand_ubv = nullptr;        // [rows][cap] candidate upper bounds
   int32_t* cand_cnt = nullptr;      // [tc_rows]
   int32_t cand_cap_assign = 0, cand_cap_probe = 0;
+  // the search front's own coarse scratch (overlaps insert's assignment in the sliding step)
+  int64_t q_rows = 0;               // max_queries rounded up to 128
+  float* qx_tiles = nullptr;        // [q_rows/128][hi, lo][Dp/4][128][4]
+  float* qx_norm = nullptr;         // [q_rows]
+  float* qcoarse = nullptr;         // [q_rows][nlist]
 };
 
 struct PhaseRec {
@@ -100,6 +105,11 @@ struct Index {
   bool payload_tmap_ok = false;
   alignas(64) unsigned char coarse_tmap[128] = {};  // TMA store descriptor of sc.coarse (k_coarse_tc.cu)
   bool coarse_tmap_ok = false;
+  alignas(64) unsigned char qcoarse_tmap[128] = {};  // TMA store descriptor of sc.qcoarse
+  bool qcoarse_tmap_ok = false;
+  bool coarse_alt = false;    // launch_coarse_tc: use the search-front scratch set
+  cudaStream_t side = nullptr;  // second stream for the sliding step's search front
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
   // phase profiling (sivf_profile_*)
@@ -117,6 +127,9 @@ struct Index {
     return e;
   }
   ~Index() {
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     for (auto& r : recs) {
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
@@ -167,6 +180,17 @@ int coarse_tc_tile_cols();
 cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsigned long long* best,
                              int32_t* probes, cudaStream_t s, bool need_dist = true);
 // k_search.cu
+struct SearchPlan {
+  bool tc, ok;
+  int nw, QT, nb, r0;
+  size_t smem;
+};
+SearchPlan plan_search(const Index& ix, int64_t nq, int32_t k, int32_t nprobe);
+cudaError_t launch_search_front(Index& ix, const SearchPlan& p, const float* d_q, int64_t nq, int32_t nprobe,
+                                int32_t* d_probes, cudaStream_t s);
+cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q, int64_t nq, int32_t k,
+                               int32_t nprobe, float* d_dist, int64_t* d_ids, cudaStream_t s);
+bool coarse_front_concurrent_ok(const Index& ix, int32_t nprobe);
 cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
                           int64_t* d_ids, int32_t* d_probes, cudaStream_t s);
 cudaError_t launch_seed_bound(Index& ix, const float* d_q, int64_t nq, int k, int nprobe, cudaStream_t s);
