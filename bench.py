@@ -216,6 +216,7 @@ def run_sivf(args):
 
     import paper_2601_11808_b200 as S
     from datagen import Generator, sift_shape
+    from paper_2601_11808_b200 import shard
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -253,8 +254,8 @@ def run_sivf(args):
 
     Xb_host = gen.range(0, N_BASE)
     ids_all = np.arange(N_BASE, dtype=np.int64)
-    mine = ids_all[ids_all % G == rank]
-    Xb = torch.from_numpy(Xb_host[mine]).to(dev)
+    mine, Xmine = shard.route(ids_all, G, rank, Xb_host)  # owner(id) = id mod G, no collective
+    Xb = torch.from_numpy(Xmine).to(dev)
     idb = torch.from_numpy(mine).to(dev)
     build_ms = []
     bl = 65536
@@ -275,8 +276,8 @@ def run_sivf(args):
     def step_host(t):
         new = np.arange(N_BASE + t * BATCH, N_BASE + (t + 1) * BATCH, dtype=np.int64)
         old = np.arange(t * BATCH, (t + 1) * BATCH, dtype=np.int64)
-        nm, om = new[new % G == rank], old[old % G == rank]
-        Xn = gen.range(int(new[0]), BATCH)[(new % G == rank)]
+        nm, Xn = shard.route(new, G, rank, gen.range(int(new[0]), BATCH))
+        om, = shard.route(old, G, rank)
         Q = gen.queries(t * NQ, NQ)
         return nm, np.ascontiguousarray(Xn), om, Q
 
@@ -289,16 +290,12 @@ def run_sivf(args):
     out_i = torch.empty(NQ, K, dtype=torch.int64, device=dev)
     status = torch.empty(BATCH, dtype=torch.int32, device=dev)
     ndel = torch.empty(1, dtype=torch.int64, device=dev)
-    if G > 1:
-        gd = torch.empty(G, NQ, K, dtype=torch.float32, device=dev)
-        gi = torch.empty(G, NQ, K, dtype=torch.int64, device=dev)
 
     def one_step(inp):
         nm, Xn, om, Q = inp
         ix.sliding_window_step(nm, Xn, om, Q, K, NPROBE, out=(out_d, out_i, status, ndel))
         if G > 1:
-            pg.all_gather_into_tensor(gd.view(-1), out_d.view(-1))
-            pg.all_gather_into_tensor(gi.view(-1), out_i.view(-1))
+            gd, gi = shard.allgather_topk(pg, out_d, out_i)  # NCCL all-gather of the per-shard top-k
             return S.merge_topk(gd, gi)
         return out_d, out_i
 
@@ -708,10 +705,11 @@ def leg_h(S, dev, log, G, rank, pg, n_total):
     import torch
 
     from datagen import TRAIN_BASE, QUERY_BASE, DeviceGenerator, sift_shape
+    from paper_2601_11808_b200 import shard
 
     NLH, NQH, NGT, MB = 16384, NQ, 100, 80_000
     gen = DeviceGenerator(sift_shape(seed=0x100A))
-    local_n = len(range(rank, n_total, G))
+    local_n = shard.local_count(n_total, G, rank)
     cap = n_total + MB + 64
     ix = S.Index(DIM, NLH, cap, S.num_slabs_for(local_n + MB // G + 1, NLH), max_batch=1 << 20, max_queries=NQH,
                  max_k=K, max_nprobe=128, max_train=1 << 20, shard_rank=rank, shard_count=G, seed=0x100A, device=dev)
@@ -776,14 +774,10 @@ def leg_h(S, dev, log, G, rank, pg, n_total):
     assert st["live"] == local_n and st["device_errors"] == 0, st
     log(f"H: train {t_train:.1f}s build {t_build:.1f}s ({build_rate / 1e6:.1f} M/s device-timed)")
 
-    gd = torch.empty(G, NQH, K, dtype=torch.float32, device=dev)
-    gi = torch.empty(G, NQH, K, dtype=torch.int64, device=dev)
-
     def search(npb):
         d, i = ix.search(Qg, K, npb)
         if pg is not None:
-            pg.all_gather_into_tensor(gd.view(-1), d.reshape(-1))
-            pg.all_gather_into_tensor(gi.view(-1), i.reshape(-1))
+            gd, gi = shard.allgather_topk(pg, d, i)
             d, i = S.merge_topk(gd, gi)
         return d, i
 
@@ -811,8 +805,8 @@ def leg_h(S, dev, log, G, rank, pg, n_total):
     rng = np.random.default_rng(0x100A)
     dids = rng.choice(n_total, MB, replace=False).astype(np.int64)
     nids = np.arange(n_total, n_total + MB, dtype=np.int64)
-    dl = torch.from_numpy(dids[dids % G == rank]).to(dev)
-    nl = torch.from_numpy(nids[nids % G == rank]).to(dev)
+    dl = torch.from_numpy(shard.route(dids, G, rank)[0]).to(dev)
+    nl = torch.from_numpy(shard.route(nids, G, rank)[0]).to(dev)
     Xn = torch.empty(nl.shape[0], DIM, dtype=torch.float32, device=dev)
     gen.range_into(Xn, n_total + rank, G)
     if pg is not None:
