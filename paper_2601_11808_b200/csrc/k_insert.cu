@@ -282,8 +282,7 @@ __global__ void __launch_bounds__(256) k_append(DevState st, const int64_t* __re
           slab = st.free_stack[newbase[l] + ((r - tf) >> 5)];
           o = (r - tf) & 31;
         }
-        // payload: [Dp/4][32][4] — 16-B chunk c4 of slot o
-        float4* dst = reinterpret_cast<float4*>(st.payload + (size_t)slab * kSlot * st.Dp);
+        float* dst = st.payload + (size_t)slab * kSlot * st.Dp;  // chunk c4 of slot o at pay_off()
         const float* xr = X + i * st.D;
         const int nc4 = st.Dp >> 2;
         float nrm = 0.f;
@@ -298,7 +297,7 @@ __global__ void __launch_bounds__(256) k_append(DevState st, const int64_t* __re
             for (int e = 0; e < 4; ++e) t[e] = (4 * c4 + e < st.D) ? xr[4 * c4 + e] : 0.f;
             v = make_float4(t[0], t[1], t[2], t[3]);
           }
-          dst[c4 * kSlot + o] = v;
+          *reinterpret_cast<float4*>(dst + pay_off(st.Dp, o, c4)) = v;
           nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nrm))));
           integral = integral && v.x == rintf(v.x) && v.y == rintf(v.y) && v.z == rintf(v.z) && v.w == rintf(v.w) &&
                      fabsf(v.x) <= 2048.f && fabsf(v.y) <= 2048.f && fabsf(v.z) <= 2048.f && fabsf(v.w) <= 2048.f;

@@ -9,34 +9,37 @@
 //
 // Why groups of 4 slabs: one MMA re-reads the whole A tile, so an N=32 (one
 // slab) instruction costs as much as N=128 (tools/mma_probe.cu).  The B
-// operand must be K-major SWIZZLE_NONE with a uniform 8-row-group stride, i.e.
-// [Dp/4][4 slabs][32 slots][4 floats].  The slab payload is [Dp/4][32][4]:
-// viewed as a 2-D tensor of 512-B rows (row = slab * Dp/4 + c4) a TMA
-// tile::gather4 of rows {s0,s1,s2,s3} * Dp/4 + c4 lands exactly the c4-th
-// 2-KB slice of that interleaved layout, so Dp/4 gather4 instructions per
-// group build the operand straight from HBM (tools/g4_probe.cu: layout
-// checked, 6.9 TB/s streaming random groups).  No shared-memory transpose.
+// operand must be K-major SWIZZLE_NONE with a uniform 8-row-group stride.  The
+// slab payload is stored as exactly that (pay_off(): [4 row groups][Dp/4][8
+// slots][4 dims], LBO = 128 B, SBO = 32 Dp B), so each slab of a group is ONE
+// contiguous cp.async.bulk of 16 KB into consecutive stage slots and the four
+// together are the N = 128 operand.  No gather, no shared-memory transpose;
+// bulk copies stream 2x faster than TMA tile::gather4 from L2 and the same
+// from HBM (tools/g4_probe.cu).
 //
 // Roles (1 persistent CTA per SM, 10 warps, no CTA-wide barrier after setup;
 // every hand-off is an mbarrier):
 //   warp 0      producer: claims work items (one ahead, published in a
 //               4-entry item ring), walks the list's slab directory, keeps
 //               the live slabs (bitmap != 0, Eq. slot_valid at slab
-//               granularity) and issues gather4 + bulk copies of ids/norms
-//               into an nst-stage group ring
+//               granularity) and issues bulk copies of the slab payloads,
+//               slot norms and ids into an nst-stage group ring
 //   warp 1      MMA: per group turns the bitmap into a NaN mask on the slot
 //               norms (group metadata for the epilogue), then one lane
 //               issues Dp/8 tcgen05.mma into one of two TMEM accumulators;
 //               tcgen05.commit frees the stage and signals the epilogue
 //   warps 2-5   query loaders: load the next item's 128 query rows into the
-//               spare one of two TMEM A buffers (double-buffered across
-//               items) with ||q||^2 and an integrality flag
+//               shared-memory A tile once the previous item's MMAs are done
+//               (the first half of each row is in registers by then), with
+//               ||q||^2 and an integrality flag.  A sits in shared memory, not
+//               TMEM: kind::tf32 with A in TMEM issues at half the rate
+//               (142 vs 71.5 cycles per 128x128x8 MMA, tools/mma_probe.cu)
 //   warps 6-9   epilogue: thread = query row (TMEM lane); per slab,
 //               t = ||x||^2 - 2 q.x is one FFMA and the slab's filter one
 //               FMNMX per candidate; only chunks whose min passes the row's
 //               threshold take the per-lane slow path (exact distance, then
 //               a sorted register top-k of (dist, id) keys)
-// TMEM columns: A[0] [0,128), A[1] [128,256), D[0] [256,384), D[1] [384,512).
+// TMEM columns: D[b] = [128 b, 128 b + 128), b < NB = 4.  The query tile (A) is in shared memory.
 //
 // Exactness (BASELINE.json tolerances): when query and slab values are
 // integers with |v| <= 2048 (tf32-exact; slab flag set by k_append) and
@@ -63,7 +66,8 @@ constexpr int TM = 128;   // queries per tile (TMEM lanes, UMMA M)
 constexpr int GS = 4;     // slabs per group (UMMA N = 128)
 constexpr int GN = GS * kSlot;
 constexpr int NITEM = 4;  // work-item ring
-constexpr int MAXST = 6;  // group ring depth cap
+constexpr int NB = 4;     // TMEM accumulator buffers (4 x 128 columns)
+constexpr int MAXST = NB; // group ring depth cap (stages are freed through the accumulator barriers)
 constexpr int NLD = 4, NEPI = 8;
 constexpr int W_SCHED = 0, W_MMA = 1, W_LD0 = 2, W_EPI0 = W_LD0 + NLD, W_TMA = W_EPI0 + NEPI;
 constexpr int TTHREADS = 32 * (W_TMA + 1);
@@ -79,8 +83,8 @@ struct TcArgs {
   const int32_t* work_n;
   unsigned long long* partial;
   uint32_t* gthr;
-  int dbg;  // experiments only (SIVF_OPT_DEBUG): bit0 skip the slow path, bit1 skip the fast path
-  int copy_mode;  // B operand: 0 TMA tile::gather4; 1 cp.async by the 4 loader warps; 2 both (c4 halves)
+  int dbg;  // experiments only (SIVF_OPT_DEBUG): bit0 skip the slow path, bit1 skip the fast path,
+            // bit2 skip the MMAs, bit3 skip the B copies, bit4 skip the A loads
 };
 
 struct ItemRec {
@@ -111,19 +115,20 @@ struct QInfo {
 };
 
 struct TcPlan {
-  size_t stage_bytes, off_meta, off_gm, off_q, off_items, off_thr, off_mrg, off_bar, total;
+  size_t a_bytes, stage_bytes, off_meta, off_gm, off_q, off_items, off_thr, off_mrg, off_bar, total;
 };
 __host__ __device__ inline TcPlan tc_plan(int Dp, int nst, int KP) {
   TcPlan p;
+  p.a_bytes = (size_t)TM * Dp * 4;                                            // query tile (UMMA A), offset 0
   p.stage_bytes = ((size_t)GN * Dp * 4 + 2 * GN * 4 + 1023) & ~(size_t)1023;  // payload + slot norms + ids
-  p.off_meta = (size_t)nst * p.stage_bytes;
+  p.off_meta = p.a_bytes + (size_t)nst * p.stage_bytes;
   p.off_gm = p.off_meta + MAXST * sizeof(StageMeta);
-  p.off_q = p.off_gm + 2 * sizeof(GroupMeta);
+  p.off_q = p.off_gm + NB * sizeof(GroupMeta);
   p.off_items = p.off_q + 2 * TM * sizeof(QInfo);
   p.off_thr = p.off_items + NITEM * (sizeof(ItemRec) + MAXS * sizeof(uint2));
   p.off_mrg = p.off_thr + 2 * TM * 8;
   p.off_bar = p.off_mrg + (size_t)TM * KP * 8;
-  p.total = p.off_bar + (3 * MAXST + 8 + 2 * NITEM + 2) * 8 + 1024;  // + alignment slack
+  p.total = p.off_bar + (2 * MAXST + 2 * NB + 5 + 2 * NITEM + 2) * 8 + 1024;  // + alignment slack
   return p;
 }
 
@@ -180,13 +185,11 @@ __device__ unsigned long long g_scnt[4];  // slow-path entries, survivors, inser
 #endif
 
 template <int KP>
-__global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
+__global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const DevState& st = a.st;
   const int Dp = st.Dp, nq4 = Dp >> 2, nst = a.nst, k = a.k;
-  // dims [0, 4 c4_tma) of each group are gathered by TMA, the rest copied by the loader warps
-  const int c4_tma = a.copy_mode == 0 ? nq4 : a.copy_mode == 1 ? 0 : nq4 / 2;
   const TcPlan p = tc_plan(Dp, nst, KP);
   StageMeta* smeta = reinterpret_cast<StageMeta*>(smem + p.off_meta);
   GroupMeta* gm = reinterpret_cast<GroupMeta*>(smem + p.off_gm);
@@ -196,22 +199,23 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
   u64* thr_sh = reinterpret_cast<u64*>(smem + p.off_thr);    // [2][TM] (item << 32 | k-th bound bits)
   u64* mrg = reinterpret_cast<u64*>(smem + p.off_mrg);       // [TM][KP] half-list hand-over
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);  // [MAXST] producer -> MMA (tx bytes)
-  uint64_t* empty = full + MAXST;                                  // [MAXST] MMA commit -> producer
-  uint64_t* meta_full = empty + MAXST;                             // [MAXST] producer -> MMA (stage metadata)
-  uint64_t* d_full = meta_full + MAXST;                            // [2] MMA -> epilogue
-  uint64_t* grp_free = d_full + 2;                                 // [2] epilogue -> MMA
-  uint64_t* a_full = grp_free + 2;                                 // [2] loaders -> MMA, epilogue
-  uint64_t* a_free = a_full + 2;                                   // [2] MMA commit + epilogue -> loaders
-  uint64_t* item_full = a_free + 2;                                // [NITEM] scheduler -> all
+  uint64_t* meta_full = full + MAXST;                              // [MAXST] producer -> MMA (stage metadata)
+  uint64_t* d_full = meta_full + MAXST;                            // [NB] MMA commit -> epilogue, producer
+  uint64_t* grp_free = d_full + NB;                                // [NB] epilogue -> MMA
+  uint64_t* a_full = grp_free + NB;                                 // [2] loaders -> MMA, epilogue
+  uint64_t* q_free = a_full + 2;                                   // [2] epilogue -> loaders (QInfo buffer)
+  uint64_t* a_free = q_free + 2;                                   // [1] MMA commit -> loaders (shared A tile)
+  uint64_t* item_full = a_free + 1;                                // [NITEM] scheduler -> all
   uint64_t* item_empty = item_full + NITEM;                        // [NITEM] epilogue -> scheduler
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(item_empty + NITEM);
-  auto stage_x = [&](int s) { return reinterpret_cast<float*>(smem + (size_t)s * p.stage_bytes); };
+  auto stage_x = [&](int s) { return reinterpret_cast<float*>(smem + p.a_bytes + (size_t)s * p.stage_bytes); };
   auto stage_nrm = [&](int s) {
-    return reinterpret_cast<float*>(smem + (size_t)s * p.stage_bytes + (size_t)GN * Dp * 4);
+    return reinterpret_cast<float*>(smem + p.a_bytes + (size_t)s * p.stage_bytes + (size_t)GN * Dp * 4);
   };
   auto stage_id = [&](int s) {
-    return reinterpret_cast<uint32_t*>(smem + (size_t)s * p.stage_bytes + (size_t)GN * Dp * 4 + GN * 4);
+    return reinterpret_cast<uint32_t*>(smem + p.a_bytes + (size_t)s * p.stage_bytes + (size_t)GN * Dp * 4 + GN * 4);
   };
+  float* const a_tile = reinterpret_cast<float*>(smem);  // [TM/8][Dp/4][8][4] (pay_off layout)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef SIVF_TC_PROF
   long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -219,16 +223,18 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
 #endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < MAXST; ++i) {
-      mbar_init(&full[i], a.copy_mode == 0 ? 1 : a.copy_mode == 1 ? 32 * NLD : 32 * NLD + 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&full[i], 1);
       mbar_init(&meta_full[i], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(&d_full[b], 2);
       mbar_init(&grp_free[b], NEPI);
-      mbar_init(&a_full[b], NLD);
-      mbar_init(&a_free[b], 1 + NEPI);
     }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&a_full[b], NLD);
+      mbar_init(&q_free[b], NEPI);
+    }
+    mbar_init(a_free, 1);
     for (int i = 0; i < NITEM; ++i) {
       mbar_init(&item_full[i], 1);
       mbar_init(&item_empty[i], NEPI);
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     fence_mbar_init();
   }
   for (int t = threadIdx.x; t < 2 * TM; t += blockDim.x) thr_sh[t] = ~0ull;  // tag matches no item
-  if (warp == W_MMA) tmem_alloc(tmem_holder, 512);
+  if (warp == W_MMA) tmem_alloc(tmem_holder, 32 * GS * NB);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -296,17 +302,18 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     uint32_t my_bm = 0u, my_fl = 0u;
     auto emit = [&](int base, int nvalid, int last) {
       const int stg = (int)(gseq % (uint32_t)nst);
-      if (lane == 0) PW(1, mbar_wait(&empty[stg], ((gseq / (uint32_t)nst) & 1u) ^ 1u));
+      // the stage is free once group gseq - nst has completed: its accumulator
+      // commit (d_full, the group's only tcgen05.commit) also frees its stage;
+      // nst <= NB, so that barrier cannot have moved on to a later phase
+      if (lane == 0 && gseq >= (uint32_t)nst) {
+        const uint32_t g0 = gseq - (uint32_t)nst;
+        PW(1, mbar_wait(&d_full[g0 % NB], (g0 / NB) & 1u));
+      }
       if (lane == 0) TR(0, gseq, clock64());
       __syncwarp();
       const int sl = __shfl_sync(kFull, my_s, base + (lane & 3));
       const uint32_t bmv = __shfl_sync(kFull, my_bm, base + (lane & 3));
       const uint32_t flv = __shfl_sync(kFull, my_fl, base + (lane & 3));
-      const int s0 = nvalid > 0 ? __shfl_sync(kFull, sl, 0) : 0;
-      const int sp = (lane & 3) < nvalid ? sl : s0;  // padding positions re-read a real slab (masked)
-      int sj[GS];
-#pragma unroll
-      for (int j = 0; j < GS; ++j) sj[j] = __shfl_sync(kFull, sp, j);
       StageMeta& m = smeta[stg];
       if (lane < GS) {
         m.slab[lane] = lane < nvalid ? sl : -1;
@@ -315,14 +322,20 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
       }
       if (lane == 0) m.last = last;
       __syncwarp();
+      const uint32_t sbytes = (uint32_t)(kSlot * Dp * 4);
       if (lane == 0) {
-        mbar_arrive(&meta_full[stg]);  // the MMA warp fetches the slot norms while the payload is in flight
-        if (a.copy_mode != 1) mbar_arrive_expect_tx(&full[stg], (uint32_t)c4_tma * 2048u);
+        mbar_arrive(&meta_full[stg]);
+        mbar_arrive_expect_tx(&full[stg], (a.dbg & 8) ? 0u : (uint32_t)nvalid * (sbytes + 2u * kSlot * 4u));
       }
       __syncwarp();
-      if (a.copy_mode != 1 && lane < c4_tma)
-        tma_gather4(stage_x(stg) + lane * 512, &tmap, 0, sj[0] * nq4 + lane, sj[1] * nq4 + lane,
-                    sj[2] * nq4 + lane, sj[3] * nq4 + lane, &full[stg]);
+      if (a.dbg & 8) nvalid = 0;  // experiment: no B traffic
+      // padding positions are not copied: their stale (finite) or uninitialised
+      // columns only reach D columns whose slot norm is the NaN mask
+      if (lane < nvalid) {
+        bulk_g2s(stage_x(stg) + (size_t)lane * kSlot * Dp, st.payload + (size_t)sl * kSlot * Dp, sbytes, &full[stg]);
+        bulk_g2s(stage_nrm(stg) + lane * kSlot, st.slab_norm + (size_t)sl * kSlot, kSlot * 4, &full[stg]);
+        bulk_g2s(stage_id(stg) + lane * kSlot, st.slab_ids + (size_t)sl * kSlot, kSlot * 4, &full[stg]);
+      }
       ++gseq;
     };
     int cnt = 0;
@@ -349,7 +362,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     };
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      mbar_wait(&item_full[slot], (i / NITEM) & 1u);
+      PW(4, mbar_wait(&item_full[slot], (i / NITEM) & 1u));
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       cnt = 0;
@@ -393,38 +406,31 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     uint32_t gseq = 0;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      mbar_wait(&item_full[slot], (i / NITEM) & 1u);
+      PW(6, mbar_wait(&item_full[slot], (i / NITEM) & 1u));
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       const uint32_t ab = i & 1u;
       PW(1, mbar_wait(&a_full[ab], (i >> 1) & 1u));
       for (;;) {
         const int stg = (int)(gseq % (uint32_t)nst);
-        const uint32_t b = gseq & 1u;
-        mbar_wait(&meta_full[stg], (gseq / (uint32_t)nst) & 1u);
+        const uint32_t b = gseq % NB;
+        PW(0, mbar_wait(&meta_full[stg], (gseq / (uint32_t)nst) & 1u));
         const StageMeta& sm = smeta[stg];
         float xnv[GS];
         uint32_t idv[GS];
-        if (!a.copy_mode) {
-#pragma unroll
-          for (int j = 0; j < GS; ++j) {  // slot norms and ids: their latency hides behind the payload's
-            const size_t o = (size_t)(sm.slab[j] >= 0 ? sm.slab[j] : 0) * kSlot + lane;
-            xnv[j] = __ldg(st.slab_norm + o);
-            idv[j] = __ldg(st.slab_ids + o);
-          }
-        }
         PW(2, mbar_wait(&full[stg], (gseq / (uint32_t)nst) & 1u));
         if (lane == 0) TR(1, gseq, clock64());
-        if (a.copy_mode) {  // staged with the payload by the copy warps
 #pragma unroll
-          for (int j = 0; j < GS; ++j) {
-            xnv[j] = stage_nrm(stg)[j * kSlot + lane];
-            idv[j] = stage_id(stg)[j * kSlot + lane];
-          }
+        for (int j = 0; j < GS; ++j) {  // staged with the payload (garbage at padding positions: masked)
+          xnv[j] = stage_nrm(stg)[j * kSlot + lane];
+          idv[j] = stage_id(stg)[j * kSlot + lane];
         }
-        PW(3, mbar_wait(&grp_free[b], ((gseq >> 1) & 1u) ^ 1u));
+        PW(3, mbar_wait(&grp_free[b], ((gseq / NB) & 1u) ^ 1u));
         if (lane == 0) TR(2, gseq, clock64());
         GroupMeta& g = gm[b];
+#ifdef SIVF_TC_PROF
+        long long _tm0 = clock64();
+#endif
 #pragma unroll
         for (int j = 0; j < GS; ++j) {
           const bool v = ((sm.bm[j] >> lane) & 1u) != 0u;
@@ -441,34 +447,41 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
         const int last = sm.last;
         if (lane == 0) g.last = last;
         __syncwarp();
+#ifdef SIVF_TC_PROF
+        pw[5] += clock64() - _tm0;
+        _tm0 = clock64();
+#endif
         if (lane == 0) {
           tc_fence_after();
-          if (a.copy_mode) fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05.mma (async proxy)
-          const uint32_t bsm = smem_u32(stage_x(stg));
-          const uint32_t dt = tbase + 256u + b * 128u, at = tbase + ab * 128u;
+          const uint32_t bsm = smem_u32(stage_x(stg)), asm_ = smem_u32(a_tile);
+          const uint32_t dt = tbase + b * 128u;
+          // A and B both K-major SWIZZLE_NONE in shared memory (kind::tf32 from
+          // TMEM A runs at half this rate: tools/mma_probe.cu)
           for (int kk = 0; kk < ((a.dbg & 4) ? 0 : (Dp >> 3)); ++kk)
-            umma_tf32_ts(dt, at + (uint32_t)(8 * kk),
-                         umma_sdesc(bsm + (uint32_t)kk * 2u * GN * 16u, (uint32_t)GN * 16u, 128u), idesc,
-                         kk > 0 ? 1u : 0u);
-          umma_commit(&empty[stg]);   // stage may be refilled once these MMAs have read it
-          umma_commit(&d_full[b]);    // accumulator ready
+            umma_tf32_ss(dt, umma_sdesc(asm_ + (uint32_t)kk * 256u, 128u, (uint32_t)Dp * 32u),
+                         umma_sdesc(bsm + (uint32_t)kk * 256u, 128u, (uint32_t)Dp * 32u), idesc, kk > 0 ? 1u : 0u);
+          umma_commit(&d_full[b]);    // accumulator ready and stage stg free (one commit per group:
+                                      // each tcgen05.commit costs ~200 cycles of tensor pipe, mma_probe)
           mbar_arrive(&d_full[b]);    // group metadata written
-          if (last) umma_commit(&a_free[ab]);
+          if (last) umma_commit(a_free);  // the A tile may be overwritten
         }
         __syncwarp();
+#ifdef SIVF_TC_PROF
+        pw[4] += clock64() - _tm0;
+#endif
         ++gseq;
         if (last) break;
       }
     }
   } else if (warp < W_EPI0) {
     // ------------------------------------------------------------ query loaders
-    // thread = query row (TMEM lane); rows are loaded 64 dims at a time, the
-    // first half before the A buffer is free (its latency hides behind the
-    // wait), then ||q||^2, an integrality flag and tcgen05.st into A[ab]
+    // thread = query row; rows are loaded 64 dims at a time, the first half
+    // before the shared A tile is free (the previous item's MMAs done: its
+    // latency hides behind the wait), then ||q||^2, an integrality flag and
+    // 16-B stores into the K-major A tile
     const int qw = warp & 3, row = 32 * qw + lane;
     const bool vec = (st.D & 3) == 0;
     const int nc8 = Dp >> 3;
-    uint32_t cseq = 0;  // group sequence (copy mode)
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
       mbar_wait(&item_full[slot], (i / NITEM) & 1u);
@@ -479,7 +492,6 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
       const bool wv = 32 * qw < rec.nqt && !(a.dbg & 16);  // warp-uniform: the warp has a real row
       const int pair = rv ? a.inv_pairs[rec.p0 + row] : -1;
       const float* qr = a.Q + (int64_t)(rv ? pair / a.nprobe : 0) * st.D;
-      const uint32_t ta = tbase + ((uint32_t)(32 * qw) << 16) + ab * 128u;
       float nrm = 0.f;
       uint32_t integ = 1u;
 #ifdef SIVF_TC_PROF
@@ -503,7 +515,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
           for (int e = 0; e < 8; ++e) v[u][e] = __float_as_uint(x[e]);
         }
         if (h0 == 0) {
-          PW(4, mbar_wait(&a_free[ab], ((i >> 1) & 1u) ^ 1u));
+          PW(4, mbar_wait(a_free, (i & 1u) ^ 1u));
           tc_fence_after();
         }
 #pragma unroll
@@ -515,54 +527,23 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
               nrm = fmaf(x, x, nrm);
               integ &= (x == rintf(x) ? 1u : 0u) & (fabsf(x) <= 2048.f ? 1u : 0u);
             }
-            if (wv) tmem_st8(ta + (uint32_t)(8 * (h0 + u)), v[u]);
+            if (wv) {
+              const int c4 = 2 * (h0 + u);
+              *reinterpret_cast<uint4*>(a_tile + pay_off(Dp, row, c4)) = make_uint4(v[u][0], v[u][1], v[u][2], v[u][3]);
+              *reinterpret_cast<uint4*>(a_tile + pay_off(Dp, row, c4 + 1)) =
+                  make_uint4(v[u][4], v[u][5], v[u][6], v[u][7]);
+            }
           }
         }
       }
 #ifdef SIVF_TC_PROF
       pw[1] += clock64() - _tl0;
-      _tl0 = clock64();
 #endif
-      tmem_st_wait();
-#ifdef SIVF_TC_PROF
-      pw[2] += clock64() - _tl0;
-#endif
+      fence_proxy_async_smem();  // generic-proxy stores -> tcgen05.mma (async proxy)
+      PW(2, mbar_wait(&q_free[ab], ((i >> 1) & 1u) ^ 1u));  // the epilogue is done with item i - 2's QInfo
       qinfo[ab * TM + row] = QInfo{nrm, pair, integ, 0u};
-      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_full[ab]);
-      if (a.copy_mode) {
-        // B operand of this item's groups: warp qw copies group position qw (one slab),
-        // lane = slot, one 16-B cp.async per 4 dims into the interleaved layout
-        // [Dp/4][4 slabs][32 slots][4]; completion arrives on full[stg] (no tx count)
-        for (;;) {
-          const int stg = (int)(cseq % (uint32_t)nst);
-          mbar_wait(&meta_full[stg], (cseq / (uint32_t)nst) & 1u);
-          const StageMeta& sm = smeta[stg];
-          const int sl = sm.slab[qw];
-          const int last = sm.last;
-          if (sl >= 0) {
-            const float* src = st.payload + (size_t)sl * kSlot * Dp + lane * 4;
-            const uint32_t dst = smem_u32(stage_x(stg)) + (uint32_t)(qw * 512 + lane * 16);
-#pragma unroll 8
-            for (int c4 = c4_tma; c4 < nq4; ++c4)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (uint32_t)c4 * 2048u),
-                           "l"(src + (size_t)c4 * 128)
-                           : "memory");
-            if (lane < 16) {  // the slab's 32 slot norms (lanes 0-7) and ids (lanes 8-15)
-              const uint32_t nd = lane < 8 ? smem_u32(stage_nrm(stg) + qw * kSlot + 4 * lane)
-                                           : smem_u32(stage_id(stg) + qw * kSlot + 4 * (lane - 8));
-              const void* ns = lane < 8 ? (const void*)(st.slab_norm + (size_t)sl * kSlot + 4 * lane)
-                                        : (const void*)(st.slab_ids + (size_t)sl * kSlot + 4 * (lane - 8));
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(nd), "l"(ns) : "memory");
-            }
-          }
-          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[stg]))
-                       : "memory");
-          ++cseq;
-          if (last) break;
-        }
-      }
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -575,7 +556,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
     uint32_t gseq = 0;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      mbar_wait(&item_full[slot], (i / NITEM) & 1u);
+      PW(4, mbar_wait(&item_full[slot], (i / NITEM) & 1u));
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       const uint32_t ab = i & 1u;
@@ -592,8 +573,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
       for (int t = 0; t < KP; ++t) keys[t] = t < KP - k ? 0ull : kPadKey;  // k-th = keys[KP-1]
       u64 kth = kPadKey;
       for (;;) {
-        const uint32_t b = gseq & 1u;
-        PW(5, mbar_wait(&d_full[b], (gseq >> 1) & 1u));
+        const uint32_t b = gseq % NB;
+        PW(5, mbar_wait(&d_full[b], (gseq / NB) & 1u));
         if (lane == 0 && warp == W_EPI0 + 2) TR(3, gseq, clock64());
         if (lane == 0 && warp == W_EPI0 + 6) TR(5, gseq, clock64());
         tc_fence_after();
@@ -661,7 +642,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
                 const float* qr = a.Q + (int64_t)qglob * st.D;
                 float acc = 0.f;
                 for (int i4 = 0; i4 < nq4; ++i4) {
-                  const float4 xv = __ldg(reinterpret_cast<const float4*>(xs + (i4 * kSlot + c) * 4));
+                  const float4 xv = __ldg(reinterpret_cast<const float4*>(xs + pay_off(Dp, c, i4)));
                   float qv[4];
 #pragma unroll
                   for (int e = 0; e < 4; ++e) qv[e] = 4 * i4 + e < st.D ? __ldg(qr + 4 * i4 + e) : 0.f;
@@ -692,7 +673,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
             pw[6] += clock64() - _ts;
 #endif
           };
-          const uint32_t dcol = tbase + ((uint32_t)(32 * qw) << 16) + 256u + b * 128u + (uint32_t)(64 * h);
+          const uint32_t dcol = tbase + ((uint32_t)(32 * qw) << 16) + b * 128u + (uint32_t)(64 * h);
 #ifdef SIVF_TC_PROF
           long long _tg = clock64();
 #endif
@@ -702,8 +683,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
 #ifdef SIVF_TC_PROF
             long long _tq = clock64();
 #endif
-            tmem_ld32(dcol + 32u * (uint32_t)jj, v);
-            tmem_ld_wait();
+            if (!(a.dbg & 32)) {
+              tmem_ld32(dcol + 32u * (uint32_t)jj, v);
+              tmem_ld_wait();
+            } else {
+#pragma unroll
+              for (int c = 0; c < 32; ++c) v[c] = 0x7f800000u;
+            }
 #ifdef SIVF_TC_PROF
             pw[3] += clock64() - _tq;
 #endif
@@ -746,7 +732,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
       }
       named_bar_sync(1 + qw, 64);
       if (lane == 0) {
-        mbar_arrive(&a_free[ab]);
+        mbar_arrive(&q_free[ab]);
         mbar_arrive(&item_empty[slot]);
       }
     }
@@ -759,7 +745,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == W_MMA) tmem_dealloc(tbase, 512);
+  if (warp == W_MMA) tmem_dealloc(tbase, 32 * GS * NB);
 }
 
 
@@ -770,7 +756,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(const __grid_constant__
 // prunes work, never results.  The difference form here and the scan's
 // distances may round differently (each within (Dp+2) 2^-24 relative of the
 // exact value), so the bound is inflated by (1 + (Dp+2) 2^-23), rounded up.
-// Warp per query; lane = slot; slab payload loads are 512-B coalesced.
+// Warp per query; lane = slot; slab payload loads are 4 full 128-B lines per chunk.
 __global__ void __launch_bounds__(128) k_seed_bound(DevState st, const float* __restrict__ Q, int64_t nq,
                                                     int nprobe, const int32_t* __restrict__ probes, int nseed,
                                                     int k, uint32_t* __restrict__ gthr) {
@@ -794,12 +780,12 @@ __global__ void __launch_bounds__(128) k_seed_bound(DevState st, const float* __
     const uint32_t bm = st.bitmap[s];
     if (!bm) continue;
     ++used;
-    const float4* xs = reinterpret_cast<const float4*>(st.payload + (size_t)s * kSlot * Dp);
+    const float* xs = st.payload + (size_t)s * kSlot * Dp;
     const float4* q4 = reinterpret_cast<const float4*>(qs[w]);
     float acc = 0.f;
 #pragma unroll 8
     for (int c4 = 0; c4 < nq4; ++c4) {
-      const float4 xv = __ldg(xs + c4 * kSlot + lane);
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(xs + pay_off(Dp, lane, c4)));
       const float4 qv = q4[c4];
       float t;
       t = qv.x - xv.x; acc = fmaf(t, t, acc);
@@ -815,10 +801,6 @@ __global__ void __launch_bounds__(128) k_seed_bound(DevState st, const float* __
   if (lane == 0 && kth != kPadKey) atomicMin(&gthr[q], __float_as_uint(key_dist(kth)));
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 // register top-k width: the insertion network costs O(KP) per survivor
 inline int scan_kp(int k) { return k <= 12 ? 12 : k <= 16 ? 16 : 32; }
 
@@ -827,44 +809,27 @@ int tc_stages(const Index& ix, int KP) {
   const size_t fixed = tc_plan(ix.st.Dp, 0, KP).total;
   if (ix.smem_optin < fixed) return 0;
   int n = (int)((ix.smem_optin - fixed) / sb);
-  return n > MAXST ? MAXST : n;
+  return n > NB ? NB : n;  // the producer reuses the accumulator barriers: nst <= NB
 }
 
 }  // namespace
 
 bool scan_tc_supported(const Index& ix, int k) {
-  return ix.st.Dp <= 128 && k <= 32 && ix.payload_tmap_ok && tc_stages(ix, scan_kp(k)) >= 2;
+  return ix.st.Dp <= 128 && k <= 32 && tc_stages(ix, scan_kp(k)) >= 2;
 }
 
 cudaError_t setup_scan_tc(Index& ix) {
   if (ix.st.Dp > 128) return cudaSuccess;
-  if (tc_stages(ix, 32) < 2) return cudaSuccess;
-  // TMA descriptor of the payload as [num_slabs * Dp/4] rows x 128 floats (512 B)
-  EncodeTiledFn enc = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q) !=
-          cudaSuccess ||
-      enc == nullptr) {
-    cudaGetLastError();
-    return cudaSuccess;  // no TMA descriptor: the CUDA-core scan serves every search
-  }
-  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
-  const cuuint64_t gdim[2] = {128, (cuuint64_t)ix.st.num_slabs * (cuuint64_t)(ix.st.Dp >> 2)};
-  const cuuint64_t gstr[1] = {512};
-  const cuuint32_t box[2] = {128, 1};
-  const cuuint32_t estr[2] = {1, 1};
-  CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(ix.payload_tmap);
-  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ix.st.payload, gdim, gstr, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  ix.payload_tmap_ok = r == CUDA_SUCCESS;
-  if (!ix.payload_tmap_ok) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_scan_tc<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)tc_plan(ix.st.Dp, tc_stages(ix, 12), 12).total);
-  if (e == cudaSuccess)
+  // KP = 32 needs a larger merge buffer: with D = 128 only one group stage fits
+  // beside the shared A tile, and scan_tc_supported() sends k > 16 to the CUDA-core scan
+  cudaError_t e = cudaSuccess;
+  if (tc_stages(ix, 12) >= 2)
+    e = cudaFuncSetAttribute(k_scan_tc<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc_plan(ix.st.Dp, tc_stages(ix, 12), 12).total);
+  if (e == cudaSuccess && tc_stages(ix, 16) >= 2)
     e = cudaFuncSetAttribute(k_scan_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)tc_plan(ix.st.Dp, tc_stages(ix, 16), 16).total);
-  if (e == cudaSuccess)
+                             (int)tc_plan(ix.st.Dp, tc_stages(ix, 16), 16).total);
+  if (e == cudaSuccess && tc_stages(ix, 32) >= 2)
     e = cudaFuncSetAttribute(k_scan_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)tc_plan(ix.st.Dp, tc_stages(ix, 32), 32).total);
   return e;
@@ -874,13 +839,11 @@ cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaS
   Scratch& sc = ix.sc;
   const int KP = scan_kp(k);
   const int nst = tc_stages(ix, KP);
-  TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, ix.dbg,
-            ix.scan_copy_mode};
+  TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, ix.dbg};
   const size_t smem = tc_plan(ix.st.Dp, nst, KP).total;
-  const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(ix.payload_tmap);
-  if (KP == 12) k_scan_tc<12><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);
-  else if (KP == 16) k_scan_tc<16><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);
-  else k_scan_tc<32><<<ix.num_sms, TTHREADS, smem, s>>>(tm, a);
+  if (KP == 12) k_scan_tc<12><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+  else if (KP == 16) k_scan_tc<16><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+  else k_scan_tc<32><<<ix.num_sms, TTHREADS, smem, s>>>(a);
   ix.launches += 1;
   return cudaGetLastError();
 }

@@ -130,7 +130,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
             const bool last = c == nch - 1;
             meta[stg] = StageMeta{s, bm, c, last ? 1 : 0};
             mbar_arrive_expect_tx(&full[stg], cw * kSlot * 4 + (last ? kSlot * 4 : 0));
-            bulk_g2s(stage_x + stg * kCH * kSlot, src + (size_t)c * kCH * kSlot, cw * kSlot * 4, &full[stg]);
+            // dims [c kCH, c kCH + cw) of the slab: one piece per 8-slot row group
+            // (pay_off layout), staged as [4][kCH/4][8][4]
+            for (int r = 0; r < kSlot / 8; ++r)
+              bulk_g2s(stage_x + stg * kCH * kSlot + r * (kCH / 4) * 32, src + pay_off(Dp, 8 * r, c * (kCH / 4)),
+                       cw * 32, &full[stg]);
             if (last) bulk_g2s(stage_id + stg * kSlot, st.slab_ids + (size_t)s * kSlot, kSlot * 4, &full[stg]);
           }
         }
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
             const float4 qv = *reinterpret_cast<const float4*>(qc + 4 * i4);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float4 xv = *reinterpret_cast<const float4*>(xs + (i4 * kSlot + ls + 8 * j) * 4);
+              const float4 xv = *reinterpret_cast<const float4*>(xs + ((j * (kCH / 4) + i4) * 8 + ls) * 4);
               float t;
               t = qv.x - xv.x; acc[j] = fmaf(t, t, acc[j]);
               t = qv.y - xv.y; acc[j] = fmaf(t, t, acc[j]);

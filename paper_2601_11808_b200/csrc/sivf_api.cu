@@ -487,7 +487,6 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
     case SIVF_OPT_TC_COARSE: ix->use_tc_coarse = value != 0; return SIVF_OK;
     case SIVF_OPT_COARSE_SELECT: ix->coarse_select = value != 0; return SIVF_OK;
     case SIVF_OPT_RANK_SPLIT: ix->rank_split = value != 0; return SIVF_OK;
-    case 98: ix->scan_copy_mode = (int)value; return SIVF_OK;  // experiments: k_scan_tc B-operand copier
     case 99: ix->dbg = (int)value; return SIVF_OK;  // SIVF_OPT_DEBUG: experiments only
     case SIVF_OPT_SEED_SLABS:
       if (value < 0 || value > (1 << 20)) return SIVF_E_INVALID_ARG;

@@ -94,15 +94,12 @@ struct Index {
   bool fuse_inv_done = false;
   bool coarse_select = true;  // A-matrix + per-row selection coarse path (SIVF_OPT_COARSE_SELECT)
   bool rank_split = true;     // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT)
-  int scan_copy_mode = 2;     // k_scan_tc B operand: 0 TMA gather4, 1 cp.async by the loader warps, 2 both (c4 halves)
   int dbg = 0;                // experiment switches (SIVF_OPT_DEBUG)
   int seed_slabs = 0;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS; off: it costs more than it saves)
   int64_t launches = 0;
   // TMA descriptor (CUtensorMap, 128 B) of the payload viewed as rows of 512 B
   // (row = slab * Dp/4 + c4), box 128 floats x 1 row: the tile::gather4 source
   // of k_scan_tc (encoded once in setup_scan_tc; the payload never moves).
-  alignas(64) unsigned char payload_tmap[128] = {};
-  bool payload_tmap_ok = false;
   alignas(64) unsigned char coarse_tmap[128] = {};  // TMA store descriptor of sc.coarse (k_coarse_tc.cu)
   bool coarse_tmap_ok = false;
   alignas(64) unsigned char qcoarse_tmap[128] = {};  // TMA store descriptor of sc.qcoarse

@@ -10,6 +10,15 @@
 namespace sivf {
 
 constexpr int kSlot = 32;                          // slab capacity C = 32 ("align with the warp size")
+// Slab payload layout [kSlot/8 row groups][Dp/4 dim chunks][8 slots][4 dims]:
+// float offset of the 16-B dim chunk c4 of slot n inside its slab.  Each
+// (row group, chunk) pair is an 8 x 16 B core matrix, so a slab copied as one
+// contiguous block is a tcgen05 K-major SWIZZLE_NONE B operand (LBO = 128 B
+// along K, SBO = 32 Dp B per 8 slots), and 4 consecutive slabs are one N = 128
+// operand; lane = slot loads of a chunk touch 4 full 128-B lines.
+__host__ __device__ __forceinline__ size_t pay_off(int Dp, int n, int c4) {
+  return ((size_t)((n >> 3) * (Dp >> 2) + c4) * 8 + (n & 7)) * 4;
+}
 constexpr uint64_t kAttInvalid = ~0ull;            // INVALID sentinel (reading C14)
 constexpr int32_t kClaimEmpty = 0x7f7f7f7f;        // byte-memsettable "no claimant"
 constexpr uint64_t kPadKey = 0x7F800000FFFFFFFFull; // (+inf, id 0xFFFFFFFF): sorts after every real key
@@ -26,7 +35,7 @@ enum { I_FREE_TOP = 0, I_DIR_BUMP, I_WORK, I_NTILES, I_NICTR = 8 };
 struct DevState {
   int32_t D, Dp, nlist, G, rank;
   int64_t cap, cap_local, num_slabs;
-  float* payload;        // [num_slabs][Dp/4][32][4]  dim-interleaved: lane = slot loads are 16-B coalesced
+  float* payload;        // [num_slabs][4][Dp/4][8][4]  see pay_off(): a slab is one UMMA B core-matrix block
   uint32_t* slab_ids;    // [num_slabs][32] user ids (u32)
   float* slab_norm;      // [num_slabs][32] ||x||^2 (fp32), for the tensor-core distance expansion
   uint32_t* slab_flag;   // [num_slabs] bit0: every payload value is an integer with |x| <= 2048 (tf32-exact)

@@ -16,7 +16,6 @@ Q = torch.from_numpy(gen.queries(0, NQ)).cuda()
 two = int(os.environ.get("TWO_PHASE", "0"))
 ix.set_option(2, two)
 ix.set_option(99, int(os.environ.get("DBG", "0")))
-ix.set_option(98, int(os.environ.get("COPY", "2")))
 ix.set_option(5, int(os.environ.get("SPLIT", "1")))
 seeds = [int(v) for v in os.environ.get("SEEDS", "8").split(",")]
 for seed, npb in [(sd, npb) for sd in seeds for npb in (8, 32)]:

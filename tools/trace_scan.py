@@ -15,8 +15,8 @@ for b in range(0, N, 65536):
     ix.insert(ids[b:b+65536], X[b:b+65536])
 Q = torch.from_numpy(gen.queries(0, NQ)).cuda()
 ix.set_option(4, 0)
+ix.set_option(5, int(os.environ.get("SPLIT", "1")))
 ix.set_option(99, int(os.environ.get("DBG", "0")))
-ix.set_option(98, int(os.environ.get("COPY", "2")))
 for _ in range(3):
     ix.search(Q, 10, npb)
 torch.cuda.synchronize()
@@ -26,3 +26,13 @@ t0 = buf[0][0]
 print("rc", rc, "cols: g prod_issue full_seen mma_issue epi_start epi_end epi2_start (cycles rel. to first issue)")
 for g in range(0, 60):
     print(g, *[int(buf[r][g] - t0) if buf[r][g] else -1 for r in range(6)])
+# summary over the traced groups of block 0
+g = [i for i in range(1, 1024) if all(buf[r][i] for r in range(5))]
+if g:
+    a = np.array([[buf[r][i] for r in range(6)] for i in g], np.float64)
+    span = (a[-1, 2] - a[0, 2]) / max(1, len(g) - 1)
+    print(f"groups {len(g)}  mma_issue interval {span:.0f} cyc/group")
+    print(f"  issue->full   {np.median(a[:,1]-a[:,0]):.0f} (median)  p90 {np.percentile(a[:,1]-a[:,0],90):.0f}")
+    print(f"  full->mma     {np.median(a[:,2]-a[:,1]):.0f}  (grp_free wait)")
+    print(f"  mma->epi      {np.median(a[:,3]-a[:,2]):.0f}")
+    print(f"  epi duration  {np.median(a[:,4]-a[:,3]):.0f}  p90 {np.percentile(a[:,4]-a[:,3],90):.0f}")
