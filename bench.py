@@ -37,8 +37,8 @@ N_BASE, DIM, NLIST, BATCH, NQ, K, NPROBE = 1_000_000, 128, 1024, 10_000, 10_000,
 N_TRAIN, N_ITER, SEED = 262_144, 20, 0x51F7
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_scan_tc launch, from the committed ncu
 # --set full capture of this bench step (per launch; compare with roofline.hbm_view).
-SCAN_TRAFFIC_NCU = 1.126747e9 + 30.904576e6
-SCAN_TRAFFIC_SRC = "profiles/r01s3c_scan_full.txt (ncu --set full, bench.py --steps 1 --warmup 1 --no-extra)"
+SCAN_TRAFFIC_NCU = 571.517184e6 + 29.563136e6
+SCAN_TRAFFIC_SRC = "profiles/r01s4_scan_full.txt (ncu --set full, bench.py --steps 1 --warmup 1 --no-sweep --no-cpu --no-extra)"
 WORKLOAD = ("SIFT1M-shaped sliding step: 1M x 128 fp32 live window, nlist=1024; per step insert 10k new + "
             "delete 10k oldest + search 10k queries (k=10, nprobe=32) + reclaim")
 
@@ -482,22 +482,25 @@ def run_sivf(args):
     hbm_peak = float(mp.get("hbm_gbs", 6650.0))
     # tf32 dense peak = measured bf16 (sustained: the scan runs inside a long step) x nominal tf32/bf16 (1.1/2.25)
     tf32_peak = float(mp.get("bf16_tflops_sustained", 1400.0)) * (1.1 / 2.25)
+    # the scan's MMAs are kind::f16 (fp16 operands, fp32 accumulate): the bf16/fp16 dense peak
+    f16_peak = float(mp.get("bf16_tflops_sustained", 1400.0))
     scan_ms = ph_ms["scan"]
     uniq = torch.unique(probes).long()
-    uniq_bytes = float(lpl[uniq].sum().item()) * (4 * DIM + 8)
+    uniq_bytes = float(lpl[uniq].sum().item()) * (2 * DIM + 8)
     flops = 2.0 * DIM * cand  # q.x on the tensor cores (the norms are per-slot / per-query precomputes)
     achieved = flops / (scan_ms / 1e3) / 1e12 if scan_ms else 0.0
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
-                "frac": achieved / tf32_peak if tf32_peak else None, "traffic": SCAN_TRAFFIC_NCU,
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": f16_peak, "unit": "TFLOP/s",
+                "frac": achieved / f16_peak if f16_peak else None, "traffic": SCAN_TRAFFIC_NCU,
                 "traffic_source": SCAN_TRAFFIC_SRC,
-                "kernel": "k_scan_tc (tcgen05 kind::tf32)", "kernel_ms": scan_ms, "algorithmic_flops": flops,
+                "kernel": "k_scan_tc (tcgen05 kind::f16, fp16 slab copy)", "kernel_ms": scan_ms, "algorithmic_flops": flops,
                 "per_unit": "2*D flop per (query, probed live slot)", "candidates_per_launch": cand,
                 "unique_list_bytes": uniq_bytes,
                 "hbm_view": {"achieved_gbs": uniq_bytes / (scan_ms / 1e3) / 1e9 if scan_ms else None,
                              "peak_gbs": hbm_peak,
                              "frac": uniq_bytes / (scan_ms / 1e3) / 1e9 / hbm_peak if scan_ms else None,
-                             "per_unit": "4*D+8 B per live slot of each probed list, read once per step"},
-                "peak_note": "tf32 = MEASURED_PEAKS bf16_tflops_sustained x 1.1/2.25 (guide nominal ratio)"}
+                             "per_unit": "2*D+8 B per live slot of each probed list (fp16 copy, norm, id), read once per step"},
+                "peak_note": "kind::f16 = MEASURED_PEAKS bf16_tflops_sustained (same dense rate); the coarse and "
+                             "assign phases (split tf32) use x 1.1/2.25 (guide nominal ratio)"}
 
     def tfrac(fl, ms):
         return None if not ms else {"achieved_tflops": fl / (ms / 1e3) / 1e12, "frac": fl / (ms / 1e3) / 1e12 / tf32_peak}

@@ -193,9 +193,12 @@ enum {
 sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
 
 /* Kernel-path switches (tests compare every path against the oracle).
- *   SIVF_OPT_TC_SCAN   (default 1): slab scan on tcgen05 tensor cores when
- *                      the padded dim <= 256 and k <= 32; 0 = CUDA-core scan.
- *   SIVF_OPT_TC_TWO_PHASE (default 0): scan every query's nearest list first.
+ *   SIVF_OPT_TC_SCAN   (default 1): slab scan on tcgen05 tensor cores (kind::f16
+ *                      over the fp16 slab copy) when dim <= 128 and k <= 32;
+ *                      0 = CUDA-core scan.
+ *   SIVF_OPT_TC_TWO_PHASE (default 0): value r0 >= 1 scans every query's r0 nearest
+ *                      lists in a first launch and the rest in a second (bounds
+ *                      complete before the second phase); 0 = one launch.
  *   SIVF_OPT_TC_COARSE (default 1): assignment and probe selection (nprobe <= 32)
  *                      on tcgen05 tensor cores with a certified band and exact
  *                      dist32 re-rank (bit-identical result); 0 = exact CUDA-core

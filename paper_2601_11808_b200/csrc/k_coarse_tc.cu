@@ -646,11 +646,12 @@ struct InvCount {
   int32_t* cnt;
   uint32_t* gthr;
   int nb, r0;
+  int keep = 0;  // experiments (SIVF_OPT_DEBUG bit 6): keep the previous search's bounds
 };
 __device__ __forceinline__ void inv_count_row(const InvCount& ic, int nlist, int64_t row, int j, int32_t l) {
   if (!ic.cnt) return;
   atomicAdd(&ic.cnt[((ic.nb == 2 && j >= ic.r0) ? nlist : 0) + l], 1);
-  if (j == 0) ic.gthr[row] = 0x7F800000u;
+  if (j == 0 && !ic.keep) ic.gthr[row] = 0x7F800000u;
 }
 #ifdef SIVF_TC_PROF
 __device__ unsigned g_selhist[2][64];
@@ -1008,7 +1009,7 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
   else                                                                                                         \
     k_coarse_select<NPL, 1><<<g, 32 * SELW, ssm, s>>>(mat, xr, nr, D, st.nlist, m, xn, sc.c_csa,  \
                                                        sc.c_cnb, bd.kb, st.centroids, Dp, nullptr, probes + r0 * m, m, 1, \
-                                                       InvCount{ix.fuse_inv_cnt, ix.sc.gthr + r0, ix.fuse_nb, ix.fuse_r0});
+                                                       InvCount{ix.fuse_inv_cnt, ix.sc.gthr + r0, ix.fuse_nb, ix.fuse_r0, (ix.dbg >> 6) & 1});
       if (st.nlist <= 256) {
         SIVF_SEL(8)
       } else if (st.nlist <= 512) {

@@ -16,6 +16,8 @@
 //                  directory, initialise their metadata
 //   k_append       warp per item: payload, id, ATT entry, then the validity
 //                  bit is published with a release fence
+#include <cuda_fp16.h>
+
 #include "sivf_host.h"
 
 namespace sivf {
@@ -236,7 +238,7 @@ __global__ void k_dir_update(DevState st, const int32_t* __restrict__ cnt, const
     st.dir_arena[off + len + j] = s;
     st.bitmap[s] = 0u;  // P:312 validity_bitmap <- 0
     st.slab_list[s] = l;
-    st.slab_flag[s] = 1u;  // integral until an appended vector says otherwise
+    st.slab_flag[s] = kFlagIntegral;  // integral (and fp16-finite) until an appended vector says otherwise
     int fill = rem - kSlot * j;
     st.cursor[s] = (uint32_t)(fill > kSlot ? kSlot : fill);
   }
@@ -286,7 +288,8 @@ __global__ void __launch_bounds__(256) k_append(DevState st, const int64_t* __re
         const float* xr = X + i * st.D;
         const int nc4 = st.Dp >> 2;
         float nrm = 0.f;
-        bool integral = true;
+        bool integral = true, over = false;
+        uint16_t* dst16 = st.payload16 ? st.payload16 + (size_t)slab * kSlot * st.Dh : nullptr;
         for (int c4 = lane; c4 < nc4; c4 += 32) {
           float4 v;
           if ((st.D & 3) == 0 && 4 * c4 + 3 < st.D) {
@@ -298,16 +301,28 @@ __global__ void __launch_bounds__(256) k_append(DevState st, const int64_t* __re
             v = make_float4(t[0], t[1], t[2], t[3]);
           }
           *reinterpret_cast<float4*>(dst + pay_off(st.Dp, o, c4)) = v;
+          if (dst16) {  // fp16 (RN) scan copy: 4 halves = one half of a 16-B chunk
+            const __half2 h01 = __floats2half2_rn(v.x, v.y), h23 = __floats2half2_rn(v.z, v.w);
+            *reinterpret_cast<uint2*>(dst16 + pay16_off(st.Dh, o, c4 >> 1) + 4 * (c4 & 1)) =
+                make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+            over = over || !(fabsf(v.x) <= 65504.f && fabsf(v.y) <= 65504.f && fabsf(v.z) <= 65504.f &&
+                             fabsf(v.w) <= 65504.f);
+          }
           nrm = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nrm))));
           integral = integral && v.x == rintf(v.x) && v.y == rintf(v.y) && v.z == rintf(v.z) && v.w == rintf(v.w) &&
                      fabsf(v.x) <= 2048.f && fabsf(v.y) <= 2048.f && fabsf(v.z) <= 2048.f && fabsf(v.w) <= 2048.f;
         }
+        if (dst16)  // zero dims [Dp, Dh) of the fp16 copy
+          for (int c4 = nc4 + lane; c4 < (st.Dh >> 2); c4 += 32)
+            *reinterpret_cast<uint2*>(dst16 + pay16_off(st.Dh, o, c4 >> 1) + 4 * (c4 & 1)) = make_uint2(0u, 0u);
 #pragma unroll
         for (int off = 16; off; off >>= 1) nrm += __shfl_xor_sync(kFull, nrm, off);
         integral = __all_sync(kFull, integral);
+        over = __any_sync(kFull, over);
         if (lane == 0) {
           st.slab_norm[(size_t)slab * kSlot + o] = nrm;
-          if (!integral) atomicAnd(&st.slab_flag[slab], 0u);
+          if (!integral) atomicAnd(&st.slab_flag[slab], ~kFlagIntegral);
+          if (over) atomicOr(&st.slab_flag[slab], kFlagF16Over);
           st.slab_ids[(size_t)slab * kSlot + o] = (uint32_t)ids[i];
           st.att[u] = ((uint64_t)(uint32_t)slab << 32) | (uint32_t)o;  // Eq. att_encoding
           st.claim[u] = kClaimEmpty;

@@ -53,6 +53,7 @@
 // thr is the row's current k-th distance, seeded from a per-query bound
 // (atomicMin of the k-th distance of finished items of the same query).
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <cstdio>
 
@@ -65,8 +66,9 @@ namespace {
 constexpr int TM = 128;   // queries per tile (TMEM lanes, UMMA M)
 constexpr int GS = 4;     // slabs per group (UMMA N = 128)
 constexpr int GN = GS * kSlot;
-constexpr int NITEM = 4;  // work-item ring
-constexpr int NB = 4;     // TMEM accumulator buffers (4 x 128 columns)
+constexpr int NITEM = 8;  // work-item ring
+constexpr int NQI = 4;    // QInfo buffers: the loaders may run NQI items ahead of the epilogue
+constexpr int NB = 3;     // TMEM accumulator buffers (3 x 128 columns after the two 64-column A buffers)
 constexpr int MAXST = NB; // group ring depth cap (stages are freed through the accumulator barriers)
 constexpr int NLD = 4, NEPI = 8;
 constexpr int W_SCHED = 0, W_MMA = 1, W_LD0 = 2, W_EPI0 = W_LD0 + NLD, W_TMA = W_EPI0 + NEPI;
@@ -83,6 +85,7 @@ struct TcArgs {
   const int32_t* work_n;
   unsigned long long* partial;
   uint32_t* gthr;
+  int phase;  // 0: every work item; 1: bucket 0 only; 2: bucket 1 only (phased scan)
   int dbg;  // experiments only (SIVF_OPT_DEBUG): bit0 skip the slow path, bit1 skip the fast path,
             // bit2 skip the MMAs, bit3 skip the B copies, bit4 skip the A loads
 };
@@ -110,25 +113,24 @@ struct GroupMeta {
 struct QInfo {
   float qn;
   int32_t pair;
-  uint32_t qint;
-  uint32_t pad;
+  uint32_t qint;  // every value an integer with |v| <= 2048 (exact in fp16)
+  uint32_t qover; // some |v| > 65504: no finite fp16 copy, every candidate is re-ranked
 };
 
 struct TcPlan {
-  size_t a_bytes, stage_bytes, off_meta, off_gm, off_q, off_items, off_thr, off_mrg, off_bar, total;
+  size_t stage_bytes, off_meta, off_gm, off_q, off_items, off_thr, off_mrg, off_bar, total;
 };
-__host__ __device__ inline TcPlan tc_plan(int Dp, int nst, int KP) {
+__host__ __device__ inline TcPlan tc_plan(int Dh, int nst, int KP) {
   TcPlan p;
-  p.a_bytes = (size_t)TM * Dp * 4;                                            // query tile (UMMA A), offset 0
-  p.stage_bytes = ((size_t)GN * Dp * 4 + 2 * GN * 4 + 1023) & ~(size_t)1023;  // payload + slot norms + ids
-  p.off_meta = p.a_bytes + (size_t)nst * p.stage_bytes;
+  p.stage_bytes = ((size_t)GN * Dh * 2 + 2 * GN * 4 + 1023) & ~(size_t)1023;  // fp16 payload + slot norms + ids
+  p.off_meta = (size_t)nst * p.stage_bytes;
   p.off_gm = p.off_meta + MAXST * sizeof(StageMeta);
   p.off_q = p.off_gm + NB * sizeof(GroupMeta);
-  p.off_items = p.off_q + 2 * TM * sizeof(QInfo);
+  p.off_items = p.off_q + NQI * TM * sizeof(QInfo);
   p.off_thr = p.off_items + NITEM * (sizeof(ItemRec) + MAXS * sizeof(uint2));
   p.off_mrg = p.off_thr + 2 * TM * 8;
   p.off_bar = p.off_mrg + (size_t)TM * KP * 8;
-  p.total = p.off_bar + (2 * MAXST + 2 * NB + 5 + 2 * NITEM + 2) * 8 + 1024;  // + alignment slack
+  p.total = p.off_bar + (2 * MAXST + 2 * NB + 4 + 2 * NQI + 2 * NITEM + 2) * 8 + 1024;  // + alignment slack
   return p;
 }
 
@@ -189,13 +191,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const DevState& st = a.st;
-  const int Dp = st.Dp, nq4 = Dp >> 2, nst = a.nst, k = a.k;
-  const TcPlan p = tc_plan(Dp, nst, KP);
+  const int Dp = st.Dp, nq4 = Dp >> 2, Dh = st.Dh, nst = a.nst, k = a.k;
+  const TcPlan p = tc_plan(Dh, nst, KP);
   StageMeta* smeta = reinterpret_cast<StageMeta*>(smem + p.off_meta);
   GroupMeta* gm = reinterpret_cast<GroupMeta*>(smem + p.off_gm);
   QInfo* qinfo = reinterpret_cast<QInfo*>(smem + p.off_q);  // [2][TM]
   ItemRec* items = reinterpret_cast<ItemRec*>(smem + p.off_items);
-  uint2* irec = reinterpret_cast<uint2*>(items + NITEM);  // [NITEM][MAXS] (slab | flag << 31, bitmap)
+  uint2* irec = reinterpret_cast<uint2*>(items + NITEM);  // [NITEM][MAXS] (slab | flags << 30, bitmap)
   u64* thr_sh = reinterpret_cast<u64*>(smem + p.off_thr);    // [2][TM] (item << 32 | k-th bound bits)
   u64* mrg = reinterpret_cast<u64*>(smem + p.off_mrg);       // [TM][KP] half-list hand-over
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);  // [MAXST] producer -> MMA (tx bytes)
@@ -203,19 +205,19 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   uint64_t* d_full = meta_full + MAXST;                            // [NB] MMA commit -> epilogue, producer
   uint64_t* grp_free = d_full + NB;                                // [NB] epilogue -> MMA
   uint64_t* a_full = grp_free + NB;                                 // [2] loaders -> MMA, epilogue
-  uint64_t* q_free = a_full + 2;                                   // [2] epilogue -> loaders (QInfo buffer)
-  uint64_t* a_free = q_free + 2;                                   // [1] MMA commit -> loaders (shared A tile)
-  uint64_t* item_full = a_free + 1;                                // [NITEM] scheduler -> all
+  uint64_t* a_free = a_full + 2;                                   // [2] MMA commit -> loaders
+  uint64_t* q_read = a_free + 2;                                   // [NQI] epilogue -> loaders (QInfo consumed)
+  uint64_t* q_full = q_read + NQI;                                 // [NQI] loaders -> epilogue (QInfo written)
+  uint64_t* item_full = q_full + NQI;                              // [NITEM] scheduler -> all
   uint64_t* item_empty = item_full + NITEM;                        // [NITEM] epilogue -> scheduler
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(item_empty + NITEM);
-  auto stage_x = [&](int s) { return reinterpret_cast<float*>(smem + p.a_bytes + (size_t)s * p.stage_bytes); };
+  auto stage_x = [&](int s) { return reinterpret_cast<uint16_t*>(smem + (size_t)s * p.stage_bytes); };
   auto stage_nrm = [&](int s) {
-    return reinterpret_cast<float*>(smem + p.a_bytes + (size_t)s * p.stage_bytes + (size_t)GN * Dp * 4);
+    return reinterpret_cast<float*>(smem + (size_t)s * p.stage_bytes + (size_t)GN * Dh * 2);
   };
   auto stage_id = [&](int s) {
-    return reinterpret_cast<uint32_t*>(smem + p.a_bytes + (size_t)s * p.stage_bytes + (size_t)GN * Dp * 4 + GN * 4);
+    return reinterpret_cast<uint32_t*>(smem + (size_t)s * p.stage_bytes + (size_t)GN * Dh * 2 + GN * 4);
   };
-  float* const a_tile = reinterpret_cast<float*>(smem);  // [TM/8][Dp/4][8][4] (pay_off layout)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef SIVF_TC_PROF
   long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -232,9 +234,12 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a_full[b], NLD);
-      mbar_init(&q_free[b], NEPI);
+      mbar_init(&a_free[b], 1);
     }
-    mbar_init(a_free, 1);
+    for (int b = 0; b < NQI; ++b) {
+      mbar_init(&q_read[b], NEPI);
+      mbar_init(&q_full[b], NLD);
+    }
     for (int i = 0; i < NITEM; ++i) {
       mbar_init(&item_full[i], 1);
       mbar_init(&item_empty[i], NEPI);
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     fence_mbar_init();
   }
   for (int t = threadIdx.x; t < 2 * TM; t += blockDim.x) thr_sh[t] = ~0ull;  // tag matches no item
-  if (warp == W_MMA) tmem_alloc(tmem_holder, 32 * GS * NB);
+  if (warp == W_MMA) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -253,13 +258,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     // claims work items and walks each list's slab directory ahead of the
     // producer (up to NITEM - 1 items ahead): the dependent loads (item ->
     // directory -> bitmap -> flag) leave the TMA issue path
-    const int ntiles = st.ictr[I_NTILES];
+    const int ntiles = st.ictr[a.phase == 1 ? I_NTILES0 : I_NTILES];
     const unsigned lt = (1u << lane) - 1u;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
       if (lane == 0) PW(0, mbar_wait(&item_empty[slot], ((i / NITEM) & 1u) ^ 1u));
       int w = 0;
-      if (lane == 0) w = atomicAdd(&st.ictr[I_WORK], 1);
+      if (lane == 0) w = atomicAdd(&st.ictr[a.phase == 2 ? I_WORK2 : I_WORK], 1);
       w = __shfl_sync(kFull, w, 0);
       ItemRec r{-1, 0, 0, 0, -1, 0, 0, 0};
       if (w < ntiles) {
@@ -279,8 +284,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           const unsigned live = __ballot_sync(kFull, bm != 0u);
           if (npre + __popc(live) > MAXS) break;  // the producer walks the rest
           if (bm) {
-            const uint32_t fl = st.slab_flag[sl] & 1u;
-            rec[npre + __popc(live & lt)] = make_uint2((uint32_t)sl | (fl << 31), bm);
+            const uint32_t fl = st.slab_flag[sl] & 3u;
+            rec[npre + __popc(live & lt)] = make_uint2((uint32_t)sl | (fl << 30), bm);
           }
           npre += __popc(live);
         }
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       }
       if (lane == 0) m.last = last;
       __syncwarp();
-      const uint32_t sbytes = (uint32_t)(kSlot * Dp * 4);
+      const uint32_t sbytes = (uint32_t)(kSlot * Dh * 2);
       if (lane == 0) {
         mbar_arrive(&meta_full[stg]);
         mbar_arrive_expect_tx(&full[stg], (a.dbg & 8) ? 0u : (uint32_t)nvalid * (sbytes + 2u * kSlot * 4u));
@@ -332,7 +337,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       // padding positions are not copied: their stale (finite) or uninitialised
       // columns only reach D columns whose slot norm is the NaN mask
       if (lane < nvalid) {
-        bulk_g2s(stage_x(stg) + (size_t)lane * kSlot * Dp, st.payload + (size_t)sl * kSlot * Dp, sbytes, &full[stg]);
+        bulk_g2s(stage_x(stg) + (size_t)lane * kSlot * Dh, st.payload16 + (size_t)sl * kSlot * Dh, sbytes, &full[stg]);
         bulk_g2s(stage_nrm(stg) + lane * kSlot, st.slab_norm + (size_t)sl * kSlot, kSlot * 4, &full[stg]);
         bulk_g2s(stage_id(stg) + lane * kSlot, st.slab_ids + (size_t)sl * kSlot, kSlot * 4, &full[stg]);
       }
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       const uint2* rr = irec + slot * MAXS;
       for (int r = 0; r < rec.npre; ++r) {
         const uint2 x = rr[r];
-        feed((int)(x.x & 0x7fffffffu), x.y, x.x >> 31);
+        feed((int)(x.x & 0x3fffffffu), x.y, x.x >> 30);
       }
       if (rec.dir_pos >= 0) {  // long list: walk the rest of the directory here
         const int32_t* dir = st.dir_arena + st.dir_off[rec.l];
@@ -381,7 +386,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           if (j < rec.len) {
             s = dir[j];
             bm = st.bitmap[s];
-            if (bm) fl = st.slab_flag[s] & 1u;
+            if (bm) fl = st.slab_flag[s] & 3u;
           }
           unsigned live = __ballot_sync(kFull, bm != 0u);
           while (live) {
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     }
   } else if (warp == W_MMA) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = umma_idesc_tf32(TM, GN);
+    const uint32_t idesc = umma_idesc_f16(TM, GN);
     uint32_t gseq = 0;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
@@ -453,17 +458,17 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
 #endif
         if (lane == 0) {
           tc_fence_after();
-          const uint32_t bsm = smem_u32(stage_x(stg)), asm_ = smem_u32(a_tile);
-          const uint32_t dt = tbase + b * 128u;
-          // A and B both K-major SWIZZLE_NONE in shared memory (kind::tf32 from
-          // TMEM A runs at half this rate: tools/mma_probe.cu)
-          for (int kk = 0; kk < ((a.dbg & 4) ? 0 : (Dp >> 3)); ++kk)
-            umma_tf32_ss(dt, umma_sdesc(asm_ + (uint32_t)kk * 256u, 128u, (uint32_t)Dp * 32u),
-                         umma_sdesc(bsm + (uint32_t)kk * 256u, 128u, (uint32_t)Dp * 32u), idesc, kk > 0 ? 1u : 0u);
+          const uint32_t bsm = smem_u32(stage_x(stg));
+          const uint32_t dt = tbase + 128u + b * 128u, at = tbase + ab * 64u;
+          // kind::f16: A (fp16 query tile) in TMEM, 8 columns per K = 16 step;
+          // B (fp16 slab copies) K-major SWIZZLE_NONE, LBO = 128 B, SBO = 16 Dh B
+          for (int kk = 0; kk < ((a.dbg & 4) ? 0 : (Dh >> 4)); ++kk)
+            umma_f16_ts(dt, at + (uint32_t)(8 * kk), umma_sdesc(bsm + (uint32_t)kk * 256u, 128u, (uint32_t)Dh * 16u),
+                        idesc, kk > 0 ? 1u : 0u);
           umma_commit(&d_full[b]);    // accumulator ready and stage stg free (one commit per group:
                                       // each tcgen05.commit costs ~200 cycles of tensor pipe, mma_probe)
           mbar_arrive(&d_full[b]);    // group metadata written
-          if (last) umma_commit(a_free);  // the A tile may be overwritten
+          if (last) umma_commit(&a_free[ab]);  // A[ab] may be overwritten once these MMAs are done
         }
         __syncwarp();
 #ifdef SIVF_TC_PROF
@@ -475,13 +480,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     }
   } else if (warp < W_EPI0) {
     // ------------------------------------------------------------ query loaders
-    // thread = query row; rows are loaded 64 dims at a time, the first half
-    // before the shared A tile is free (the previous item's MMAs done: its
-    // latency hides behind the wait), then ||q||^2, an integrality flag and
-    // 16-B stores into the K-major A tile
+    // thread = query row (TMEM lane); rows are loaded 64 dims at a time, the
+    // first half before A[ab] is free (its latency hides behind the wait),
+    // then ||q||^2 (fp32), the integrality and fp16-range flags and
+    // tcgen05.st of the fp16 (RN) row, two halves per column
     const int qw = warp & 3, row = 32 * qw + lane;
     const bool vec = (st.D & 3) == 0;
-    const int nc8 = Dp >> 3;
+    const int nc8 = Dh >> 3;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
       mbar_wait(&item_full[slot], (i / NITEM) & 1u);
@@ -492,58 +497,68 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       const bool wv = 32 * qw < rec.nqt && !(a.dbg & 16);  // warp-uniform: the warp has a real row
       const int pair = rv ? a.inv_pairs[rec.p0 + row] : -1;
       const float* qr = a.Q + (int64_t)(rv ? pair / a.nprobe : 0) * st.D;
+      const uint32_t ta = tbase + ((uint32_t)(32 * qw) << 16) + ab * 64u;
       float nrm = 0.f;
-      uint32_t integ = 1u;
+      uint32_t integ = 1u, over = 0u;
 #ifdef SIVF_TC_PROF
       long long _tl0 = clock64();
 #endif
       for (int h0 = 0; h0 < nc8; h0 += 8) {
-        uint32_t v[8][8];
+        float x[8][8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int d0 = 8 * (h0 + u);
-          float x[8];
           if (wv && rv && vec && d0 + 7 < st.D) {
             const float4 lo = __ldg(reinterpret_cast<const float4*>(qr + d0));
             const float4 hi = __ldg(reinterpret_cast<const float4*>(qr + d0 + 4));
-            x[0] = lo.x, x[1] = lo.y, x[2] = lo.z, x[3] = lo.w, x[4] = hi.x, x[5] = hi.y, x[6] = hi.z, x[7] = hi.w;
+            x[u][0] = lo.x, x[u][1] = lo.y, x[u][2] = lo.z, x[u][3] = lo.w;
+            x[u][4] = hi.x, x[u][5] = hi.y, x[u][6] = hi.z, x[u][7] = hi.w;
           } else {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) x[e] = (rv && d0 + e < st.D) ? __ldg(qr + d0 + e) : 0.f;
+            for (int e = 0; e < 8; ++e) x[u][e] = (rv && h0 + u < nc8 && d0 + e < st.D) ? __ldg(qr + d0 + e) : 0.f;
           }
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v[u][e] = __float_as_uint(x[e]);
         }
         if (h0 == 0) {
-          PW(4, mbar_wait(a_free, (i & 1u) ^ 1u));
+          PW(4, mbar_wait(&a_free[ab], ((i >> 1) & 1u) ^ 1u));
           tc_fence_after();
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (h0 + u < nc8) {
+        for (int u = 0; u < 8; u += 2) {
+          if (h0 + u < nc8) {  // nc8 is even: 16 dims = 8 columns
+            uint32_t hv[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float x = __uint_as_float(v[u][e]);
-              nrm = fmaf(x, x, nrm);
-              integ &= (x == rintf(x) ? 1u : 0u) & (fabsf(x) <= 2048.f ? 1u : 0u);
+            for (int e = 0; e < 16; ++e) {
+              const float xe = x[u + (e >> 3)][e & 7];
+              nrm = fmaf(xe, xe, nrm);
+              integ &= (xe == rintf(xe) ? 1u : 0u) & (fabsf(xe) <= 2048.f ? 1u : 0u);
+              over |= fabsf(xe) <= 65504.f ? 0u : 1u;
             }
-            if (wv) {
-              const int c4 = 2 * (h0 + u);
-              *reinterpret_cast<uint4*>(a_tile + pay_off(Dp, row, c4)) = make_uint4(v[u][0], v[u][1], v[u][2], v[u][3]);
-              *reinterpret_cast<uint4*>(a_tile + pay_off(Dp, row, c4 + 1)) =
-                  make_uint4(v[u][4], v[u][5], v[u][6], v[u][7]);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const __half2 h2 = __floats2half2_rn(x[u + (c >> 2)][2 * (c & 3)], x[u + (c >> 2)][2 * (c & 3) + 1]);
+              hv[c] = *reinterpret_cast<const uint32_t*>(&h2);
             }
+            if (wv) tmem_st8(ta + (uint32_t)(4 * (h0 + u)), hv);
           }
         }
       }
 #ifdef SIVF_TC_PROF
       pw[1] += clock64() - _tl0;
+      _tl0 = clock64();
 #endif
-      fence_proxy_async_smem();  // generic-proxy stores -> tcgen05.mma (async proxy)
-      PW(2, mbar_wait(&q_free[ab], ((i >> 1) & 1u) ^ 1u));  // the epilogue is done with item i - 2's QInfo
-      qinfo[ab * TM + row] = QInfo{nrm, pair, integ, 0u};
+      tmem_st_wait();
+#ifdef SIVF_TC_PROF
+      pw[2] += clock64() - _tl0;
+#endif
+      const int qb = (int)(i % NQI);
+      PW(5, mbar_wait(&q_read[qb], ((i / NQI) & 1u) ^ 1u));  // item i - NQI's QInfo has been read
+      qinfo[qb * TM + row] = QInfo{nrm, pair, integ, over};
+      tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&a_full[ab]);
+      if (lane == 0) {
+        mbar_arrive(&a_full[ab]);
+        mbar_arrive(&q_full[qb]);
+      }
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -551,8 +566,14 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     // halves of a row keep separate top-k lists (merged at the item's end) and
     // share their k-th distance bounds through shared memory every group
     const int qw = warp & 3, row = 32 * qw + lane, h = (warp - W_EPI0) >> 2;
-    const float eps1 = 0x1p-9f + 0x1p-19f + (float)Dp * 0x1p-23f;
+    // certified band of the fp16 filter (u = 2^-11, RN): eps1 bounds the
+    // relative error of q.x from the operand roundings (2u + u^2 <= 2^-9 +
+    // 2^-19, tf32-safe margin kept) and fp32 accumulation (Dh 2^-23); esub the
+    // absolute error of fp16 subnormals (|v| < 2^-14: error <= 2^-25 per value,
+    // sum <= 2^-25 sqrt(Dh) (||q|| + ||x||)), times 2 for d and 2 for safety
+    const float eps1 = 0x1p-9f + 0x1p-19f + (float)Dh * 0x1p-23f;
     const float eps2 = (float)(2 * Dp + 10) * 0x1p-24f;
+    const float esub = 0x1p-23f * 1.001f * sqrtf((float)Dh);
     uint32_t gseq = 0;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
@@ -560,8 +581,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       const uint32_t ab = i & 1u;
-      PW(1, mbar_wait(&a_full[ab], (i >> 1) & 1u));
-      const QInfo qi = qinfo[ab * TM + row];
+      PW(1, mbar_wait(&q_full[i % NQI], (i / NQI) & 1u));
+      const QInfo qi = qinfo[(i % NQI) * TM + row];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&q_read[i % NQI]);
       const bool rv = row < rec.nqt;
       const bool wact = 32 * qw < rec.nqt;
       const int qglob = rv ? qi.pair / a.nprobe : 0;
@@ -588,11 +611,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           auto chunk = [&](const int j, const uint32_t(&v)[32]) {
             const float xm = g.xnmax[j], sxm = sqrtf(xm);
             const float rs = sqn + sxm;
-            const bool ex = qi.qint != 0u && (g.flag[j] & 1u) != 0u && rs * rs < 16000000.f;
+            const bool ex = qi.qint != 0u && (g.flag[j] & kFlagIntegral) != 0u && rs * rs < 16000000.f;
+            // no finite fp16 copy of the query or the slab: every valid slot is re-ranked exactly
+            const bool unsafe = qi.qover != 0u || (g.flag[j] & kFlagF16Over) != 0u;
             float E = 0.f;
             if (!ex) {
               const float cs = sqn * sxm;
-              E = 2.f * (2.f * eps1 * cs + eps2 * (qn + xm + 2.f * cs));
+              E = 2.f * (2.f * eps1 * cs + eps2 * (qn + xm + 2.f * cs)) + esub * rs;
             }
             float tadj = ex ? __fsub_ru(thr, qn) : __fadd_ru(__fsub_ru(thr, qn), E);
             const float4* x4 = reinterpret_cast<const float4*>(g.xnm + 32 * j);
@@ -608,7 +633,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
             }
             const float mn = fminf(fminf(fminf(m8[0], m8[1]), fminf(m8[2], m8[3])),
                                    fminf(fminf(m8[4], m8[5]), fminf(m8[6], m8[7])));
-            if (!(mn <= tadj) || (a.dbg & 1)) return;
+            if (!unsafe && (!(mn <= tadj) || (a.dbg & 1))) return;
             // slow path (per lane): survivors of this slab, exact distance, register top-k
 #ifdef SIVF_TC_PROF
             long long _ts = clock64();
@@ -617,6 +642,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
             atomicAdd(&g_scnt[0], 1ull);
 #endif
             uint32_t pm = 0u;
+            if (unsafe) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c) pm |= (g.xnm[32 * j + c] == g.xnm[32 * j + c] ? 1u : 0u) << c;  // valid
+            } else
 #pragma unroll
             for (int c4 = 0; c4 < 8; ++c4) {
               if (!(m8[c4] <= tadj)) continue;  // the quad's minimum already fails
@@ -633,7 +662,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
               const int c = __ffs(pm) - 1;
               pm &= pm - 1;
               const float t = fmaf(-2.f, __uint_as_float(pick32(v, c)), g.xnm[32 * j + c]);
-              if (!(t <= tadj)) continue;  // the threshold may have tightened
+              if (!unsafe && !(t <= tadj)) continue;  // the threshold may have tightened
               float d;
               if (ex) {
                 d = qn + t;  // exact: every term an integer < 2^24
@@ -673,7 +702,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
             pw[6] += clock64() - _ts;
 #endif
           };
-          const uint32_t dcol = tbase + ((uint32_t)(32 * qw) << 16) + b * 128u + (uint32_t)(64 * h);
+          const uint32_t dcol = tbase + ((uint32_t)(32 * qw) << 16) + 128u + b * 128u + (uint32_t)(64 * h);
 #ifdef SIVF_TC_PROF
           long long _tg = clock64();
 #endif
@@ -732,7 +761,6 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       }
       named_bar_sync(1 + qw, 64);
       if (lane == 0) {
-        mbar_arrive(&q_free[ab]);
         mbar_arrive(&item_empty[slot]);
       }
     }
@@ -745,7 +773,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == W_MMA) tmem_dealloc(tbase, 32 * GS * NB);
+  if (warp == W_MMA) tmem_dealloc(tbase, 512);
 }
 
 
@@ -805,8 +833,8 @@ __global__ void __launch_bounds__(128) k_seed_bound(DevState st, const float* __
 inline int scan_kp(int k) { return k <= 12 ? 12 : k <= 16 ? 16 : 32; }
 
 int tc_stages(const Index& ix, int KP) {
-  const size_t sb = tc_plan(ix.st.Dp, 0, KP).stage_bytes;
-  const size_t fixed = tc_plan(ix.st.Dp, 0, KP).total;
+  const size_t sb = tc_plan(ix.st.Dh, 0, KP).stage_bytes;
+  const size_t fixed = tc_plan(ix.st.Dh, 0, KP).total;
   if (ix.smem_optin < fixed) return 0;
   int n = (int)((ix.smem_optin - fixed) / sb);
   return n > NB ? NB : n;  // the producer reuses the accumulator barriers: nst <= NB
@@ -815,32 +843,30 @@ int tc_stages(const Index& ix, int KP) {
 }  // namespace
 
 bool scan_tc_supported(const Index& ix, int k) {
-  return ix.st.Dp <= 128 && k <= 32 && tc_stages(ix, scan_kp(k)) >= 2;
+  return ix.st.Dh > 0 && ix.st.Dh <= 128 && k <= 32 && tc_stages(ix, scan_kp(k)) >= 2;
 }
 
 cudaError_t setup_scan_tc(Index& ix) {
-  if (ix.st.Dp > 128) return cudaSuccess;
-  // KP = 32 needs a larger merge buffer: with D = 128 only one group stage fits
-  // beside the shared A tile, and scan_tc_supported() sends k > 16 to the CUDA-core scan
+  if (ix.st.Dh == 0 || ix.st.Dh > 128) return cudaSuccess;
   cudaError_t e = cudaSuccess;
   if (tc_stages(ix, 12) >= 2)
     e = cudaFuncSetAttribute(k_scan_tc<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc_plan(ix.st.Dp, tc_stages(ix, 12), 12).total);
+                             (int)tc_plan(ix.st.Dh, tc_stages(ix, 12), 12).total);
   if (e == cudaSuccess && tc_stages(ix, 16) >= 2)
     e = cudaFuncSetAttribute(k_scan_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc_plan(ix.st.Dp, tc_stages(ix, 16), 16).total);
+                             (int)tc_plan(ix.st.Dh, tc_stages(ix, 16), 16).total);
   if (e == cudaSuccess && tc_stages(ix, 32) >= 2)
     e = cudaFuncSetAttribute(k_scan_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc_plan(ix.st.Dp, tc_stages(ix, 32), 32).total);
+                             (int)tc_plan(ix.st.Dh, tc_stages(ix, 32), 32).total);
   return e;
 }
 
-cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s) {
+cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s, int phase) {
   Scratch& sc = ix.sc;
   const int KP = scan_kp(k);
   const int nst = tc_stages(ix, KP);
-  TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, ix.dbg};
-  const size_t smem = tc_plan(ix.st.Dp, nst, KP).total;
+  TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, phase, ix.dbg};
+  const size_t smem = tc_plan(ix.st.Dh, nst, KP).total;
   if (KP == 12) k_scan_tc<12><<<ix.num_sms, TTHREADS, smem, s>>>(a);
   else if (KP == 16) k_scan_tc<16><<<ix.num_sms, TTHREADS, smem, s>>>(a);
   else k_scan_tc<32><<<ix.num_sms, TTHREADS, smem, s>>>(a);

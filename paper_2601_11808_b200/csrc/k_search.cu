@@ -219,11 +219,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
 // major, so each query's nearest list is scanned first and the per-query bound
 // on its k-th distance is already in place for its other lists.
 __global__ void k_inv_count(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int nb, int r0,
-                            int nlist, int32_t* __restrict__ cnt, uint32_t* __restrict__ gthr) {
+                            int nlist, int32_t* __restrict__ cnt, uint32_t* __restrict__ gthr, int keep) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npairs) return;
   const int p = (int)(i % nprobe);
-  if (p == 0) gthr[i / nprobe] = 0x7F800000u;  // per-query bound = +inf
+  if (p == 0 && !keep) gthr[i / nprobe] = 0x7F800000u;  // per-query bound = +inf
   const int b = (nb == 2 && p >= r0) ? 1 : 0;
   atomicAdd(&cnt[b * nlist + probes[i]], 1);
 }
@@ -289,6 +289,11 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
     tile_off[nent] = carry[1];
     ictr[I_NTILES] = carry[1];
     ictr[I_WORK] = 0;
+    // bucket 0 (each query's r0 nearest lists) = tiles [0, tile_off[nlist]): the
+    // phased tensor-core scan runs it to completion before bucket 1
+    const int t0 = nent > nlist ? tile_off[nlist] : carry[1];
+    ictr[I_NTILES0] = t0;
+    ictr[I_WORK2] = t0;
   }
   __syncthreads();  // the block's offsets are visible to all of its threads
   // work items (list, first pair, number of pairs), bucket-major (k_work_fill fused)
@@ -413,7 +418,7 @@ size_t scan_smem_for(const Index& ix, int k, int* nw_out) {
 
 bool scan_tc_supported(const Index& ix, int k);
 cudaError_t setup_scan_tc(Index& ix);
-cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s);
+cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s, int phase);
 int scan_tc_tile();
 
 cudaError_t setup_search_kernels(Index& ix) {
@@ -446,7 +451,7 @@ SearchPlan plan_search(const Index& ix, int64_t nq, int32_t k, int32_t nprobe) {
   p.r0 = nprobe;
   if (p.tc && nprobe >= 8) {
     const int64_t per_list = nq * nprobe / nlist;
-    const int rr = ix.tc_two_phase ? 1 : nprobe / 4;
+    const int rr = ix.tc_two_phase ? (ix.tc_two_phase < nprobe ? ix.tc_two_phase : nprobe - 1) : nprobe / 4;
     const int64_t ta = ceil_div(per_list * rr / nprobe, p.QT),
                   tb = ceil_div(per_list - per_list * rr / nprobe, p.QT);
     if (ix.tc_two_phase || (ix.rank_split && ta + tb <= ceil_div(per_list, p.QT))) {
@@ -480,7 +485,7 @@ cudaError_t launch_search_front(Index& ix, const SearchPlan& p, const float* d_q
   PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
   if (!counted) {
     k_inv_count<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, p.nb, p.r0, nlist, sc.inv_cnt,
-                                                       sc.gthr);
+                                                       sc.gthr, (ix.dbg >> 6) & 1);
     ix.launches += 1;
   }
   k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, p.QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr, nlist,
@@ -502,7 +507,14 @@ cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q,
     PhaseTimer pt(ix, SIVF_PH_SCAN, s);
     if (p.tc) {
       e = launch_seed_bound(ix, d_q, nq, k, nprobe, s);  // after the front reset gthr to +inf
-      if (e == cudaSuccess) e = launch_scan_tc(ix, d_q, k, nprobe, s);
+      if (e == cudaSuccess && p.nb == 2 && ix.tc_two_phase) {
+        // two launches: every query's r0 nearest lists complete (and its k-th
+        // distance bound is published) before any of its other lists starts
+        e = launch_scan_tc(ix, d_q, k, nprobe, s, 1);
+        if (e == cudaSuccess) e = launch_scan_tc(ix, d_q, k, nprobe, s, 2);
+      } else if (e == cudaSuccess) {
+        e = launch_scan_tc(ix, d_q, k, nprobe, s, 0);
+      }
     } else if (p.nw == 8) {
       k_scan<8><<<grid, 32 * 9, p.smem, s>>>(a);
     } else if (p.nw == 4) {

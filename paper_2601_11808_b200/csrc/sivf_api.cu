@@ -15,7 +15,7 @@ constexpr size_t kAlign = 256;
 
 struct Layout {
   size_t total = 0;
-  size_t payload, slab_ids, slab_norm, slab_flag, bitmap, cursor, slab_list, free_stack, slab_mark, att, claim,
+  size_t payload, payload16, slab_ids, slab_norm, slab_flag, bitmap, cursor, slab_list, free_stack, slab_mark, att, claim,
       dir_off, dir_len, dir_cap, dir_arena, centroids, ctr, ictr, tmp64, gthr;
   size_t row_list, row_rank, row_status, row_lid, row_best, chunk_hist, list_cnt, list_tail_free, list_tail_slab,
       list_granted, list_newbase, list_short;
@@ -25,7 +25,7 @@ struct Layout {
   int64_t q_rows;
   size_t x_tiles, x_norm, c_tiles, c_norm, c_csa, c_cnb, cand, cand_ubv, cand_cnt;
   int64_t tc_rows, cap_assign, cap_probe;
-  int64_t Dp, cap_local, dir_arena_cap, max_rows, max_chunks, coarse_rows, max_work;
+  int64_t Dp, Dh, cap_local, dir_arena_cap, max_rows, max_chunks, coarse_rows, max_work;
 };
 
 size_t take(Layout& L, size_t bytes) {
@@ -52,6 +52,7 @@ Layout make_layout(const sivf_config* c) {
   Layout L;
   const int64_t D = c->dim, nl = c->nlist, S = c->num_slabs;
   L.Dp = (D + 7) / 8 * 8;  // tf32 MMA K-step = 8 dims
+  L.Dh = D <= 128 ? (D + 15) / 16 * 16 : 0;  // fp16 scan copy (kind::f16 K-step = 16 dims); D > 128: none
   const int64_t cap = c->id_capacity, G = c->shard_count, r = c->shard_rank;
   L.cap_local = cap > r ? (cap - r + G - 1) / G : 0;
   L.dir_arena_cap = 4 * S + 16 * nl + 1024;
@@ -71,6 +72,7 @@ Layout make_layout(const sivf_config* c) {
   L.max_work = (npairs + 7) / 8 + 2 * nl + 1;
 
   L.payload = take(L, (size_t)S * kSlot * L.Dp * 4);
+  L.payload16 = take(L, (size_t)S * kSlot * L.Dh * 2);
   L.slab_ids = take(L, (size_t)S * kSlot * 4);
   L.slab_norm = take(L, (size_t)S * kSlot * 4);
   L.slab_flag = take(L, (size_t)S * 4);
@@ -211,6 +213,7 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   DevState& st = ix->st;
   st.D = cfg->dim;
   st.Dp = (int32_t)L.Dp;
+  st.Dh = (int32_t)L.Dh;
   st.nlist = cfg->nlist;
   st.G = cfg->shard_count;
   st.rank = cfg->shard_rank;
@@ -218,6 +221,7 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   st.cap_local = L.cap_local;
   st.num_slabs = cfg->num_slabs;
   st.payload = at<float>(d_arena, L.payload);
+  st.payload16 = L.Dh ? at<uint16_t>(d_arena, L.payload16) : nullptr;
   st.slab_ids = at<uint32_t>(d_arena, L.slab_ids);
   st.slab_norm = at<float>(d_arena, L.slab_norm);
   st.slab_flag = at<uint32_t>(d_arena, L.slab_flag);
@@ -483,7 +487,7 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
   Index* ix = reinterpret_cast<Index*>(h);
   switch (option) {
     case SIVF_OPT_TC_SCAN: ix->use_tc_scan = value != 0; return SIVF_OK;
-    case SIVF_OPT_TC_TWO_PHASE: ix->tc_two_phase = value != 0; return SIVF_OK;
+    case SIVF_OPT_TC_TWO_PHASE: ix->tc_two_phase = value < 0 ? 0 : (int)value; return SIVF_OK;
     case SIVF_OPT_TC_COARSE: ix->use_tc_coarse = value != 0; return SIVF_OK;
     case SIVF_OPT_COARSE_SELECT: ix->coarse_select = value != 0; return SIVF_OK;
     case SIVF_OPT_RANK_SPLIT: ix->rank_split = value != 0; return SIVF_OK;

@@ -86,7 +86,7 @@ struct Index {
   bool trained = false;
   bool use_tc_scan = true;
   bool use_tc_coarse = true;  // tcgen05 coarse quantisation (k_coarse_tc.cu); false = exact SIMT k_dist_exact
-  bool tc_two_phase = false;  // nearest-list-first scan phase (SIVF_OPT_TC_TWO_PHASE)  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
+  int tc_two_phase = 0;    // nearest-list-first scan phase (SIVF_OPT_TC_TWO_PHASE)  // tensor-core scan when Dp <= 256 and k <= 32 (k_scan_tc.cu)
   // search -> coarse hand-off: when set, k_coarse_select also counts the inverse probe map
   // (k_inv_count fused) into fuse_inv_cnt and sets fuse_inv_done
   int32_t* fuse_inv_cnt = nullptr;

@@ -19,6 +19,14 @@ constexpr int kSlot = 32;                          // slab capacity C = 32 (P:15
 __host__ __device__ __forceinline__ size_t pay_off(int Dp, int n, int c4) {
   return ((size_t)((n >> 3) * (Dp >> 2) + c4) * 8 + (n & 7)) * 4;
 }
+// The fp16 scan copy has the same structure with 16-B chunks of 8 halves:
+// half offset of chunk c8 of slot n (LBO = 128 B, SBO = 16 Dh B).
+__host__ __device__ __forceinline__ size_t pay16_off(int Dh, int n, int c8) {
+  return ((size_t)((n >> 3) * (Dh >> 3) + c8) * 8 + (n & 7)) * 8;
+}
+// slab_flag bits
+constexpr uint32_t kFlagIntegral = 1u;  // every value an integer with |v| <= 2048 (exact in tf32 and fp16)
+constexpr uint32_t kFlagF16Over = 2u;   // some value has |v| > 65504 (no finite fp16 copy): scan re-ranks all
 constexpr uint64_t kAttInvalid = ~0ull;            // INVALID sentinel (reading C14)
 constexpr int32_t kClaimEmpty = 0x7f7f7f7f;        // byte-memsettable "no claimant"
 constexpr uint64_t kPadKey = 0x7F800000FFFFFFFFull; // (+inf, id 0xFFFFFFFF): sorts after every real key
@@ -28,14 +36,15 @@ using u64 = unsigned long long;
 // Counters (u64, arena) — index into DevState::ctr
 enum { C_LIVE = 0, C_INSERTED, C_DELETED, C_EXHAUSTED, C_RECLAIMED, C_DEVERR, C_NDEL_TMP, C_NCTR = 8 };
 // Counters (i32, arena) — index into DevState::ictr
-enum { I_FREE_TOP = 0, I_DIR_BUMP, I_WORK, I_NTILES, I_NICTR = 8 };
+enum { I_FREE_TOP = 0, I_DIR_BUMP, I_WORK, I_NTILES, I_NTILES0, I_WORK2, I_NICTR = 8 };  // *0/*2: phased scan
 
 // POD view of the arena, passed by value to kernels (the paper's
 // SlabManagerDevice).
 struct DevState {
-  int32_t D, Dp, nlist, G, rank;
+  int32_t D, Dp, Dh, nlist, G, rank;  // Dh: fp16 scan copy dims (D rounded up to 16; 0 = no copy)
   int64_t cap, cap_local, num_slabs;
   float* payload;        // [num_slabs][4][Dp/4][8][4]  see pay_off(): a slab is one UMMA B core-matrix block
+  uint16_t* payload16;   // [num_slabs][4][Dh/8][8][8]  fp16 (RN) copy for the tensor-core scan, pay16_off()
   uint32_t* slab_ids;    // [num_slabs][32] user ids (u32)
   float* slab_norm;      // [num_slabs][32] ||x||^2 (fp32), for the tensor-core distance expansion
   uint32_t* slab_flag;   // [num_slabs] bit0: every payload value is an integer with |x| <= 2048 (tf32-exact)
@@ -214,6 +223,20 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, u
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Instruction descriptor: kind::f16 with fp16 A and B, fp32 accumulate, K-major.
+__host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16 (K = 16 per instruction; A: 8
+// TMEM columns per K step, two halves per 32-bit column, lower half first).
+__device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }

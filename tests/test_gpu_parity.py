@@ -260,6 +260,26 @@ def test_float_data_d128_rerank_path(tc):
     assert srch(g2, o2, np.rint(Q * 1000).astype(np.float32), 10, 8, exact=False) <= 3
 
 
+@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05-scan", "simt-scan"])
+def test_values_beyond_fp16_range(tc):
+    # the tensor-core scan filters with an fp16 copy of the slabs and queries;
+    # values with |v| > 65504 have none: those slabs (flag) and queries re-rank
+    # every valid slot exactly, so results match the oracle as for any data
+    gen = Generator(gist_shape(seed=0x6158, dim=128))
+    X = gen.range(0, 4000) * 1000.0
+    X[::7] *= 100.0  # some vectors (hence some slabs) beyond the fp16 range
+    X = X.astype(np.float32)
+    C = O.kmeans(X, 32, 6, 3)
+    g, o = make_pair(128, 32, 4000, C, max_batch=4000, max_queries=200, tc=tc)
+    ins(g, o, np.arange(4000), X)
+    dele(g, o, np.arange(2, 4000, 9))
+    Q = gen.queries(0, 200) * 1000.0
+    Q[::5] *= 100.0  # and some queries
+    Q = Q.astype(np.float32)
+    for k, npb in ((10, 8), (5, 32)):
+        assert srch(g, o, Q, k, npb, exact=False) <= 3
+
+
 def test_sliding_window_scaled():
     gen = Generator(sift_shape(seed=0x51F7))
     W, B, steps = 20000, 1000, 25
