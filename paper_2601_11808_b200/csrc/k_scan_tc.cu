@@ -163,6 +163,11 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 
 #ifdef SIVF_TC_PROF
+#ifdef SIVF_TC_NOCOUNT  // timing builds: no contended counters on the slow path
+#define SCNT_ADD(p, v) ((void)0)
+#else
+#define SCNT_ADD(p, v) atomicAdd(p, v)
+#endif
 __device__ long long g_tr[6][1024];
 __device__ unsigned long long g_scnt[4];  // slow-path entries, survivors, insertions, warp-level loop iterations
 #define TR(r, g, v) \
@@ -639,7 +644,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
             long long _ts = clock64();
 #endif
 #ifdef SIVF_TC_PROF
-            atomicAdd(&g_scnt[0], 1ull);
+            SCNT_ADD(&g_scnt[0], 1ull);
 #endif
             uint32_t pm = 0u;
             if (unsafe) {
@@ -656,7 +661,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
               pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 3]), xx.w) <= tadj ? 1u : 0u) << (4 * c4 + 3);
             }
 #ifdef SIVF_TC_PROF
-            atomicAdd(&g_scnt[1], (unsigned long long)__popc(pm));
+            SCNT_ADD(&g_scnt[1], (unsigned long long)__popc(pm));
 #endif
             while (pm) {
               const int c = __ffs(pm) - 1;
@@ -695,7 +700,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
               }
 #ifdef SIVF_TC_PROF
               pw[7]++;
-              atomicAdd(&g_scnt[2], 1ull);
+              SCNT_ADD(&g_scnt[2], 1ull);
 #endif
             }
 #ifdef SIVF_TC_PROF
@@ -830,7 +835,7 @@ __global__ void __launch_bounds__(128) k_seed_bound(DevState st, const float* __
 }
 
 // register top-k width: the insertion network costs O(KP) per survivor
-inline int scan_kp(int k) { return k <= 12 ? 12 : k <= 16 ? 16 : 32; }
+inline int scan_kp(int k) { return k <= 10 ? 10 : k <= 16 ? 16 : 32; }
 
 int tc_stages(const Index& ix, int KP) {
   const size_t sb = tc_plan(ix.st.Dh, 0, KP).stage_bytes;
@@ -849,9 +854,9 @@ bool scan_tc_supported(const Index& ix, int k) {
 cudaError_t setup_scan_tc(Index& ix) {
   if (ix.st.Dh == 0 || ix.st.Dh > 128) return cudaSuccess;
   cudaError_t e = cudaSuccess;
-  if (tc_stages(ix, 12) >= 2)
-    e = cudaFuncSetAttribute(k_scan_tc<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc_plan(ix.st.Dh, tc_stages(ix, 12), 12).total);
+  if (tc_stages(ix, 10) >= 2)
+    e = cudaFuncSetAttribute(k_scan_tc<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc_plan(ix.st.Dh, tc_stages(ix, 10), 10).total);
   if (e == cudaSuccess && tc_stages(ix, 16) >= 2)
     e = cudaFuncSetAttribute(k_scan_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)tc_plan(ix.st.Dh, tc_stages(ix, 16), 16).total);
@@ -867,7 +872,7 @@ cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaS
   const int nst = tc_stages(ix, KP);
   TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, phase, ix.dbg};
   const size_t smem = tc_plan(ix.st.Dh, nst, KP).total;
-  if (KP == 12) k_scan_tc<12><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+  if (KP == 10) k_scan_tc<10><<<ix.num_sms, TTHREADS, smem, s>>>(a);
   else if (KP == 16) k_scan_tc<16><<<ix.num_sms, TTHREADS, smem, s>>>(a);
   else k_scan_tc<32><<<ix.num_sms, TTHREADS, smem, s>>>(a);
   ix.launches += 1;

@@ -451,10 +451,11 @@ SearchPlan plan_search(const Index& ix, int64_t nq, int32_t k, int32_t nprobe) {
   p.r0 = nprobe;
   if (p.tc && nprobe >= 8) {
     const int64_t per_list = nq * nprobe / nlist;
-    const int rr = ix.tc_two_phase ? (ix.tc_two_phase < nprobe ? ix.tc_two_phase : nprobe - 1) : nprobe / 4;
+    const int rr = ix.tc_two_phase ? (ix.tc_two_phase < nprobe ? ix.tc_two_phase : nprobe - 1)
+                 : ix.rank_split > 1 ? (ix.rank_split < nprobe ? ix.rank_split : nprobe - 1) : nprobe / 4;
     const int64_t ta = ceil_div(per_list * rr / nprobe, p.QT),
                   tb = ceil_div(per_list - per_list * rr / nprobe, p.QT);
-    if (ix.tc_two_phase || (ix.rank_split && ta + tb <= ceil_div(per_list, p.QT))) {
+    if (ix.tc_two_phase || ix.rank_split > 1 || (ix.rank_split && ta + tb <= ceil_div(per_list, p.QT))) {
       p.nb = 2;
       p.r0 = rr;
     }

@@ -490,7 +490,7 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
     case SIVF_OPT_TC_TWO_PHASE: ix->tc_two_phase = value < 0 ? 0 : (int)value; return SIVF_OK;
     case SIVF_OPT_TC_COARSE: ix->use_tc_coarse = value != 0; return SIVF_OK;
     case SIVF_OPT_COARSE_SELECT: ix->coarse_select = value != 0; return SIVF_OK;
-    case SIVF_OPT_RANK_SPLIT: ix->rank_split = value != 0; return SIVF_OK;
+    case SIVF_OPT_RANK_SPLIT: ix->rank_split = value < 0 ? 0 : (int)value; return SIVF_OK;
     case 99: ix->dbg = (int)value; return SIVF_OK;  // SIVF_OPT_DEBUG: experiments only
     case SIVF_OPT_SEED_SLABS:
       if (value < 0 || value > (1 << 20)) return SIVF_E_INVALID_ARG;

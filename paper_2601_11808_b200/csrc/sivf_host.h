@@ -93,7 +93,7 @@ struct Index {
   int fuse_nb = 1, fuse_r0 = 0;
   bool fuse_inv_done = false;
   bool coarse_select = true;  // A-matrix + per-row selection coarse path (SIVF_OPT_COARSE_SELECT)
-  bool rank_split = true;     // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT)
+  int rank_split = 1;         // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT; > 1: r0)
   int dbg = 0;                // experiment switches (SIVF_OPT_DEBUG)
   int seed_slabs = 0;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS; off: it costs more than it saves)
   int64_t launches = 0;
