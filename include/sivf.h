@@ -59,6 +59,15 @@ typedef enum {
   SIVF_ST_WRONG_SHARD = 4      /* id % shard_count != shard_rank */
 } sivf_item_status;
 
+/* sivf_config.flags */
+enum {
+  /* No fp16 copy of the slab payload: the arena is the paper's footprint (fp32
+   * payload + ids + metadata) and search scans on CUDA cores.  By default
+   * (dim <= 128) the arena also holds an fp16 (RN) copy of every slab that the
+   * tensor-core scan reads (+50 % of the payload bytes at dim 128; reading C35). */
+  SIVF_CFG_NO_SCAN_COPY = 1
+};
+
 typedef struct {
   int32_t dim;          /* D >= 1 */
   int32_t nlist;        /* number of inverted lists, 1..65536 */
@@ -71,7 +80,7 @@ typedef struct {
   int32_t max_train;    /* max training points for sivf_train_centroids (0 = none) */
   int32_t shard_rank;   /* 0..shard_count-1 */
   int32_t shard_count;  /* >= 1; owner(id) = id % shard_count */
-  int32_t reserved0;
+  int32_t flags;        /* SIVF_CFG_* bits (0 = defaults) */
   uint64_t seed;        /* k-means initialisation seed */
 } sivf_config;
 
@@ -86,6 +95,7 @@ typedef struct {
   int64_t device_errors;        /* sticky internal errors (directory arena overflow); must stay 0 */
   double overhead_paper;        /* 128/(32*(4d+8)): the paper's per-slab header accounting (reading C17) */
   double overhead_actual;       /* this build: (16 B metadata/slab * slabs_in_use + 8 B * id slots) / (live payload+id bytes) */
+  double overhead_scan_copy;    /* the fp16 scan copy (2 Dh B per slot of slabs_in_use) / (live payload+id bytes); 0 without */
 } sivf_stats_t;
 
 /* Bytes of device memory the index needs for `cfg` (host-only, pure). */

@@ -35,7 +35,7 @@ class Config(ctypes.Structure):
         ("max_train", _i32),
         ("shard_rank", _i32),
         ("shard_count", _i32),
-        ("reserved0", _i32),
+        ("flags", _i32),
         ("seed", _u64),
     ]
 
@@ -52,6 +52,7 @@ class Stats(ctypes.Structure):
         ("device_errors", _i64),
         ("overhead_paper", ctypes.c_double),
         ("overhead_actual", ctypes.c_double),
+        ("overhead_scan_copy", ctypes.c_double),
     ]
 
 
@@ -79,6 +80,7 @@ EXPORTS = {
     "sivf_set_option": (_i32, [_P, _i32, _i64]),
 }
 
+CFG_NO_SCAN_COPY = 1  # sivf_config.flags: no fp16 scan copy (paper footprint, CUDA-core scan)
 OPT_TC_SCAN = 1
 OPT_TC_TWO_PHASE = 2
 OPT_TC_COARSE = 3
@@ -141,7 +143,8 @@ class Index:
 
     def __init__(self, dim: int, nlist: int, id_capacity: int, num_slabs: int, max_batch: int = 10000,
                  max_queries: int = 10000, max_k: int = 128, max_nprobe: int | None = None, max_train: int = 0,
-                 shard_rank: int = 0, shard_count: int = 1, seed: int = 0, device=None, stream=None):
+                 shard_rank: int = 0, shard_count: int = 1, seed: int = 0, flags: int = 0, device=None,
+                 stream=None):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2601_11808_b200 needs a CUDA device (no CPU fallback)")
         L = lib()
@@ -150,7 +153,7 @@ class Index:
         c.dim, c.nlist, c.id_capacity, c.num_slabs = dim, nlist, id_capacity, num_slabs
         c.max_batch, c.max_queries, c.max_k = max_batch, max_queries, max_k
         c.max_nprobe = min(nlist, 1024) if max_nprobe is None else max_nprobe
-        c.max_train, c.shard_rank, c.shard_count, c.seed = max_train, shard_rank, shard_count, seed
+        c.max_train, c.shard_rank, c.shard_count, c.seed, c.flags = max_train, shard_rank, shard_count, seed, flags
         self.cfg = c
         nbytes = ctypes.c_size_t(0)
         _check(L.sivf_arena_bytes(ctypes.byref(c), ctypes.byref(nbytes)), "sivf_arena_bytes")

@@ -45,6 +45,7 @@ bool valid_config(const sivf_config* c) {
   if (c->shard_count < 1 || c->shard_rank < 0 || c->shard_rank >= c->shard_count) return false;
   if (c->max_train > 0 && c->max_train < c->nlist) return false;
   if ((int64_t)c->max_queries * c->max_nprobe > 0x7FFFFFFFll) return false;
+  if (c->flags & ~(int32_t)SIVF_CFG_NO_SCAN_COPY) return false;  // unknown flag bits
   return true;
 }
 
@@ -52,7 +53,8 @@ Layout make_layout(const sivf_config* c) {
   Layout L;
   const int64_t D = c->dim, nl = c->nlist, S = c->num_slabs;
   L.Dp = (D + 7) / 8 * 8;  // tf32 MMA K-step = 8 dims
-  L.Dh = D <= 128 ? (D + 15) / 16 * 16 : 0;  // fp16 scan copy (kind::f16 K-step = 16 dims); D > 128: none
+  // fp16 scan copy (kind::f16 K-step = 16 dims); none for D > 128 or SIVF_CFG_NO_SCAN_COPY
+  L.Dh = (D <= 128 && !(c->flags & SIVF_CFG_NO_SCAN_COPY)) ? (D + 15) / 16 * 16 : 0;
   const int64_t cap = c->id_capacity, G = c->shard_count, r = c->shard_rank;
   L.cap_local = cap > r ? (cap - r + G - 1) / G : 0;
   L.dir_arena_cap = 4 * S + 16 * nl + 1024;
@@ -475,6 +477,8 @@ sivf_rc sivf_stats(sivf_index h, sivf_stats_t* out, sivf_stream_t stream) {
   const double live_bytes = (double)out->live * (4.0 * d + 4.0);
   out->overhead_actual =
       live_bytes > 0 ? (16.0 * out->slabs_in_use + 8.0 * (double)ix->st.cap_local) / live_bytes : 0.0;
+  out->overhead_scan_copy =
+      live_bytes > 0 ? 2.0 * ix->st.Dh * kSlot * (double)out->slabs_in_use / live_bytes : 0.0;
   return SIVF_OK;
 }
 

@@ -24,11 +24,12 @@ def T(a, dtype=None):
 
 
 def make_pair(dim, nlist, cap, C, num_slabs=None, max_batch=4096, max_queries=1024, max_k=128, max_nprobe=None,
-              shard_rank=0, shard_count=1, max_train=0, tc=True, coarse=True):
+              shard_rank=0, shard_count=1, max_train=0, tc=True, coarse=True, flags=0):
     if num_slabs is None:
         num_slabs = S.num_slabs_for(cap, nlist)
     g = S.Index(dim, nlist, cap, num_slabs, max_batch=max_batch, max_queries=max_queries, max_k=max_k,
-                max_nprobe=max_nprobe, shard_rank=shard_rank, shard_count=shard_count, max_train=max_train)
+                max_nprobe=max_nprobe, shard_rank=shard_rank, shard_count=shard_count, max_train=max_train,
+                flags=flags)
     g.set_option(S.OPT_TC_SCAN, 1 if tc else 0)
     g.set_option(S.OPT_TC_COARSE, 1 if coarse else 0)
     o = O.Index(dim, nlist, cap, num_slabs=num_slabs, shard_rank=shard_rank, shard_count=shard_count)
@@ -258,6 +259,25 @@ def test_float_data_d128_rerank_path(tc):
     g2, o2 = make_pair(128, 48, 6000, np.rint(C * 1000).astype(np.float32), max_batch=6000, max_queries=300, tc=tc)
     ins(g2, o2, np.arange(6000), Xi)
     assert srch(g2, o2, np.rint(Q * 1000).astype(np.float32), 10, 8, exact=False) <= 3
+
+
+def test_no_scan_copy_flag():
+    # SIVF_CFG_NO_SCAN_COPY: the paper's footprint (no fp16 copy), search on CUDA cores, same results
+    gen = Generator(sift_shape(seed=0x51F7))
+    X = gen.range(0, 5000)
+    C = O.kmeans(X, 32, 6, 4)
+    g, o = make_pair(128, 32, 5000, C, max_batch=5000, max_queries=200, flags=S.CFG_NO_SCAN_COPY)
+    g2, o2 = make_pair(128, 32, 5000, C, max_batch=5000, max_queries=200)
+    ins(g, o, np.arange(5000), X)
+    ins(g2, o2, np.arange(5000), X)
+    dele(g, o, np.arange(0, 5000, 3))
+    dele(g2, o2, np.arange(0, 5000, 3))
+    Q = gen.queries(0, 200)
+    assert srch(g, o, Q, 10, 8) == 0 and srch(g2, o2, Q, 10, 8) == 0
+    s, s2 = g.stats(), g2.stats()
+    want = 2.0 * 128 * 32 * s2["slabs_in_use"] / (s2["live"] * (4.0 * 128 + 4.0))  # 2 Dh B per slot in use
+    assert s["overhead_scan_copy"] == 0.0 and abs(s2["overhead_scan_copy"] - want) < 1e-12
+    assert s["overhead_actual"] == s2["overhead_actual"] and g2.arena_bytes > g.arena_bytes
 
 
 @pytest.mark.parametrize("tc", [True, False], ids=["tcgen05-scan", "simt-scan"])
