@@ -2,6 +2,8 @@
 element by element on the same seeded inputs (SURVEY §8(c) parity matrix)."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -322,6 +324,58 @@ def test_sliding_window_scaled():
         o.reclaim()
         check_state(g, o, f"step {t}")
         assert g.stats()["live"] == W
+
+
+def test_full_size_sift1m_step_sampled():
+    # BASELINE configs[1] at full size, in the launch configuration bench.py times:
+    # 1M x 128 SIFT-shaped, nlist 1024, one sliding step (insert 10k + delete the 10k
+    # oldest + search 10k queries at k = 10, nprobe = 32 through sivf_sliding_window_step).
+    # Every one of the 1M + 10k assignments and the whole mutation state are compared
+    # bit-exact with the oracle; the search on a sample of 500 queries (integer data:
+    # ids and distances exact).
+    N, NL, B, NQ = 1_000_000, 1024, 10_000, 10_000
+    O.set_threads(os.cpu_count() or 1)
+    gen = Generator(sift_shape(seed=0x51F7))
+    C = gen.range(1 << 41, NL)  # quantizer: sampled points (parity does not depend on training)
+    g, o = make_pair(128, NL, N + B, C, num_slabs=S.num_slabs_for(N, NL), max_batch=100_000, max_queries=NQ,
+                     max_k=32, max_nprobe=128)
+    for b0 in range(0, N, 100_000):
+        ins(g, o, np.arange(b0, b0 + 100_000), gen.range(b0, 100_000))
+    check_state(g, o, "built")
+    new, old = np.arange(N, N + B), np.arange(0, B)
+    Xn, Q = gen.range(N, B), gen.queries(0, NQ)
+    dist, ids, status, ndel = g.sliding_window_step(T(new, torch.int64), T(Xn), T(old, torch.int64), T(Q), 10, 32)
+    ost, _ = o.insert(new, Xn)
+    assert np.array_equal(status.cpu().numpy()[:B], ost)
+    assert int(ndel.item()) == o.delete(old) == B
+    o.reclaim()
+    check_state(g, o, "after the step")
+    sample = np.random.default_rng(11).choice(NQ, 500, replace=False)
+    od, oi, _ = o.search(Q[sample], 10, 32)
+    assert np.array_equal(ids.cpu().numpy()[sample], oi)
+    assert np.array_equal(dist.cpu().numpy()[sample], od)
+
+
+def test_full_size_gist1m_mutations_sampled():
+    # BASELINE configs[2] at full size: 1M x 960 GIST-shaped float data, nlist 1024; a
+    # 10k delete batch and a 10k insert batch; 1M + 10k assignments and the mutation
+    # state bit-exact; k = 100, nprobe = 32 search on 100 sampled queries (float data:
+    # distances within 1e-4 relative, id differences only at near-ties)
+    N, NL, B = 1_000_000, 1024, 10_000
+    O.set_threads(os.cpu_count() or 1)
+    gen = Generator(gist_shape(seed=0x6157, dim=960))
+    C = gen.range(1 << 41, NL)
+    g, o = make_pair(960, NL, N + B, C, num_slabs=S.num_slabs_for(N + B, NL), max_batch=100_000, max_queries=100,
+                     max_k=128, max_nprobe=128)
+    for b0 in range(0, N, 100_000):
+        ins(g, o, np.arange(b0, b0 + 100_000), gen.range(b0, 100_000))
+    dele(g, o, np.arange(0, N, 100)[:B])
+    ins(g, o, np.arange(N, N + B), gen.range(N, B))
+    o.reclaim()
+    g.reclaim()
+    check_state(g, o, "gist 1M")
+    Q = gen.queries(0, 100)
+    assert srch(g, o, Q, 100, 32, exact=False) <= 3
 
 
 def test_merge_topk_matches_oracle():
