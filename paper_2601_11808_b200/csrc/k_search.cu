@@ -11,8 +11,9 @@
 // slab granularity) into shared memory with cp.async.bulk + mbarrier (one
 // producer warp, NS-deep ring) and every compute warp reuses it for its 4
 // queries: HBM bytes per list are read once per tile instead of once per
-// query.  The dim-interleaved slab layout [D/4][32][4] makes any 128-dim
-// chunk one contiguous block and lane=slot float4 reads conflict-free.
+// query.  In the slab layout [4 row groups][Dp/4][8][4] (pay_off()) a 128-dim
+// chunk of a slab is 4 contiguous pieces, one bulk copy each, staged as
+// [4][kCH/4][8][4] so that lane = slot float4 reads are conflict-free.
 // Lane (lq, ls) of a compute warp owns query lq and slots ls, ls+8, ls+16,
 // ls+24; distances use the difference form t = q - x, acc = fma(t, t, acc)
 // in ascending dimension order (|err| <= (D+2) u relative; exact on
