@@ -292,9 +292,12 @@ def run_sivf(args):
     status = torch.empty(BATCH, dtype=torch.int32, device=dev)
     ndel = torch.empty(1, dtype=torch.int64, device=dev)
 
-    def one_step(inp):
+    def one_step(inp, dd=None, ii=None):
         nm, Xn, om, Q = inp
-        ix.sliding_window_step(nm, Xn, om, Q, K, NPROBE, out=(out_d, out_i, status, ndel))
+        ix.sliding_window_step(nm, Xn, om, Q, K, NPROBE,
+                               out=(out_d if dd is None else dd, out_i if ii is None else ii, status, ndel))
+        if dd is not None:
+            return dd, ii
         if G > 1:
             gd, gi = shard.allgather_topk(pg, out_d, out_i)  # NCCL all-gather of the per-shard top-k
             return S.merge_topk(gd, gi)
@@ -411,9 +414,12 @@ def run_sivf(args):
         main.wait_event(ev_in[b])
         if t >= 2:
             main.wait_event(ev_out[b])  # results of step t-2 copied out of this buffer set
-        dd, ii = one_step(tuple(stage[b]))
-        res_d[b].copy_(dd, non_blocking=True)
-        res_i[b].copy_(ii, non_blocking=True)
+        if G == 1:  # results straight into this step's output buffers
+            one_step(tuple(stage[b]), res_d[b], res_i[b])
+        else:
+            dd, ii = one_step(tuple(stage[b]))
+            res_d[b].copy_(dd, non_blocking=True)
+            res_i[b].copy_(ii, non_blocking=True)
         ev_done[b].record(main)
         with torch.cuda.stream(cs):
             cs.wait_event(ev_done[b])
