@@ -223,12 +223,18 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
  *                      its other lists (when that adds no work items on
  *                      average); the bounds on the k-th distances are then
  *                      tight early.  Changes speed only, never results.
+ *   SIVF_OPT_STEP_GRAPH (default 1): sivf_sliding_window_step captures the whole
+ *                      step once per call signature (device pointers, sizes, k,
+ *                      nprobe, stream, options) as a CUDA graph and replays it on
+ *                      repeat calls (up to 4 signatures cached, LRU); the data
+ *                      are read on the device at replay time.  Not used while
+ *                      phase profiling is on; 0 = direct launches every call.
  *   SIVF_OPT_COARSE_SELECT (default 1): tensor-core coarse quantisation stores
  *                      the approximate distance matrix and selects per row (exact
  *                      m-th upper bound by bisection, candidates, exact dist32
  *                      re-rank); 0 = the fused two-pass epilogue.  Same results. */
 enum { SIVF_OPT_TC_SCAN = 1, SIVF_OPT_TC_TWO_PHASE = 2, SIVF_OPT_TC_COARSE = 3, SIVF_OPT_SEED_SLABS = 4,
-       SIVF_OPT_RANK_SPLIT = 5, SIVF_OPT_COARSE_SELECT = 6 };
+       SIVF_OPT_RANK_SPLIT = 5, SIVF_OPT_COARSE_SELECT = 6, SIVF_OPT_STEP_GRAPH = 7 };
 sivf_rc sivf_set_option(sivf_index ix, int32_t option, int64_t value);
 sivf_rc sivf_profile_read(sivf_index ix, double* h_ms, int64_t* h_count);
 

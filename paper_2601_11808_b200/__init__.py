@@ -84,6 +84,10 @@ CFG_NO_SCAN_COPY = 1  # sivf_config.flags: no fp16 scan copy (paper footprint, C
 OPT_TC_SCAN = 1
 OPT_TC_TWO_PHASE = 2
 OPT_TC_COARSE = 3
+OPT_SEED_SLABS = 4
+OPT_RANK_SPLIT = 5
+OPT_COARSE_SELECT = 6
+OPT_STEP_GRAPH = 7
 
 PHASES = ("assign", "append", "delete", "coarse", "invmap", "scan", "merge", "reclaim")
 

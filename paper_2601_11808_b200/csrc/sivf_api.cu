@@ -301,6 +301,7 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   k_init<<<ceil_div(m, 256), 256, 0, s>>>(st);
   ix->launches += 1;
   cudaStreamCreateWithFlags(&ix->side, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&ix->cap_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ix->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ix->ev_join, cudaEventDisableTiming);
   cudaError_t e = setup_search_kernels(*ix);
@@ -390,22 +391,12 @@ sivf_rc sivf_reclaim(sivf_index h, int64_t* d_nreclaimed, sivf_stream_t stream) 
   return cuda_rc(launch_reclaim(*reinterpret_cast<Index*>(h), d_nreclaimed, reinterpret_cast<cudaStream_t>(stream)));
 }
 
-sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const float* d_new_x, int64_t n_new,
-                                 const int64_t* d_old_ids, int64_t n_old, const float* d_q, int64_t nq, int32_t k,
-                                 int32_t nprobe, float* d_dist, int64_t* d_ids, int32_t* d_status,
-                                 int64_t* d_ndeleted, sivf_stream_t stream) {
-  if (!h) return SIVF_E_INVALID_ARG;
-  Index* ix = reinterpret_cast<Index*>(h);
-  if (n_new < 0 || n_new > ix->cfg.max_batch || n_old < 0 || nq < 0 || nq > ix->cfg.max_queries)
-    return SIVF_E_INVALID_ARG;
-  if ((n_new > 0 && (!d_new_ids || !d_new_x)) || (n_old > 0 && !d_old_ids)) return SIVF_E_INVALID_ARG;
-  if (nq > 0) {
-    if (k < 1 || k > ix->cfg.max_k || nprobe < 1 || nprobe > ix->cfg.max_nprobe || nprobe > ix->st.nlist)
-      return SIVF_E_INVALID_ARG;
-    if (!d_q || !d_dist || !d_ids) return SIVF_E_INVALID_ARG;
-  }
-  if (!ix->trained) return SIVF_E_NOT_TRAINED;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+// One sliding-window step enqueued on s (direct launches; also the body captured by
+// the step graph cache).
+static sivf_rc sliding_step_body(Index* ix, const int64_t* d_new_ids, const float* d_new_x, int64_t n_new,
+                          const int64_t* d_old_ids, int64_t n_old, const float* d_q, int64_t nq, int32_t k,
+                          int32_t nprobe, float* d_dist, int64_t* d_ids, int32_t* d_status, int64_t* d_ndeleted,
+                          cudaStream_t s) {
   // The search's coarse quantisation and inverse probe map read only centroids and
   // queries, so they run on a side stream concurrently with insert + delete; the
   // scan joins after the mutations (C22: the search sees the post-step window).
@@ -428,6 +419,86 @@ sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const f
   if (e == cudaSuccess && nq > 0) e = launch_search_back(*ix, sp, d_q, nq, k, nprobe, d_dist, d_ids, s);
   if (e == cudaSuccess) e = launch_reclaim(*ix, nullptr, s);
   return cuda_rc(e);
+}
+
+
+sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const float* d_new_x, int64_t n_new,
+                                 const int64_t* d_old_ids, int64_t n_old, const float* d_q, int64_t nq, int32_t k,
+                                 int32_t nprobe, float* d_dist, int64_t* d_ids, int32_t* d_status,
+                                 int64_t* d_ndeleted, sivf_stream_t stream) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (n_new < 0 || n_new > ix->cfg.max_batch || n_old < 0 || nq < 0 || nq > ix->cfg.max_queries)
+    return SIVF_E_INVALID_ARG;
+  if ((n_new > 0 && (!d_new_ids || !d_new_x)) || (n_old > 0 && !d_old_ids)) return SIVF_E_INVALID_ARG;
+  if (nq > 0) {
+    if (k < 1 || k > ix->cfg.max_k || nprobe < 1 || nprobe > ix->cfg.max_nprobe || nprobe > ix->st.nlist)
+      return SIVF_E_INVALID_ARG;
+    if (!d_q || !d_dist || !d_ids) return SIVF_E_INVALID_ARG;
+  }
+  if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cst) != cudaSuccess) {
+    cudaGetLastError();
+    cst = cudaStreamCaptureStatusActive;  // unknown: stay with direct launches
+  }
+  // a caller that is itself capturing s gets the launches recorded into its graph
+  if (ix->step_graph && !ix->prof && ix->cap_stream && cst == cudaStreamCaptureStatusNone) {
+    // repeat calls with the same signature replay one CUDA graph of the whole step
+    // (every launch parameter is a function of the signature and the options; the
+    // data are read on the device at replay time)
+    Index::StepGraph key;
+    const void* p[8] = {d_new_ids, d_new_x, d_old_ids, d_q, d_dist, d_ids, d_status, d_ndeleted};
+    for (int i = 0; i < 8; ++i) key.p[i] = p[i];
+    key.n[0] = n_new, key.n[1] = n_old, key.n[2] = nq;
+    key.k = nq > 0 ? k : 0, key.nprobe = nq > 0 ? nprobe : 0, key.s = s, key.epoch = ix->opt_epoch;
+    auto same = [&](const Index::StepGraph& g) {
+      if (!g.exec || g.s != key.s || g.epoch != key.epoch || g.k != key.k || g.nprobe != key.nprobe) return false;
+      for (int i = 0; i < 8; ++i)
+        if (g.p[i] != key.p[i]) return false;
+      return g.n[0] == key.n[0] && g.n[1] == key.n[1] && g.n[2] == key.n[2];
+    };
+    Index::StepGraph* hit = nullptr;
+    Index::StepGraph* victim = &ix->step_graphs[0];
+    for (auto& g : ix->step_graphs) {
+      if (same(g)) hit = &g;
+      if (g.used < victim->used) victim = &g;
+    }
+    if (!hit) {
+      // capture on cap_stream (the caller's stream may be the legacy default stream)
+      cudaGraph_t graph = nullptr;
+      const int64_t l0 = ix->launches;
+      cudaError_t e = cudaStreamBeginCapture(ix->cap_stream, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        const sivf_rc rc = sliding_step_body(ix, d_new_ids, d_new_x, n_new, d_old_ids, n_old, d_q, nq, k, nprobe,
+                                             d_dist, d_ids, d_status, d_ndeleted, ix->cap_stream);
+        e = cudaStreamEndCapture(ix->cap_stream, &graph);
+        if (rc != SIVF_OK && e == cudaSuccess) e = cudaErrorUnknown;
+      }
+      cudaGraphExec_t exec = nullptr;
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        ix->launches = l0;
+        ix->step_graph = false;  // not capturable here: direct launches from now on
+        return sliding_step_body(ix, d_new_ids, d_new_x, n_new, d_old_ids, n_old, d_q, nq, k, nprobe, d_dist,
+                                 d_ids, d_status, d_ndeleted, s);
+      }
+      if (victim->exec) cudaGraphExecDestroy(victim->exec);
+      *victim = key;
+      victim->exec = exec;
+      victim->launches = ix->launches - l0;
+      ix->launches = l0;
+      hit = victim;
+    }
+    hit->used = ++ix->step_tick;
+    ix->launches += hit->launches;
+    return cuda_rc(cudaGraphLaunch(hit->exec, s));
+  }
+  return sliding_step_body(ix, d_new_ids, d_new_x, n_new, d_old_ids, n_old, d_q, nq, k, nprobe, d_dist, d_ids,
+                           d_status, d_ndeleted, s);
 }
 
 sivf_rc sivf_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int32_t G, int64_t nq, int32_t k,
@@ -489,7 +560,9 @@ int64_t sivf_launch_count(sivf_index h) { return h ? reinterpret_cast<Index*>(h)
 sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
   if (!h) return SIVF_E_INVALID_ARG;
   Index* ix = reinterpret_cast<Index*>(h);
+  ++ix->opt_epoch;  // cached step graphs captured under other options never match again
   switch (option) {
+    case SIVF_OPT_STEP_GRAPH: ix->step_graph = value != 0; return SIVF_OK;
     case SIVF_OPT_TC_SCAN: ix->use_tc_scan = value != 0; return SIVF_OK;
     case SIVF_OPT_TC_TWO_PHASE: ix->tc_two_phase = value < 0 ? 0 : (int)value; return SIVF_OK;
     case SIVF_OPT_TC_COARSE: ix->use_tc_coarse = value != 0; return SIVF_OK;

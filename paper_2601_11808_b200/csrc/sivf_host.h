@@ -97,9 +97,6 @@ struct Index {
   int dbg = 0;                // experiment switches (SIVF_OPT_DEBUG)
   int seed_slabs = 0;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS; off: it costs more than it saves)
   int64_t launches = 0;
-  // TMA descriptor (CUtensorMap, 128 B) of the payload viewed as rows of 512 B
-  // (row = slab * Dp/4 + c4), box 128 floats x 1 row: the tile::gather4 source
-  // of k_scan_tc (encoded once in setup_scan_tc; the payload never moves).
   alignas(64) unsigned char coarse_tmap[128] = {};  // TMA store descriptor of sc.coarse (k_coarse_tc.cu)
   bool coarse_tmap_ok = false;
   alignas(64) unsigned char qcoarse_tmap[128] = {};  // TMA store descriptor of sc.qcoarse
@@ -107,6 +104,23 @@ struct Index {
   bool coarse_alt = false;    // launch_coarse_tc: use the search-front scratch set
   cudaStream_t side = nullptr;  // second stream for the sliding step's search front
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // sliding-step graph cache (SIVF_OPT_STEP_GRAPH): one instantiated CUDA graph per
+  // distinct call signature (pointers, sizes, stream, options epoch), replayed on
+  // repeat calls; captured on cap_stream, launched on the caller's stream
+  struct StepGraph {
+    const void* p[8] = {};
+    int64_t n[3] = {};
+    int32_t k = 0, nprobe = 0;
+    cudaStream_t s = nullptr;
+    uint64_t epoch = 0, used = 0;
+    int64_t launches = 0;
+    cudaGraphExec_t exec = nullptr;
+  };
+  static constexpr int kStepGraphs = 4;
+  StepGraph step_graphs[kStepGraphs];
+  bool step_graph = true;
+  uint64_t opt_epoch = 1, step_tick = 0;
+  cudaStream_t cap_stream = nullptr;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
   // phase profiling (sivf_profile_*)
@@ -127,6 +141,9 @@ struct Index {
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    for (auto& g : step_graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     for (auto& r : recs) {
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);

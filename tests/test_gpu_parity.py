@@ -378,6 +378,49 @@ def test_full_size_gist1m_mutations_sampled():
     assert srch(g, o, Q, 100, 32, exact=False) <= 3
 
 
+def test_sliding_window_step_graph_replay():
+    # SIVF_OPT_STEP_GRAPH: repeat calls with the same buffers replay one captured CUDA
+    # graph; each replay must read the current inputs and index state (bit-exact vs the
+    # oracle every step), a new signature (k, nprobe) or an option change recaptures
+    gen = Generator(sift_shape(seed=0x51F7))
+    W, B = 20000, 1000
+    C = O.kmeans(gen.train(4000), 64, 10, 9)
+    cap = W + B * 14
+    g, o = make_pair(128, 64, cap, C, num_slabs=S.num_slabs_for(W, 64) + 2 * (B // 32 + 64), max_batch=W,
+                     max_queries=100)
+    ins(g, o, np.arange(W), gen.range(0, W))
+    new_d = torch.empty(B, dtype=torch.int64, device="cuda")
+    x_d = torch.empty(B, 128, device="cuda")
+    old_d = torch.empty(B, dtype=torch.int64, device="cuda")
+    q_d = torch.empty(100, 128, device="cuda")
+    st_d = torch.empty(B, dtype=torch.int32, device="cuda")
+    nd_d = torch.empty(1, dtype=torch.int64, device="cuda")
+    outs = {kk: (torch.empty(100, kk, device="cuda"), torch.empty(100, kk, dtype=torch.int64, device="cuda"))
+            for kk in (10, 16)}
+    launches = []
+    for t in range(13):
+        k, npb = (10, 16) if t < 6 else (16, 8)
+        if t == 9:
+            g.set_option(S.OPT_RANK_SPLIT, 0)  # options epoch: recapture
+        new, old = np.arange(W + t * B, W + (t + 1) * B), np.arange(t * B, (t + 1) * B)
+        new_d.copy_(T(new, torch.int64))
+        x_d.copy_(T(gen.range(new[0], B)))
+        old_d.copy_(T(old, torch.int64))
+        q_d.copy_(T(gen.queries(t * 100, 100)))
+        l0 = g.launch_count()
+        dist, ids, status, ndel = g.sliding_window_step(new_d, x_d, old_d, q_d, k, npb,
+                                                        out=(outs[k][0], outs[k][1], st_d, nd_d))
+        launches.append(g.launch_count() - l0)
+        ost, _ = o.insert(new, gen.range(new[0], B))
+        assert np.array_equal(status.cpu().numpy()[:B], ost)
+        assert int(ndel.item()) == o.delete(old) == B
+        od, oi, _ = o.search(gen.queries(t * 100, 100), k, npb)
+        assert np.array_equal(ids.cpu().numpy(), oi) and np.array_equal(dist.cpu().numpy(), od), f"step {t}"
+        o.reclaim()
+        check_state(g, o, f"step {t}")
+    assert min(launches) > 0 and len(set(launches[1:6])) == 1  # replays count the captured kernels
+
+
 def test_merge_topk_matches_oracle():
     rng = np.random.default_rng(8)
     G, nq, k = 4, 50, 10
