@@ -500,7 +500,7 @@ cudaError_t launch_search_front(Index& ix, const SearchPlan& p, const float* d_q
 
 // Slab scan + per-query merge (reads the index state).
 cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q, int64_t nq, int32_t k,
-                               int32_t nprobe, float* d_dist, int64_t* d_ids, cudaStream_t s) {
+                               int32_t nprobe, float* d_dist, int64_t* d_ids, cudaStream_t s, cudaEvent_t after_scan) {
   Scratch& sc = ix.sc;
   cudaError_t e = cudaSuccess;
   ScanArgs a{ix.st, d_q, nprobe, k, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial};
@@ -528,6 +528,7 @@ cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q,
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return e;  // a failed scan launch must not be masked by the merge below
   }
+  if (after_scan) cudaEventRecord(after_scan, s);  // the index is no longer read by this search
   PhaseTimer pt(ix, SIVF_PH_MERGE, s);
   const int wpb = 4;
   if (nprobe <= 32 && k <= 16) {

@@ -416,6 +416,18 @@ static sivf_rc sliding_step_body(Index* ix, const int64_t* d_new_ids, const floa
   if (e == cudaSuccess) e = launch_delete(*ix, d_old_ids, n_old, d_ndeleted, s);
   if (fork) cudaStreamWaitEvent(s, ix->ev_join, 0);  // always join, even after an error
   if (e == cudaSuccess && nq > 0 && !fork) e = launch_search_front(*ix, sp, d_q, nq, nprobe, nullptr, s);
+  if (e == cudaSuccess && nq > 0 && ix->side && !ix->prof) {
+    // the merge reads only the per-(query, probe) partial lists: the reclaim (which
+    // rewrites directories) runs beside it on the side stream once the scan is done
+    e = launch_search_back(*ix, sp, d_q, nq, k, nprobe, d_dist, d_ids, s, ix->ev_fork);
+    if (e == cudaSuccess) {
+      cudaStreamWaitEvent(ix->side, ix->ev_fork, 0);
+      e = launch_reclaim(*ix, nullptr, ix->side);
+      cudaEventRecord(ix->ev_join, ix->side);
+      cudaStreamWaitEvent(s, ix->ev_join, 0);
+    }
+    return cuda_rc(e);
+  }
   if (e == cudaSuccess && nq > 0) e = launch_search_back(*ix, sp, d_q, nq, k, nprobe, d_dist, d_ids, s);
   if (e == cudaSuccess) e = launch_reclaim(*ix, nullptr, s);
   return cuda_rc(e);
