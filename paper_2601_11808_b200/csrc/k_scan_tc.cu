@@ -3,55 +3,62 @@
 // Work decomposition as in k_search.cu (a work item = list l x a tile of
 // <= 128 queries probing l).  Eq. l2 for (query tile, slabs) is a
 // dense contraction:  d(q, x) = ||q||^2 + ||x||^2 - 2 q.x.
-// q.x runs on tcgen05.mma kind::tf32 with M = 128 queries (A, resident in
-// TMEM), N = 128 slots = a GROUP of 4 slabs (B, shared memory), K = 8 per
-// instruction, fp32 accumulators in TMEM.
+// q.x runs on tcgen05.mma kind::f16 (fp16 operands, fp32 accumulation) with
+// M = 128 queries (A, resident in TMEM), N = 128 slots = a GROUP of 4 slabs
+// (B, shared memory), K = 16 per instruction, accumulators in TMEM.  The B
+// operand is the slab's fp16 (RN) copy written by k_append beside the fp32
+// payload (reading C35); kind::f16 with A in TMEM issues a 128x128x16 MMA per
+// 68 cycles, 4x the kind::tf32 TMEM-A rate (tools/mma_probe.cu).
 //
 // Why groups of 4 slabs: one MMA re-reads the whole A tile, so an N=32 (one
 // slab) instruction costs as much as N=128 (tools/mma_probe.cu).  The B
 // operand must be K-major SWIZZLE_NONE with a uniform 8-row-group stride.  The
-// slab payload is stored as exactly that (pay_off(): [4 row groups][Dp/4][8
-// slots][4 dims], LBO = 128 B, SBO = 32 Dp B), so each slab of a group is ONE
-// contiguous cp.async.bulk of 16 KB into consecutive stage slots and the four
-// together are the N = 128 operand.  No gather, no shared-memory transpose;
-// bulk copies stream 2x faster than TMA tile::gather4 from L2 and the same
-// from HBM (tools/g4_probe.cu).
+// fp16 copy is stored as exactly that (pay16_off(): [4 row groups][Dh/8][8
+// slots][8 halves], LBO = 128 B, SBO = 16 Dh B), so each slab of a group is
+// ONE contiguous cp.async.bulk of 8 KB into consecutive stage slots and the
+// four together are the N = 128 operand.  No gather, no shared-memory
+// transpose (bulk copies stream 2x faster than TMA tile::gather4 from L2,
+// tools/g4_probe.cu).
 //
-// Roles (1 persistent CTA per SM, 10 warps, no CTA-wide barrier after setup;
+// Roles (1 persistent CTA per SM, 15 warps, no CTA-wide barrier after setup;
 // every hand-off is an mbarrier):
-//   warp 0      producer: claims work items (one ahead, published in a
-//               4-entry item ring), walks the list's slab directory, keeps
-//               the live slabs (bitmap != 0, Eq. slot_valid at slab
-//               granularity) and issues bulk copies of the slab payloads,
-//               slot norms and ids into an nst-stage group ring
+//   warp 0      scheduler: claims work items (up to NITEM - 1 ahead, in an
+//               item ring) and walks each list's slab directory ahead of
+//               the producer, keeping the live slabs (bitmap != 0, Eq.
+//               slot_valid at slab granularity) with their flags
+//   warp 14     producer: per group of 4 live slabs, bulk copies of the fp16
+//               payloads, slot norms and ids into an nst-stage ring; a stage
+//               is refilled once the group that used it has completed
 //   warp 1      MMA: per group turns the bitmap into a NaN mask on the slot
 //               norms (group metadata for the epilogue), then one lane
-//               issues Dp/8 tcgen05.mma into one of two TMEM accumulators;
-//               tcgen05.commit frees the stage and signals the epilogue
-//   warps 2-5   query loaders: load the next item's 128 query rows into the
-//               shared-memory A tile once the previous item's MMAs are done
-//               (the first half of each row is in registers by then), with
-//               ||q||^2 and an integrality flag.  A sits in shared memory, not
-//               TMEM: kind::tf32 with A in TMEM issues at half the rate
-//               (142 vs 71.5 cycles per 128x128x8 MMA, tools/mma_probe.cu)
-//   warps 6-9   epilogue: thread = query row (TMEM lane); per slab,
+//               issues Dh/16 tcgen05.mma into one of NB = 3 TMEM accumulators;
+//               one tcgen05.commit per group (each costs ~200 cycles of
+//               tensor pipe) signals the epilogue and frees the stage
+//   warps 2-5   query loaders: the next item's 128 query rows as fp16 into
+//               the spare one of two TMEM A buffers (double-buffered across
+//               items), with ||q||^2 (fp32), the integrality and fp16-range
+//               flags (QInfo ring: up to NQI items ahead of the epilogue)
+//   warps 6-13  epilogue: thread = (query row, slab half); per slab,
 //               t = ||x||^2 - 2 q.x is one FFMA and the slab's filter one
 //               FMNMX per candidate; only chunks whose min passes the row's
 //               threshold take the per-lane slow path (exact distance, then
-//               a sorted register top-k of (dist, id) keys)
-// TMEM columns: D[b] = [128 b, 128 b + 128), b < NB = 4.  The query tile (A) is in shared memory.
+//               a sorted register top-k of (dist, id) keys); the two halves
+//               of a row merge at the item's end
+// TMEM columns: A[0] [0,64), A[1] [64,128), D[b] = [128 + 128 b, 256 + 128 b), b < 3.
 //
 // Exactness (BASELINE.json tolerances): when query and slab values are
-// integers with |v| <= 2048 (tf32-exact; slab flag set by k_append) and
+// integers with |v| <= 2048 (exact in fp16; slab flag set by k_append) and
 // (||q|| + ||x||)^2 < 2^24, every product, partial sum, t and ||q||^2 + t is
 // an exact integer: the tensor-core distance IS the exact distance (the
 // SIFT-shaped case).  Otherwise the value only filters: a slot is re-ranked
 // with the exact fp32 difference form iff t <= (thr - ||q||^2) + E, rounded
 // up, E a certified bound on |d_tc - d_exact| evaluated at the slab's largest
-// ||x||^2 (tf32 truncation + fp32 accumulation + the roundings of t and the
-// norms, safety factor 2), so no member of the exact top-k is ever dropped.
-// thr is the row's current k-th distance, seeded from a per-query bound
-// (atomicMin of the k-th distance of finished items of the same query).
+// ||x||^2 (operand rounding + fp32 accumulation + subnormals + the roundings
+// of t and the norms, safety factor 2), so no member of the exact top-k is
+// ever dropped; a slab or query without a finite fp16 copy (|v| > 65504)
+// re-ranks every valid slot.  thr is the row's current k-th distance, seeded
+// from a per-query bound (atomicMin of the k-th distance of the query's
+// other items, read every group).
 #include <cuda.h>
 #include <cuda_fp16.h>
 
