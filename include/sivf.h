@@ -224,11 +224,12 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
  *                      average); the bounds on the k-th distances are then
  *                      tight early.  Changes speed only, never results.
  *   SIVF_OPT_STEP_GRAPH (default 1): sivf_sliding_window_step captures the whole
- *                      step once per call signature (device pointers, sizes, k,
- *                      nprobe, stream, options) as a CUDA graph and replays it on
- *                      repeat calls (up to 4 signatures cached, LRU); the data
- *                      are read on the device at replay time.  Not used while
- *                      phase profiling is on; 0 = direct launches every call.
+ *                      step as a CUDA graph the second time it sees a call
+ *                      signature (device pointers, sizes, k, nprobe, stream,
+ *                      options) and replays it on later calls (up to 4 graphs,
+ *                      LRU); the data are read on the device at replay time.
+ *                      Direct launches while phase profiling is on or when the
+ *                      caller's stream is being captured; 0 = always direct.
  *   SIVF_OPT_COARSE_SELECT (default 1): tensor-core coarse quantisation stores
  *                      the approximate distance matrix and selects per row (exact
  *                      m-th upper bound by bisection, candidates, exact dist32

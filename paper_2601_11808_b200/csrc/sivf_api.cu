@@ -465,12 +465,14 @@ sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const f
     for (int i = 0; i < 8; ++i) key.p[i] = p[i];
     key.n[0] = n_new, key.n[1] = n_old, key.n[2] = nq;
     key.k = nq > 0 ? k : 0, key.nprobe = nq > 0 ? nprobe : 0, key.s = s, key.epoch = ix->opt_epoch;
-    auto same = [&](const Index::StepGraph& g) {
-      if (!g.exec || g.s != key.s || g.epoch != key.epoch || g.k != key.k || g.nprobe != key.nprobe) return false;
+    auto same_sig = [&](const Index::StepGraph& g) {
+      if (g.used == 0 || g.s != key.s || g.epoch != key.epoch || g.k != key.k || g.nprobe != key.nprobe)
+        return false;
       for (int i = 0; i < 8; ++i)
         if (g.p[i] != key.p[i]) return false;
       return g.n[0] == key.n[0] && g.n[1] == key.n[1] && g.n[2] == key.n[2];
     };
+    auto same = [&](const Index::StepGraph& g) { return g.exec && same_sig(g); };
     Index::StepGraph* hit = nullptr;
     Index::StepGraph* victim = &ix->step_graphs[0];
     for (auto& g : ix->step_graphs) {
@@ -478,6 +480,21 @@ sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const f
       if (g.used < victim->used) victim = &g;
     }
     if (!hit) {
+      // a signature is captured on its second call: callers that pass fresh buffers
+      // every step never pay for a capture
+      Index::StepGraph* seen = nullptr;
+      Index::StepGraph* oldest = &ix->step_seen[0];
+      for (auto& g : ix->step_seen) {
+        if (same_sig(g)) seen = &g;
+        if (g.used < oldest->used) oldest = &g;
+      }
+      if (!seen) {
+        *oldest = key;
+        oldest->used = ++ix->step_tick;
+        return sliding_step_body(ix, d_new_ids, d_new_x, n_new, d_old_ids, n_old, d_q, nq, k, nprobe, d_dist,
+                                 d_ids, d_status, d_ndeleted, s);
+      }
+      seen->used = 0;  // promoted to a captured graph below
       // capture on cap_stream (the caller's stream may be the legacy default stream)
       cudaGraph_t graph = nullptr;
       const int64_t l0 = ix->launches;

@@ -118,6 +118,7 @@ struct Index {
   };
   static constexpr int kStepGraphs = 4;
   StepGraph step_graphs[kStepGraphs];
+  StepGraph step_seen[kStepGraphs];  // signatures seen once (captured on their second call)
   bool step_graph = true;
   uint64_t opt_epoch = 1, step_tick = 0;
   cudaStream_t cap_stream = nullptr;
