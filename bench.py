@@ -460,6 +460,9 @@ def run_sivf(args):
         gt = (torch.cat(gt) + lo).cpu().numpy()
         del Xl
         for npb in (1, 2, 4, 8, 16, 32, 64, 128):
+            for _ in range(2):  # warm-up (the API captures a repeated call as a graph on its 2nd sighting)
+                ix.search(Qs, K, npb)
+            torch.cuda.synchronize()
             reps = []
             for _ in range(3):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -717,7 +720,8 @@ def leg_gist(S, dev, log):
     gt = torch.cat(gt).cpu().numpy()
     sweep, qps_at_09, np_at_09 = {}, None, None
     for npb in (4, 8, 16, 32, 64):
-        ix.search(Q, KG, npb)
+        for _ in range(2):  # warm-up (graph capture on the 2nd sighting of a call)
+            ix.search(Q, KG, npb)
         torch.cuda.synchronize()
         reps_ms = []
         for _ in range(3):
@@ -856,7 +860,8 @@ def leg_h(S, dev, log, G, rank, pg, n_total):
 
     sweep, qps_at_09, np_at_09 = {}, None, None
     for npb in (8, 16, 32, 64):
-        search(npb)
+        for _ in range(2):  # warm-up (graph capture on the 2nd sighting of a call)
+            search(npb)
         torch.cuda.synchronize()
         times = []
         for _ in range(3):

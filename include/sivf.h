@@ -223,8 +223,8 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
  *                      its other lists (when that adds no work items on
  *                      average); the bounds on the k-th distances are then
  *                      tight early.  Changes speed only, never results.
- *   SIVF_OPT_STEP_GRAPH (default 1): sivf_sliding_window_step captures the whole
- *                      step as a CUDA graph the second time it sees a call
+ *   SIVF_OPT_STEP_GRAPH (default 1): sivf_sliding_window_step and sivf_search
+ *                      capture the call as a CUDA graph the second time they see a call
  *                      signature (device pointers, sizes, k, nprobe, stream,
  *                      options) and replays it on later calls (up to 4 graphs,
  *                      LRU); the data are read on the device at replay time.

@@ -374,6 +374,89 @@ sivf_rc sivf_delete(sivf_index h, const int64_t* d_ids, int64_t n, int64_t* d_nd
   return cuda_rc(launch_delete(*ix, d_ids, n, d_ndeleted, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+}  // extern "C" (a template helper follows)
+
+// Graph cache of repeated API calls (SIVF_OPT_STEP_GRAPH): `body(stream)` enqueues
+// the call's launches; a call signature (key) is captured as a CUDA graph on its
+// second sighting and replayed afterwards.  Direct launches while profiling or when
+// the caller's stream is itself being captured.
+template <class Body>
+static sivf_rc graph_cached(Index* ix, Index::StepGraph key, cudaStream_t s, Body&& body) {
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cst) != cudaSuccess) {
+    cudaGetLastError();
+    cst = cudaStreamCaptureStatusActive;  // unknown: stay with direct launches
+  }
+  // a caller that is itself capturing s gets the launches recorded into its graph
+  if (ix->step_graph && !ix->prof && ix->cap_stream && cst == cudaStreamCaptureStatusNone) {
+    // repeat calls with the same signature replay one CUDA graph of the whole step
+    // (every launch parameter is a function of the signature and the options; the
+    // data are read on the device at replay time)
+    key.s = s, key.epoch = ix->opt_epoch;
+    auto same_sig = [&](const Index::StepGraph& g) {
+      if (g.used == 0 || g.kind != key.kind || g.s != key.s || g.epoch != key.epoch || g.k != key.k ||
+          g.nprobe != key.nprobe)
+        return false;
+      for (int i = 0; i < 8; ++i)
+        if (g.p[i] != key.p[i]) return false;
+      return g.n[0] == key.n[0] && g.n[1] == key.n[1] && g.n[2] == key.n[2];
+    };
+    auto same = [&](const Index::StepGraph& g) { return g.exec && same_sig(g); };
+    Index::StepGraph* hit = nullptr;
+    Index::StepGraph* victim = &ix->step_graphs[0];
+    for (auto& g : ix->step_graphs) {
+      if (same(g)) hit = &g;
+      if (g.used < victim->used) victim = &g;
+    }
+    if (!hit) {
+      // a signature is captured on its second call: callers that pass fresh buffers
+      // every step never pay for a capture
+      Index::StepGraph* seen = nullptr;
+      Index::StepGraph* oldest = &ix->step_seen[0];
+      for (auto& g : ix->step_seen) {
+        if (same_sig(g)) seen = &g;
+        if (g.used < oldest->used) oldest = &g;
+      }
+      if (!seen) {
+        *oldest = key;
+        oldest->used = ++ix->step_tick;
+        return body(s);
+      }
+      seen->used = 0;  // promoted to a captured graph below
+      // capture on cap_stream (the caller's stream may be the legacy default stream)
+      cudaGraph_t graph = nullptr;
+      const int64_t l0 = ix->launches;
+      cudaError_t e = cudaStreamBeginCapture(ix->cap_stream, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        const sivf_rc rc = body(ix->cap_stream);
+        e = cudaStreamEndCapture(ix->cap_stream, &graph);
+        if (rc != SIVF_OK && e == cudaSuccess) e = cudaErrorUnknown;
+      }
+      cudaGraphExec_t exec = nullptr;
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        ix->launches = l0;
+        ix->step_graph = false;  // not capturable here: direct launches from now on
+        return body(s);
+      }
+      if (victim->exec) cudaGraphExecDestroy(victim->exec);
+      *victim = key;
+      victim->exec = exec;
+      victim->launches = ix->launches - l0;
+      ix->launches = l0;
+      hit = victim;
+    }
+    hit->used = ++ix->step_tick;
+    ix->launches += hit->launches;
+    return cuda_rc(cudaGraphLaunch(hit->exec, s));
+  }
+  return body(s);
+}
+
+extern "C" {
+
 sivf_rc sivf_search(sivf_index h, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
                     int64_t* d_ids, int32_t* d_probes, sivf_stream_t stream) {
   if (!h) return SIVF_E_INVALID_ARG;
@@ -383,7 +466,14 @@ sivf_rc sivf_search(sivf_index h, const float* d_q, int64_t nq, int32_t k, int32
   if (nprobe < 1 || nprobe > ix->cfg.max_nprobe || nprobe > ix->st.nlist) return SIVF_E_INVALID_ARG;
   if (nq > 0 && (!d_q || !d_dist || !d_ids)) return SIVF_E_INVALID_ARG;
   if (!ix->trained) return SIVF_E_NOT_TRAINED;
-  return cuda_rc(launch_search(*ix, d_q, nq, k, nprobe, d_dist, d_ids, d_probes, reinterpret_cast<cudaStream_t>(stream)));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Index::StepGraph key;
+  const void* p[8] = {d_q, d_dist, d_ids, d_probes, nullptr, nullptr, nullptr, nullptr};
+  for (int i = 0; i < 8; ++i) key.p[i] = p[i];
+  key.n[2] = nq, key.k = k, key.nprobe = nprobe, key.kind = 1;
+  return graph_cached(ix, key, s, [&](cudaStream_t cs) {
+    return cuda_rc(launch_search(*ix, d_q, nq, k, nprobe, d_dist, d_ids, d_probes, cs));
+  });
 }
 
 sivf_rc sivf_reclaim(sivf_index h, int64_t* d_nreclaimed, sivf_stream_t stream) {
@@ -450,85 +540,17 @@ sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const f
   }
   if (!ix->trained) return SIVF_E_NOT_TRAINED;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(s, &cst) != cudaSuccess) {
-    cudaGetLastError();
-    cst = cudaStreamCaptureStatusActive;  // unknown: stay with direct launches
-  }
-  // a caller that is itself capturing s gets the launches recorded into its graph
-  if (ix->step_graph && !ix->prof && ix->cap_stream && cst == cudaStreamCaptureStatusNone) {
-    // repeat calls with the same signature replay one CUDA graph of the whole step
-    // (every launch parameter is a function of the signature and the options; the
-    // data are read on the device at replay time)
-    Index::StepGraph key;
-    const void* p[8] = {d_new_ids, d_new_x, d_old_ids, d_q, d_dist, d_ids, d_status, d_ndeleted};
-    for (int i = 0; i < 8; ++i) key.p[i] = p[i];
-    key.n[0] = n_new, key.n[1] = n_old, key.n[2] = nq;
-    key.k = nq > 0 ? k : 0, key.nprobe = nq > 0 ? nprobe : 0, key.s = s, key.epoch = ix->opt_epoch;
-    auto same_sig = [&](const Index::StepGraph& g) {
-      if (g.used == 0 || g.s != key.s || g.epoch != key.epoch || g.k != key.k || g.nprobe != key.nprobe)
-        return false;
-      for (int i = 0; i < 8; ++i)
-        if (g.p[i] != key.p[i]) return false;
-      return g.n[0] == key.n[0] && g.n[1] == key.n[1] && g.n[2] == key.n[2];
-    };
-    auto same = [&](const Index::StepGraph& g) { return g.exec && same_sig(g); };
-    Index::StepGraph* hit = nullptr;
-    Index::StepGraph* victim = &ix->step_graphs[0];
-    for (auto& g : ix->step_graphs) {
-      if (same(g)) hit = &g;
-      if (g.used < victim->used) victim = &g;
-    }
-    if (!hit) {
-      // a signature is captured on its second call: callers that pass fresh buffers
-      // every step never pay for a capture
-      Index::StepGraph* seen = nullptr;
-      Index::StepGraph* oldest = &ix->step_seen[0];
-      for (auto& g : ix->step_seen) {
-        if (same_sig(g)) seen = &g;
-        if (g.used < oldest->used) oldest = &g;
-      }
-      if (!seen) {
-        *oldest = key;
-        oldest->used = ++ix->step_tick;
-        return sliding_step_body(ix, d_new_ids, d_new_x, n_new, d_old_ids, n_old, d_q, nq, k, nprobe, d_dist,
-                                 d_ids, d_status, d_ndeleted, s);
-      }
-      seen->used = 0;  // promoted to a captured graph below
-      // capture on cap_stream (the caller's stream may be the legacy default stream)
-      cudaGraph_t graph = nullptr;
-      const int64_t l0 = ix->launches;
-      cudaError_t e = cudaStreamBeginCapture(ix->cap_stream, cudaStreamCaptureModeThreadLocal);
-      if (e == cudaSuccess) {
-        const sivf_rc rc = sliding_step_body(ix, d_new_ids, d_new_x, n_new, d_old_ids, n_old, d_q, nq, k, nprobe,
-                                             d_dist, d_ids, d_status, d_ndeleted, ix->cap_stream);
-        e = cudaStreamEndCapture(ix->cap_stream, &graph);
-        if (rc != SIVF_OK && e == cudaSuccess) e = cudaErrorUnknown;
-      }
-      cudaGraphExec_t exec = nullptr;
-      if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
-      if (graph) cudaGraphDestroy(graph);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        ix->launches = l0;
-        ix->step_graph = false;  // not capturable here: direct launches from now on
-        return sliding_step_body(ix, d_new_ids, d_new_x, n_new, d_old_ids, n_old, d_q, nq, k, nprobe, d_dist,
-                                 d_ids, d_status, d_ndeleted, s);
-      }
-      if (victim->exec) cudaGraphExecDestroy(victim->exec);
-      *victim = key;
-      victim->exec = exec;
-      victim->launches = ix->launches - l0;
-      ix->launches = l0;
-      hit = victim;
-    }
-    hit->used = ++ix->step_tick;
-    ix->launches += hit->launches;
-    return cuda_rc(cudaGraphLaunch(hit->exec, s));
-  }
-  return sliding_step_body(ix, d_new_ids, d_new_x, n_new, d_old_ids, n_old, d_q, nq, k, nprobe, d_dist, d_ids,
-                           d_status, d_ndeleted, s);
+  Index::StepGraph key;
+  const void* p[8] = {d_new_ids, d_new_x, d_old_ids, d_q, d_dist, d_ids, d_status, d_ndeleted};
+  for (int i = 0; i < 8; ++i) key.p[i] = p[i];
+  key.n[0] = n_new, key.n[1] = n_old, key.n[2] = nq;
+  key.k = nq > 0 ? k : 0, key.nprobe = nq > 0 ? nprobe : 0, key.kind = 0;
+  return graph_cached(ix, key, s, [&](cudaStream_t cs) {
+    return sliding_step_body(ix, d_new_ids, d_new_x, n_new, d_old_ids, n_old, d_q, nq, k, nprobe, d_dist, d_ids,
+                             d_status, d_ndeleted, cs);
+  });
 }
+
 
 sivf_rc sivf_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int32_t G, int64_t nq, int32_t k,
                         float* d_dist, int64_t* d_ids, sivf_stream_t stream) {

@@ -110,7 +110,7 @@ struct Index {
   struct StepGraph {
     const void* p[8] = {};
     int64_t n[3] = {};
-    int32_t k = 0, nprobe = 0;
+    int32_t k = 0, nprobe = 0, kind = 0;  // kind: 0 sliding step, 1 search
     cudaStream_t s = nullptr;
     uint64_t epoch = 0, used = 0;
     int64_t launches = 0;
