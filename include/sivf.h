@@ -222,7 +222,9 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
  *                      every query's nprobe/4 nearest lists are scanned before
  *                      its other lists (when that adds no work items on
  *                      average); the bounds on the k-th distances are then
- *                      tight early.  Changes speed only, never results.
+ *                      tight early.  A value r0 > 1 forces the split at the r0
+ *                      nearest lists; 0 = one bucket.  Changes speed only, never
+ *                      results.
  *   SIVF_OPT_STEP_GRAPH (default 1): sivf_sliding_window_step and sivf_search
  *                      capture the call as a CUDA graph the second time they see a call
  *                      signature (device pointers, sizes, k, nprobe, stream,
