@@ -748,7 +748,29 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
       ns += __popc(pm);
     }
     __syncwarp();
-    if (ns <= CCAP) {
+    if (ns <= 64 && m <= 32) {
+      // <= 64 values: the m-th smallest (m <= 32) by sorting, not bisection: two warp
+      // bitonic sorts, the 32 smallest of both by one bitonic merge
+      uint32_t a0 = lane < ns ? sv[lane] : 0xFFFFFFFFu;
+      uint32_t a1 = lane + 32 < ns ? sv[lane + 32] : 0xFFFFFFFFu;
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          const uint32_t o0 = __shfl_xor_sync(kFull, a0, stride), o1 = __shfl_xor_sync(kFull, a1, stride);
+          const bool up = (lane & size) == 0 || size == 32, lower = (lane & stride) == 0;
+          a0 = (lower == up) ? min(a0, o0) : max(a0, o0);
+          a1 = (lower == up) ? min(a1, o1) : max(a1, o1);
+        }
+      }
+      uint32_t b = min(a0, __shfl_sync(kFull, a1, 31 - lane));  // bitonic: the 32 smallest
+#pragma unroll
+      for (int j = 16; j > 0; j >>= 1) {
+        const uint32_t o = __shfl_xor_sync(kFull, b, j);
+        b = (lane & j) ? max(b, o) : min(b, o);
+      }
+      lo = hi = __shfl_sync(kFull, b, m - 1);
+    } else if (ns <= CCAP) {
       uint32_t u[CCAP / 32];
 #pragma unroll
       for (int t = 0; t < CCAP / 32; ++t) u[t] = lane + 32 * t < ns ? sv[lane + 32 * t] : 0xFFFFFFFFu;
