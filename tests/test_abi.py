@@ -80,3 +80,16 @@ def test_no_oracle_in_product_path():
     if os.path.exists(so):
         out = subprocess.run(["nm", "-D", so], capture_output=True, text=True).stdout
         assert "or_" not in " ".join(l.split()[-1] for l in out.splitlines() if l.split()[-1].startswith("or_"))
+
+
+def test_python_constants_match_the_header():
+    """OPT_* / CFG_* in the binding equal the SIVF_OPT_* / SIVF_CFG_* values of include/sivf.h."""
+    import re
+
+    import paper_2601_11808_b200 as S
+
+    hdr = open(os.path.join(ROOT, "include", "sivf.h")).read()
+    vals = {m.group(1): int(m.group(2)) for m in re.finditer(r"SIVF_(OPT_[A-Z_]+|CFG_[A-Z_]+)\s*=\s*(\d+)", hdr)}
+    assert vals, "no SIVF_OPT_/SIVF_CFG_ enumerators found"
+    for name, v in vals.items():
+        assert getattr(S, name) == v, f"{name}: binding {getattr(S, name, None)} header {v}"
