@@ -672,7 +672,7 @@ __host__ __device__ inline size_t select_smem_per_warp(int Dp) {
   return (size_t)Dp * 4 + 2 * CCAP * 4 + 2 * 32 * 8;
 }
 __host__ __device__ inline size_t select_smem(int Dp, int nlist) {
-  return SELW * select_smem_per_warp(Dp) + (size_t)2 * nlist * 4;
+  return SELW * select_smem_per_warp(Dp) + (size_t)(2 + SELW) * nlist * 4;  // + per-warp E row
 }
 template <int NPL, int MODE>
 __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __restrict__ mat,
@@ -710,11 +710,18 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
 #pragma unroll
   for (int i = 0; i < NPL; ++i) A[i] = lane + 32 * i < nlist ? __ldcs(arow + lane + 32 * i) : INFINITY;
   const float qn = xnorm[row], sq = sqrtf(qn), qnb = kb * qn;
-  // the certified half-width E of column lane + 32 i (recomputed where needed: keeping
-  // only A in registers doubles the resident warps of this latency-bound kernel)
+  // the certified half-width E of column lane + 32 i, computed once into the warp's
+  // shared row and read back by the later passes (only A stays in registers)
+  float* e_row = cnb_s + nlist + (size_t)w * nlist;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nlist) e_row[c] = fmaf(sq, csa_s[c], qnb + cnb_s[c]);
+  }
+  __syncwarp();
   auto Eat = [&](int i) {
     const int c = lane + 32 * i;
-    return c < nlist ? fmaf(sq, csa_s[c], qnb + cnb_s[c]) : 0.f;
+    return c < nlist ? e_row[c] : 0.f;
   };
   auto ubat = [&](int i) { return __float_as_uint(fmaxf(A[i] + Eat(i), 0.f)); };  // +inf beyond nlist
   const float* xr = X + row * (int64_t)D;
