@@ -671,8 +671,8 @@ constexpr int SELW = 8;  // rows (warps) per block
 __host__ __device__ inline size_t select_smem_per_warp(int Dp) {
   return (size_t)Dp * 4 + 2 * CCAP * 4 + 2 * 32 * 8;
 }
-__host__ __device__ inline size_t select_smem(int Dp, int nlist) {
-  return SELW * select_smem_per_warp(Dp) + (size_t)(2 + SELW) * nlist * 4;  // + per-warp E row
+__host__ __device__ inline size_t select_smem(int Dp, int nlist, int mode = 1) {
+  return SELW * select_smem_per_warp(Dp) + (size_t)(2 + (mode ? SELW : 0)) * nlist * 4;  // + per-warp E rows
 }
 template <int NPL, int MODE>
 __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __restrict__ mat,
@@ -712,16 +712,20 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
   const float qn = xnorm[row], sq = sqrtf(qn), qnb = kb * qn;
   // the certified half-width E of column lane + 32 i, computed once into the warp's
   // shared row and read back by the later passes (only A stays in registers)
+  // (MODE 0, the argmin of an insert, makes two passes: it recomputes E inline)
   float* e_row = cnb_s + nlist + (size_t)w * nlist;
+  if (MODE == 1) {
 #pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int c = lane + 32 * i;
-    if (c < nlist) e_row[c] = fmaf(sq, csa_s[c], qnb + cnb_s[c]);
+    for (int i = 0; i < NPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < nlist) e_row[c] = fmaf(sq, csa_s[c], qnb + cnb_s[c]);
+    }
+    __syncwarp();
   }
-  __syncwarp();
   auto Eat = [&](int i) {
     const int c = lane + 32 * i;
-    return c < nlist ? e_row[c] : 0.f;
+    if (MODE == 1) return c < nlist ? e_row[c] : 0.f;
+    return c < nlist ? fmaf(sq, csa_s[c], qnb + cnb_s[c]) : 0.f;
   };
   auto ubat = [&](int i) { return __float_as_uint(fmaxf(A[i] + Eat(i), 0.f)); };  // +inf beyond nlist
   const float* xr = X + row * (int64_t)D;
@@ -1015,7 +1019,7 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
   const int64_t R = alt ? sc.q_rows
                         : (sc.tc_rows < sc.coarse_rows / TM * TM ? sc.tc_rows : sc.coarse_rows / TM * TM);
   if (ix.coarse_select && ix.coarse_tmap_ok && st.nlist <= 1024 && R >= TM) {
-    const size_t ssm = select_smem(Dp, st.nlist);
+    const size_t ssm = select_smem(Dp, st.nlist), ssm0 = select_smem(Dp, st.nlist, 0);
     for (int64_t r0 = 0; r0 < n; r0 += R) {
       const int64_t nr = n - r0 < R ? n - r0 : R;
       const float* xr = d_x + r0 * D;
@@ -1032,7 +1036,7 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
       const dim3 g((unsigned)ceil_div(nr, SELW));
 #define SIVF_SEL(NPL)                                                                                          \
   if (probes == nullptr)                                                                                       \
-    k_coarse_select<NPL, 0><<<g, 32 * SELW, ssm, s>>>(mat, xr, nr, D, st.nlist, m, xn, sc.c_csa,  \
+    k_coarse_select<NPL, 0><<<g, 32 * SELW, ssm0, s>>>(mat, xr, nr, D, st.nlist, m, xn, sc.c_csa,  \
                                                        sc.c_cnb, bd.kb, st.centroids, Dp, best + r0, nullptr, 0,  \
                                                        need_dist, InvCount{nullptr, nullptr, 1, 0});              \
   else                                                                                                         \
