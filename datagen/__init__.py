@@ -146,6 +146,8 @@ class DeviceGenerator:
         self._L.sivfgen_cuda_model_free.argtypes = [ctypes.c_void_p]
         self._L.sivfgen_cuda_range.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
                                                ctypes.c_void_p, ctypes.c_void_p]
+        self._L.sivfgen_cuda_list.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                              ctypes.c_void_p]
         self.shape = shape
         self._p = shape._params()
         self._m = self._L.sivfgen_cuda_model_new(ctypes.byref(self._p))
@@ -168,6 +170,19 @@ class DeviceGenerator:
         rc = self._L.sivfgen_cuda_range(self._m, g0, gstride, out.shape[0], out.data_ptr(), st)
         if rc != 0:
             raise RuntimeError(f"sivfgen_cuda_range: CUDA error {rc}")
+        return out
+
+
+    def take_into(self, out, gs, stream=None):
+        """out: CUDA float32 [n][dim]; gs: CUDA int64 [n] indices; row i = vector(gs[i])."""
+        import torch
+
+        assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.shape[1] == self.shape.dim
+        assert gs.is_cuda and gs.dtype == torch.int64 and gs.is_contiguous() and gs.shape[0] == out.shape[0]
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        rc = self._L.sivfgen_cuda_list(self._m, gs.data_ptr(), gs.shape[0], out.data_ptr(), st)
+        if rc != 0:
+            raise RuntimeError(f"sivfgen_cuda_list: CUDA error {rc}")
         return out
 
 

@@ -48,6 +48,27 @@ __global__ void __launch_bounds__(kThreads) k_range(sivfgen_params p, const floa
   }
 }
 
+/* block per listed id (grid-stride) */
+__global__ void __launch_bounds__(kThreads) k_list(sivfgen_params p, const float* __restrict__ mu,
+                                                   const float* __restrict__ A, const uint64_t* __restrict__ gs,
+                                                   int64_t n, float* __restrict__ out) {
+  __shared__ float z[kMaxR];
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint64_t g = gs[i];
+    float* o = out + (size_t)i * p.dim;
+    if (p.kind == SIVFGEN_UNIFORM) {
+      for (int k = threadIdx.x; k < p.dim; k += blockDim.x) o[k] = sivfgen_uniform(p.seed, g, k);
+      continue;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < p.r; j += blockDim.x) z[j] = sivfgen_N01(p.seed, g, 1000u + (uint64_t)j);
+    __syncthreads();
+    const int m = sivfgen_component(&p, g);
+    for (int k = threadIdx.x; k < p.dim; k += blockDim.x)
+      o[k] = sivfgen_coord(&p, g, k, mu[(size_t)m * p.dim + k], A + ((size_t)m * p.dim + k) * p.r, z);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -99,6 +120,15 @@ int sivfgen_cuda_range(const sivfgen_cuda_model* md, uint64_t g0, uint64_t gstri
   if (n == 0) return 0;
   const int64_t grid = n < 148 * 64 ? n : 148 * 64;
   k_range<<<(unsigned)grid, kThreads, 0, (cudaStream_t)stream>>>(md->p, md->mu, md->A, g0, gstride, n, d_out);
+  return (int)cudaGetLastError();
+}
+
+/* out[i][:] = vector(d_gs[i]), i < n (device ids list); asynchronous on `stream`. */
+int sivfgen_cuda_list(const sivfgen_cuda_model* md, const uint64_t* d_gs, int64_t n, float* d_out, void* stream) {
+  if (!md || n < 0 || (n > 0 && (!d_out || !d_gs))) return (int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  const int64_t grid = n < 148 * 64 ? n : 148 * 64;
+  k_list<<<(unsigned)grid, kThreads, 0, (cudaStream_t)stream>>>(md->p, md->mu, md->A, d_gs, n, d_out);
   return (int)cudaGetLastError();
 }
 }

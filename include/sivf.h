@@ -92,10 +92,11 @@ typedef struct {
   int64_t slabs_free;           /* free-stack height P_top (Eq. 2) */
   int64_t pool_exhausted_items; /* sticky count of SIVF_ST_POOL_EXHAUSTED items */
   int64_t reclaimed_slabs;      /* total slabs recycled by sivf_reclaim / sliding steps */
-  int64_t device_errors;        /* sticky internal errors (directory arena overflow); must stay 0 */
+  int64_t device_errors;        /* sticky internal errors (unreachable directory-arena overflow); must stay 0 */
   double overhead_paper;        /* 128/(32*(4d+8)): the paper's per-slab header accounting (reading C17) */
   double overhead_actual;       /* this build: (16 B metadata/slab * slabs_in_use + 8 B * id slots) / (live payload+id bytes) */
   double overhead_scan_copy;    /* the fp16 scan copy (2 Dh B per slot of slabs_in_use) / (live payload+id bytes); 0 without */
+  int64_t dir_compactions;      /* times the list directories were repacked into the idle arena half (k_reserve) */
 } sivf_stats_t;
 
 /* Bytes of device memory the index needs for `cfg` (host-only, pure). */
@@ -140,7 +141,11 @@ sivf_rc sivf_delete(sivf_index ix, const int64_t* d_ids, int64_t n, int64_t* d_n
 /* Batched search (Alg. 3): the nprobe nearest lists by
  * (dist32, list) (reading C3), scan of valid slots only (Eq. slot_valid),
  * per-query top-k by (distance, id).  d_q[nq][dim]; d_dist[nq][k] fp32;
- * d_ids[nq][k] int64; d_probes[nq][nprobe] (nullable) receives the probe set. */
+ * d_ids[nq][k] int64; d_probes[nq][nprobe] (nullable) receives the probe SET of
+ * each query (reading C3): its members are exact, their order within a row is
+ * unspecified (nearest-first when the exact distances were needed to decide the
+ * set, otherwise by the tensor-core approximation).  A configuration no scan
+ * kernel supports (e.g. shared memory for dim) returns SIVF_E_UNSUPPORTED. */
 sivf_rc sivf_search(sivf_index ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
                     int64_t* d_ids, int32_t* d_probes, sivf_stream_t stream);
 

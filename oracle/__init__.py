@@ -58,6 +58,7 @@ def lib():
             "or_delete": (_i64, [_P, _P, _i64]),
             "or_search": (None, [_P, _P, _i64, _i32, _i32, _P, _P, _P]),
             "or_bruteforce": (None, [_P, _P, _i64, _i32, _P, _P]),
+            "or_topk_candidates": (None, [_P, _i32, _P, _P, _i64, _i32, _P, _P]),
             "or_reclaim": (_i64, [_P]),
             "or_dump_state": (None, [_P, _P, _P]),
             "or_stats": (None, [_P, ctypes.POINTER(Stats)]),
@@ -112,6 +113,17 @@ def probe(C, q, m: int) -> np.ndarray:
     return out
 
 
+def topk_candidates(q, X, ids, k: int):
+    """Top-k by (dist32, id) of query q over the candidates X[n][d] with ids[n]."""
+    q = _f32(q).reshape(-1)
+    X = _f32(X).reshape(-1, q.shape[0])
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    d = np.empty(k, np.float32)
+    i = np.empty(k, np.int64)
+    lib().or_topk_candidates(_p(q), q.shape[0], _p(X), _p(ids), ids.shape[0], k, _p(d), _p(i))
+    return d, i
+
+
 def merge_topk(dist_g, ids_g, k: int):
     dist_g = _f32(dist_g)
     ids_g = np.ascontiguousarray(ids_g, dtype=np.int64)
@@ -140,6 +152,7 @@ class Index:
     def __init__(self, dim: int, nlist: int, id_capacity: int, num_slabs: int = 0, shard_rank: int = 0,
                  shard_count: int = 1):
         self.dim, self.nlist = dim, nlist
+        self.shard_rank, self.shard_count = shard_rank, shard_count
         self._h = lib().or_create(dim, nlist, id_capacity, num_slabs, shard_rank, shard_count)
         if not self._h:
             raise ValueError("or_create: invalid arguments")

@@ -314,6 +314,18 @@ void or_search(or_index* ix, const float* Q, int64_t nq, int32_t k, int32_t npro
   });
 }
 
+// Alg. 3's result restricted to a given candidate set (readings C4, C5): the
+// top-k of (dist32(q, x_i), id_i) over the n candidates, ascending, padded (+inf, -1).
+// Used by the sampled checks of configurations too large for an oracle index (config H:
+// the candidates are the members of a query's probed lists).
+void or_topk_candidates(const float* q, int32_t d, const float* X, const int64_t* ids, int64_t n, int32_t k,
+                        float* dist, int64_t* out_ids) {
+  std::vector<Hit> cand;
+  cand.reserve((size_t)n);
+  for (int64_t i = 0; i < n; ++i) cand.push_back({dist32(q, X + (size_t)i * d, d), ids[i]});
+  topk_fill(cand, k, dist, out_ids);
+}
+
 void or_bruteforce(or_index* ix, const float* Q, int64_t nq, int32_t k, float* dist, int64_t* ids) {
   const int d = ix->d;
   parallel_for(nq, [&](int64_t qi) {

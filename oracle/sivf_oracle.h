@@ -56,6 +56,9 @@ void or_insert(or_index*, const int64_t* ids, const float* X, int64_t n, int32_t
 int64_t or_delete(or_index*, const int64_t* ids, int64_t n);
 void or_search(or_index*, const float* Q, int64_t nq, int32_t k, int32_t nprobe, float* dist, int64_t* ids,
                int32_t* probes /*nullable [nq][nprobe]*/);
+/* top-k by (dist32, id) of one query over n given candidates X[n][d] with ids[n] (search restricted to them) */
+void or_topk_candidates(const float* q, int32_t d, const float* X, const int64_t* ids, int64_t n, int32_t k,
+                        float* dist, int64_t* out_ids);
 void or_bruteforce(or_index*, const float* Q, int64_t nq, int32_t k, float* dist, int64_t* ids);
 int64_t or_reclaim(or_index*);
 void or_dump_state(or_index*, int32_t* list_of_id /*[local capacity]*/, int64_t* live_per_list /*[nlist]*/);

@@ -53,6 +53,7 @@ class Stats(ctypes.Structure):
         ("overhead_paper", ctypes.c_double),
         ("overhead_actual", ctypes.c_double),
         ("overhead_scan_copy", ctypes.c_double),
+        ("dir_compactions", _i64),
     ]
 
 

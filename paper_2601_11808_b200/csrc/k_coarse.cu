@@ -115,6 +115,15 @@ __global__ void k_select_probes(const float* __restrict__ dist, int64_t nq, int6
 
 }  // namespace
 
+// k_select_probes keeps 2 nprobe keys per warp (4 warps) in dynamic shared memory:
+// 64 nprobe B, beyond the 48 KB default for nprobe > 768.
+cudaError_t setup_coarse_exact(Index& ix) {
+  const size_t need = sizeof(unsigned long long) * 2 * (size_t)ix.cfg.max_nprobe * 4;
+  if (need <= 48 * 1024) return cudaSuccess;
+  if (need > ix.smem_optin) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(k_select_probes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+}
+
 cudaError_t launch_assign_exact(Index& ix, const float* d_x, int64_t n, cudaStream_t s, bool need_dist) {
   if (n <= 0) return cudaSuccess;
   PhaseTimer pt(ix, SIVF_PH_ASSIGN, s);

@@ -958,8 +958,13 @@ cudaError_t setup_coarse_tc(Index& ix) {
   }
   cudaError_t e = cudaFuncSetAttribute(k_coarse_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)coarse_smem_bytes(0));
-  {
-    const int sel = (int)select_smem(ix.st.Dp, 1024);  // nlist <= 1024 on this path
+  // the per-row selection path (nlist <= 1024): its shared memory grows with Dp and
+  // nlist; beyond the opt-in limit the path is switched off (the fused two-pass
+  // epilogue serves instead) rather than failing sivf_create
+  if (ix.st.nlist > 1024 || select_smem(ix.st.Dp, ix.st.nlist) > ix.smem_optin) {
+    ix.coarse_select = ix.coarse_select_ok = false;
+  } else if (e == cudaSuccess) {
+    const int sel = (int)select_smem(ix.st.Dp, ix.st.nlist);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_select<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_select<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_select<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel);

@@ -133,16 +133,50 @@ __global__ void k_chunk_prefix(int32_t* __restrict__ hist, int64_t nchunks, int 
   cnt[l] = run;
 }
 
+// Block-wide exclusive scan of one value per thread (1024 threads); returns the
+// exclusive prefix, *total receives the block sum.  All threads must call it.
+__device__ __forceinline__ long long block_excl_scan(long long v, long long* ws /*[32]*/, long long* total) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  long long x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const long long o = __shfl_up_sync(kFull, x, off);
+    if (lane >= off) x += o;
+  }
+  if (lane == 31) ws[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    long long y = ws[lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long o = __shfl_up_sync(kFull, y, off);
+      if (lane >= off) y += o;
+    }
+    ws[lane] = y;
+  }
+  __syncthreads();
+  const long long excl = (w > 0 ? ws[w - 1] : 0) + x - v;
+  *total = ws[31];
+  __syncthreads();
+  return excl;
+}
+
 // Single CTA: lists in ascending order share the free stack (reading C33 /
 // SURVEY a4 policy).  Slabs for list l: free_stack[newbase_l, newbase_l+granted_l).
+// Then the directory space: every list that outgrows its directory takes a new
+// one of max(2 cap, len + g, 8) entries from the active arena half
+// (k_dir_update).  If that would not fit, every directory is first compacted
+// into the idle half with cap = max(8, 2 (len + g)) (sum <= 2 num_slabs + 8 nlist
+// <= dir_half), so no list grows in this batch and the arena never overflows
+// however the lists' peaks drift over time.
 __global__ void __launch_bounds__(1024) k_reserve(DevState st, const int32_t* __restrict__ cnt,
                                                   int32_t* __restrict__ tail_free, int32_t* __restrict__ tail_slab,
                                                   int32_t* __restrict__ granted, int32_t* __restrict__ newbase,
-                                                  int32_t* __restrict__ short_flag) {
-  __shared__ int32_t wsum[32];
-  __shared__ int64_t carry_s;
+                                                  int64_t* __restrict__ newoff) {
+  __shared__ long long ws[32];
+  __shared__ long long carry_s;
   __shared__ int32_t F;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int t = threadIdx.x;
   if (t == 0) {
     carry_s = 0;
     F = st.ictr[I_FREE_TOP];
@@ -161,26 +195,8 @@ __global__ void __launch_bounds__(1024) k_reserve(DevState st, const int32_t* __
       int rest = c > tf ? c - tf : 0;
       need = (rest + kSlot - 1) / kSlot;
     }
-    // block exclusive scan of need
-    int v = need;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      int o = __shfl_up_sync(kFull, v, off);
-      if (lane >= off) v += o;
-    }
-    if (lane == 31) wsum[w] = v;
-    __syncthreads();
-    if (w == 0) {
-      int x = wsum[lane];
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        int o = __shfl_up_sync(kFull, x, off);
-        if (lane >= off) x += o;
-      }
-      wsum[lane] = x;
-    }
-    __syncthreads();
-    int64_t excl = carry_s + (w > 0 ? wsum[w - 1] : 0) + v - need;
+    long long tot;
+    const long long excl = carry_s + block_excl_scan(need, ws, &tot);
     if (l < st.nlist) {
       int64_t avail = (int64_t)F - excl;
       int g = (int)(avail <= 0 ? 0 : (avail < need ? avail : need));
@@ -188,20 +204,64 @@ __global__ void __launch_bounds__(1024) k_reserve(DevState st, const int32_t* __
       tail_slab[l] = ts;
       granted[l] = g;
       newbase[l] = (int32_t)(avail - g > 0 ? avail - g : 0);
-      short_flag[l] = (g < need) ? 1 : 0;
     }
-    __syncthreads();
-    if (t == 0) carry_s += wsum[31];
+    if (t == 0) carry_s += tot;
     __syncthreads();
   }
   if (t == 0) {
     int64_t total = carry_s;
     st.ictr[I_FREE_TOP] = (int32_t)(total >= F ? 0 : F - total);
   }
+  // directory space this batch will bump-allocate
+  long long grow = 0;
+  for (int l = t; l < st.nlist; l += 1024) {
+    const int g = granted[l], len = st.dir_len[l], cap = st.dir_cap[l];
+    if (g > 0 && len + g > cap) grow += max(max(2 * cap, len + g), 8);
+  }
+  long long total_grow;
+  block_excl_scan(grow, ws, &total_grow);
+  const int half = st.ictr[I_DIR_HALF];
+  const long long bump = st.ictr[I_DIR_BUMP];
+  if (bump + total_grow <= (long long)(half + 1) * st.dir_half) return;  // block-uniform
+  // compaction into the idle half
+  const long long base = (long long)(1 - half) * st.dir_half;
+  if (t == 0) carry_s = 0;
+  __syncthreads();
+  for (int l0 = 0; l0 < st.nlist; l0 += 1024) {
+    const int l = l0 + t;
+    long long ncap = 0;
+    if (l < st.nlist) {
+      const int need = st.dir_len[l] + granted[l];
+      ncap = need > 0 ? max(8, 2 * need) : 0;
+    }
+    long long tot;
+    const long long excl = carry_s + block_excl_scan(ncap, ws, &tot);
+    if (l < st.nlist) newoff[l] = base + excl;
+    if (t == 0) carry_s += tot;
+    __syncthreads();
+  }
+  const int lane = t & 31, w = t >> 5;
+  for (int l = w; l < st.nlist; l += 32) {  // warp per list: copy the live entries
+    const int len = st.dir_len[l];
+    const int32_t* src = st.dir_arena + st.dir_off[l];
+    int32_t* dst = st.dir_arena + newoff[l];
+    for (int j = lane; j < len; j += 32) dst[j] = src[j];
+  }
+  __syncthreads();
+  for (int l = t; l < st.nlist; l += 1024) {
+    const int need = st.dir_len[l] + granted[l];
+    st.dir_off[l] = newoff[l];
+    st.dir_cap[l] = need > 0 ? max(8, 2 * need) : 0;
+  }
+  if (t == 0) {
+    st.ictr[I_DIR_BUMP] = (int32_t)(base + carry_s);
+    st.ictr[I_DIR_HALF] = 1 - half;
+    atomicAdd(&st.ctr[C_DIRCOMPACT], 1ull);
+  }
 }
 
 __global__ void k_dir_update(DevState st, const int32_t* __restrict__ cnt, const int32_t* __restrict__ tail_free,
-                             const int32_t* __restrict__ tail_slab, const int32_t* __restrict__ granted,
+                             const int32_t* __restrict__ tail_slab, int32_t* __restrict__ granted,
                              const int32_t* __restrict__ newbase) {
   const int lane = threadIdx.x & 31;
   const int l = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -220,8 +280,15 @@ __global__ void k_dir_update(DevState st, const int32_t* __restrict__ cnt, const
     int64_t noff = 0;
     if (lane == 0) noff = atomicAdd(&st.ictr[I_DIR_BUMP], ncap);
     noff = __shfl_sync(kFull, noff, 0);
-    if (noff + ncap > st.dir_arena_cap) {
-      if (lane == 0) atomicAdd(&st.ctr[C_DEVERR], 1ull);
+    if (noff + ncap > (int64_t)(st.ictr[I_DIR_HALF] + 1) * st.dir_half) {
+      // unreachable: k_reserve compacts first whenever this batch's growth would
+      // not fit.  Fail safe all the same: the list's new slabs are not linked and
+      // its items beyond the tail slab become POOL_EXHAUSTED (k_append reads
+      // granted); the stranded slabs show up as sivf_dump_state violations.
+      if (lane == 0) {
+        atomicAdd(&st.ctr[C_DEVERR], 1ull);
+        granted[l] = 0;
+      }
       return;
     }
     for (int j = lane; j < len; j += 32) st.dir_arena[noff + j] = st.dir_arena[off + j];
@@ -380,7 +447,7 @@ cudaError_t launch_insert(Index& ix, const int64_t* d_ids, const float* d_x, int
   e = launch_stable_ranks(ix, n, 1, s);
   if (e != cudaSuccess) return e;
   k_reserve<<<1, 1024, 0, s>>>(st, sc.list_cnt, sc.list_tail_free, sc.list_tail_slab, sc.list_granted,
-                               sc.list_newbase, sc.list_short);
+                               sc.list_newbase, sc.list_newoff);
   k_dir_update<<<ceil_div((int64_t)st.nlist * 32, 256), 256, 0, s>>>(st, sc.list_cnt, sc.list_tail_free,
                                                                      sc.list_tail_slab, sc.list_granted,
                                                                      sc.list_newbase);

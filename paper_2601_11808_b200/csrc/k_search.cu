@@ -556,6 +556,11 @@ cudaError_t launch_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int
                               float* d_dist, int64_t* d_ids, cudaStream_t s, int64_t* launches) {
   if (nq <= 0) return cudaSuccess;
   const int wpb = 4;
+  const size_t smem = sizeof(unsigned long long) * 2 * k * wpb;  // 64 k B: beyond 48 KB for k > 768
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_merge_shards, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   k_merge_shards<<<ceil_div(nq, wpb), 32 * wpb, sizeof(unsigned long long) * 2 * k * wpb, s>>>(d_dist_g, d_ids_g, G,
                                                                                               nq, k, d_dist, d_ids);
   if (launches) *launches += 1;

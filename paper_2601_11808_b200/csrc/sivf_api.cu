@@ -18,14 +18,14 @@ struct Layout {
   size_t payload, payload16, slab_ids, slab_norm, slab_flag, bitmap, cursor, slab_list, free_stack, slab_mark, att, claim,
       dir_off, dir_len, dir_cap, dir_arena, centroids, ctr, ictr, tmp64, gthr;
   size_t row_list, row_rank, row_status, row_lid, row_best, chunk_hist, list_cnt, list_tail_free, list_tail_slab,
-      list_granted, list_newbase, list_short;
+      list_granted, list_newbase, list_newoff;
   size_t coarse, probes, inv_cnt, inv_off, inv_cursor, inv_pairs, tile_off, work_l, work_p0, work_n, partial;
   size_t train_perm, train_members, train_off;
   size_t qx_tiles, qx_norm, qcoarse;
   int64_t q_rows;
   size_t x_tiles, x_norm, c_tiles, c_norm, c_csa, c_cnb, cand, cand_ubv, cand_cnt;
   int64_t tc_rows, cap_assign, cap_probe;
-  int64_t Dp, Dh, cap_local, dir_arena_cap, max_rows, max_chunks, coarse_rows, max_work;
+  int64_t Dp, Dh, cap_local, dir_half, max_rows, max_chunks, coarse_rows, max_work;
 };
 
 size_t take(Layout& L, size_t bytes) {
@@ -57,7 +57,9 @@ Layout make_layout(const sivf_config* c) {
   L.Dh = (D <= 128 && !(c->flags & SIVF_CFG_NO_SCAN_COPY)) ? (D + 15) / 16 * 16 : 0;
   const int64_t cap = c->id_capacity, G = c->shard_count, r = c->shard_rank;
   L.cap_local = cap > r ? (cap - r + G - 1) / G : 0;
-  L.dir_arena_cap = 4 * S + 16 * nl + 1024;
+  // directory arena: two halves; a compaction into the idle half needs at most
+  // sum over lists of max(8, 2 len) <= 2 S + 8 nl entries (k_reserve)
+  L.dir_half = 2 * S + 8 * nl + 64;
   L.max_rows = c->max_batch > c->max_train ? c->max_batch : c->max_train;
   if (L.max_rows < 1) L.max_rows = 1;
   L.max_chunks = (L.max_rows + 1023) / 1024;
@@ -88,7 +90,7 @@ Layout make_layout(const sivf_config* c) {
   L.dir_off = take(L, (size_t)nl * 8);
   L.dir_len = take(L, (size_t)nl * 4);
   L.dir_cap = take(L, (size_t)nl * 4);
-  L.dir_arena = take(L, (size_t)L.dir_arena_cap * 4);
+  L.dir_arena = take(L, (size_t)2 * L.dir_half * 4);
   L.centroids = take(L, (size_t)nl * L.Dp * 4);
   L.ctr = take(L, C_NCTR * 8);
   L.ictr = take(L, I_NICTR * 4);
@@ -105,7 +107,7 @@ Layout make_layout(const sivf_config* c) {
   L.list_tail_slab = take(L, (size_t)nl * 4);
   L.list_granted = take(L, (size_t)nl * 4);
   L.list_newbase = take(L, (size_t)nl * 4);
-  L.list_short = take(L, (size_t)nl * 4);
+  L.list_newoff = take(L, (size_t)nl * 8);
   L.coarse = take(L, (size_t)L.coarse_rows * nl * 4);
   L.probes = take(L, (size_t)npairs * 4 + 4);
   L.inv_cnt = take(L, (size_t)2 * nl * 4);
@@ -237,7 +239,7 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   st.dir_len = at<int32_t>(d_arena, L.dir_len);
   st.dir_cap = at<int32_t>(d_arena, L.dir_cap);
   st.dir_arena = at<int32_t>(d_arena, L.dir_arena);
-  st.dir_arena_cap = L.dir_arena_cap;
+  st.dir_half = L.dir_half;
   st.centroids = at<float>(d_arena, L.centroids);
   st.ctr = at<unsigned long long>(d_arena, L.ctr);
   st.ictr = at<int32_t>(d_arena, L.ictr);
@@ -255,7 +257,7 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   sc.list_tail_slab = at<int32_t>(d_arena, L.list_tail_slab);
   sc.list_granted = at<int32_t>(d_arena, L.list_granted);
   sc.list_newbase = at<int32_t>(d_arena, L.list_newbase);
-  sc.list_short = at<int32_t>(d_arena, L.list_short);
+  sc.list_newoff = at<int64_t>(d_arena, L.list_newoff);
   sc.coarse = at<float>(d_arena, L.coarse);
   sc.q_rows = L.q_rows;
   sc.qx_tiles = at<float>(d_arena, L.qx_tiles);
@@ -306,12 +308,8 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   cudaEventCreateWithFlags(&ix->ev_join, cudaEventDisableTiming);
   cudaError_t e = setup_search_kernels(*ix);
   if (e == cudaSuccess) e = setup_coarse_tc(*ix);
-  if (e == cudaSuccess) {
-    int wpb = 4;
-    size_t sel = sizeof(unsigned long long) * 2 * cfg->max_nprobe * wpb;
-    (void)sel;
-    e = cudaGetLastError();
-  }
+  if (e == cudaSuccess) e = setup_coarse_exact(*ix);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     delete ix;
     return SIVF_E_CUDA;
@@ -422,6 +420,10 @@ static sivf_rc graph_cached(Index* ix, Index::StepGraph key, cudaStream_t s, Bod
         oldest->used = ++ix->step_tick;
         return body(s);
       }
+      if (seen->bad) {  // not capturable (remembered per signature)
+        seen->used = ++ix->step_tick;
+        return body(s);
+      }
       seen->used = 0;  // promoted to a captured graph below
       // capture on cap_stream (the caller's stream may be the legacy default stream)
       cudaGraph_t graph = nullptr;
@@ -438,7 +440,10 @@ static sivf_rc graph_cached(Index* ix, Index::StepGraph key, cudaStream_t s, Bod
       if (e != cudaSuccess) {
         cudaGetLastError();
         ix->launches = l0;
-        ix->step_graph = false;  // not capturable here: direct launches from now on
+        // this signature is not capturable: direct launches for it from now on
+        // (other signatures keep their graphs)
+        seen->bad = true;
+        seen->used = ++ix->step_tick;
         return body(s);
       }
       if (victim->exec) cudaGraphExecDestroy(victim->exec);
@@ -466,6 +471,7 @@ sivf_rc sivf_search(sivf_index h, const float* d_q, int64_t nq, int32_t k, int32
   if (nprobe < 1 || nprobe > ix->cfg.max_nprobe || nprobe > ix->st.nlist) return SIVF_E_INVALID_ARG;
   if (nq > 0 && (!d_q || !d_dist || !d_ids)) return SIVF_E_INVALID_ARG;
   if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  if (nq > 0 && !plan_search(*ix, nq, k, nprobe).ok) return SIVF_E_UNSUPPORTED;  // before any capture
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   Index::StepGraph key;
   const void* p[8] = {d_q, d_dist, d_ids, d_probes, nullptr, nullptr, nullptr, nullptr};
@@ -539,6 +545,7 @@ sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const f
     if (!d_q || !d_dist || !d_ids) return SIVF_E_INVALID_ARG;
   }
   if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  if (nq > 0 && !plan_search(*ix, nq, k, nprobe).ok) return SIVF_E_UNSUPPORTED;  // before any capture
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   Index::StepGraph key;
   const void* p[8] = {d_new_ids, d_new_x, d_old_ids, d_q, d_dist, d_ids, d_status, d_ndeleted};
@@ -592,6 +599,7 @@ sivf_rc sivf_stats(sivf_index h, sivf_stats_t* out, sivf_stream_t stream) {
   out->pool_exhausted_items = (int64_t)c[C_EXHAUSTED];
   out->reclaimed_slabs = (int64_t)c[C_RECLAIMED];
   out->device_errors = (int64_t)c[C_DEVERR];
+  out->dir_compactions = (int64_t)c[C_DIRCOMPACT];
   out->slabs_free = ic[I_FREE_TOP];
   out->slabs_in_use = ix->st.num_slabs - ic[I_FREE_TOP];
   const double d = ix->st.D;
@@ -617,7 +625,7 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
     case SIVF_OPT_TC_SCAN: ix->use_tc_scan = value != 0; return SIVF_OK;
     case SIVF_OPT_TC_TWO_PHASE: ix->tc_two_phase = value < 0 ? 0 : (int)value; return SIVF_OK;
     case SIVF_OPT_TC_COARSE: ix->use_tc_coarse = value != 0; return SIVF_OK;
-    case SIVF_OPT_COARSE_SELECT: ix->coarse_select = value != 0; return SIVF_OK;
+    case SIVF_OPT_COARSE_SELECT: ix->coarse_select = value != 0 && ix->coarse_select_ok; return SIVF_OK;
     case SIVF_OPT_RANK_SPLIT: ix->rank_split = value < 0 ? 0 : (int)value; return SIVF_OK;
     case 99: ix->dbg = (int)value; return SIVF_OK;  // SIVF_OPT_DEBUG: experiments only
     case SIVF_OPT_SEED_SLABS:

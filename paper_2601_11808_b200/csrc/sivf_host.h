@@ -28,7 +28,7 @@ struct Scratch {
   int32_t* list_tail_slab = nullptr;// [nlist]
   int32_t* list_granted = nullptr;  // [nlist]
   int32_t* list_newbase = nullptr;  // [nlist] index into free_stack of the list's first new slab
-  int32_t* list_short = nullptr;    // [nlist] 1 if the list was not fully served
+  int64_t* list_newoff = nullptr;   // [nlist] directory offsets after a compaction (k_reserve)
   // search (max_queries x max_nprobe)
   float* coarse = nullptr;          // [coarse_rows][nlist] distance matrix (exact SIMT path) or the
                                     // tensor-core approximation A (k_coarse_select path)
@@ -93,6 +93,7 @@ struct Index {
   int fuse_nb = 1, fuse_r0 = 0;
   bool fuse_inv_done = false;
   bool coarse_select = true;  // A-matrix + per-row selection coarse path (SIVF_OPT_COARSE_SELECT)
+  bool coarse_select_ok = true;  // the selection kernels' shared memory fits (setup_coarse_tc)
   int rank_split = 1;         // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT; > 1: r0)
   int dbg = 0;                // experiment switches (SIVF_OPT_DEBUG)
   int seed_slabs = 0;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS; off: it costs more than it saves)
@@ -114,6 +115,7 @@ struct Index {
     cudaStream_t s = nullptr;
     uint64_t epoch = 0, used = 0;
     int64_t launches = 0;
+    bool bad = false;  // step_seen: this signature failed to capture; always launched directly
     cudaGraphExec_t exec = nullptr;
   };
   static constexpr int kStepGraphs = 4;
@@ -186,6 +188,7 @@ cudaError_t launch_dump(Index& ix, int32_t* d_list_of_id, int64_t* d_live_per_li
 // -> sc.row_best (list in the low word; the dist32 in the high word only when need_dist)
 cudaError_t launch_assign_exact(Index& ix, const float* d_x, int64_t n, cudaStream_t s, bool need_dist = true);
 cudaError_t launch_probe_exact(Index& ix, const float* d_q, int64_t nq, int32_t nprobe, cudaStream_t s); // -> sc.probes
+cudaError_t setup_coarse_exact(Index& ix);
 // k_coarse_tc.cu
 bool coarse_tc_supported(const Index& ix, int m);
 cudaError_t setup_coarse_tc(Index& ix);

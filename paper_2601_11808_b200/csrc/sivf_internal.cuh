@@ -34,9 +34,10 @@ constexpr unsigned kFull = 0xffffffffu;
 using u64 = unsigned long long;
 
 // Counters (u64, arena) — index into DevState::ctr
-enum { C_LIVE = 0, C_INSERTED, C_DELETED, C_EXHAUSTED, C_RECLAIMED, C_DEVERR, C_NDEL_TMP, C_NCTR = 8 };
+enum { C_LIVE = 0, C_INSERTED, C_DELETED, C_EXHAUSTED, C_RECLAIMED, C_DEVERR, C_NDEL_TMP, C_DIRCOMPACT, C_NCTR = 8 };
 // Counters (i32, arena) — index into DevState::ictr
-enum { I_FREE_TOP = 0, I_DIR_BUMP, I_WORK, I_NTILES, I_NTILES0, I_WORK2, I_NICTR = 8 };  // *0/*2: phased scan
+// I_DIR_BUMP: next free entry of the active directory half; I_DIR_HALF: which half (0/1) is active
+enum { I_FREE_TOP = 0, I_DIR_BUMP, I_WORK, I_NTILES, I_NTILES0, I_WORK2, I_DIR_HALF, I_NICTR = 8 };  // *0/*2: phased scan
 
 // POD view of the arena, passed by value to kernels (the paper's
 // SlabManagerDevice).
@@ -57,8 +58,8 @@ struct DevState {
   int64_t* dir_off;      // [nlist] offset of list l's slab directory in dir_arena
   int32_t* dir_len;      // [nlist] slabs in list l (oldest first; last = tail)
   int32_t* dir_cap;      // [nlist]
-  int32_t* dir_arena;    // [dir_arena_cap]
-  int64_t dir_arena_cap;
+  int32_t* dir_arena;    // [2 dir_half]: two halves; directories live in the active one (ictr[I_DIR_HALF])
+  int64_t dir_half;      // entries per half (>= 2 num_slabs + 8 nlist: a compaction always fits)
   float* centroids;      // [nlist][Dp] (zero padded)
   unsigned long long* ctr;
   int32_t* ictr;

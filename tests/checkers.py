@@ -27,11 +27,15 @@ def check_state(ix, ref: "O.Index", what: str = ""):
     assert gs["device_errors"] == 0
 
 
-def check_search(g, o, exact: bool, X_of=None, rel: float = 1e-4, what: str = ""):
-    """g, o = (dist [nq,k], ids [nq,k], probes [nq,nprobe]) numpy.
-    exact=True (integer-valued data): ids and distances identical.
-    Otherwise: probe sets equal, distances within rel, id sets equal up to
-    near-ties at the k-th boundary."""
+def check_search(g, o, exact: bool, ref=None, Q=None, rel: float = 1e-4, what: str = ""):
+    """g, o = (dist [nq,k], ids [nq,k], probes [nq,nprobe]) numpy (GPU, oracle).
+    SURVEY §8(c) "Search, per query":
+      - probe sets equal;
+      - exact=True (integer-valued data): ids and distances identical;
+      - otherwise: sorted distance lists agree within rel; every GPU id is live,
+        lies in a probed list and is unique, and its reported distance is within
+        rel of dist64(q, x_id) (needs ref = the oracle Index holding the same
+        state, and Q); every id in R xor O is a near-tie of the k-th distance."""
     gd, gi, gp = g
     od, oi, op = o
     nq, k = od.shape
@@ -41,6 +45,7 @@ def check_search(g, o, exact: bool, X_of=None, rel: float = 1e-4, what: str = ""
         assert np.array_equal(gi, oi), f"{what}: ids differ: first rows {np.nonzero((gi != oi).any(1))[0][:5]}"
         assert np.array_equal(gd, od), f"{what}: distances differ"
         return 0
+    loi = ref.dump_state()[0] if ref is not None else None
     exemptions = 0
     for q in range(nq):
         live_o = oi[q] >= 0
@@ -49,6 +54,17 @@ def check_search(g, o, exact: bool, X_of=None, rel: float = 1e-4, what: str = ""
         assert np.all(np.abs(gd[q][m] - od[q][m]) <= rel * np.maximum(od[q][m], 1e-30)), \
             f"{what}: distances out of tolerance for query {q}: {gd[q][m]} vs {od[q][m]}"
         assert len(set(gi[q][m].tolist())) == m.sum(), f"{what}: duplicate ids for query {q}"
+        if ref is not None:
+            probed = set(op[q].tolist())
+            for j in np.nonzero(m)[0]:
+                i = int(gi[q][j])
+                lid = i // ref.shard_count
+                assert i % ref.shard_count == ref.shard_rank and 0 <= lid < len(loi) and loi[lid] >= 0, \
+                    f"{what}: query {q} returned id {i}, which is not live"
+                assert int(loi[lid]) in probed, f"{what}: query {q} id {i} is in list {loi[lid]}, not probed"
+                d64 = O.dist64(Q[q], ref.get_vector(i))
+                assert abs(float(gd[q][j]) - d64) <= rel * max(d64, 1e-30), \
+                    f"{what}: query {q} id {i}: reported {gd[q][j]} vs dist64 {d64}"
         diff = set(gi[q][m].tolist()) ^ set(oi[q][m].tolist())
         if diff:
             kth = od[q][m][-1]

@@ -58,3 +58,7 @@ def test_device_generator_bit_identical():
         dev.range_into(out, 12345, 3)  # ids 12345 + 3 i (rank-local ids of an id-sharded index)
         ref = host.take(12345 + 3 * np.arange(300))
         assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+        gs = np.random.default_rng(1).integers(0, 10**8, 257).astype(np.int64)
+        out2 = torch.empty(257, shape.dim, dtype=torch.float32, device="cuda")
+        dev.take_into(out2, torch.from_numpy(gs).cuda())  # arbitrary id lists (sampled H checks)
+        assert np.array_equal(out2.cpu().numpy().view(np.uint32), host.take(gs).view(np.uint32))

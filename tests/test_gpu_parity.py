@@ -58,7 +58,8 @@ def dele(g, o, ids):
 def srch(g, o, Q, k, nprobe, exact=True):
     gd, gi, gp = g.search(T(Q), k, nprobe, return_probes=True)
     od, oi, op = o.search(Q, k, nprobe)
-    return check_search((gd.cpu().numpy(), gi.cpu().numpy(), gp.cpu().numpy()), (od, oi, op), exact=exact)
+    return check_search((gd.cpu().numpy(), gi.cpu().numpy(), gp.cpu().numpy()), (od, oi, op), exact=exact,
+                        ref=o, Q=np.asarray(Q, np.float32))
 
 
 # ------------------------------------------------------------------ SPEC examples

@@ -383,3 +383,80 @@ def test_kmeans_init_hash_pinned():
         return z ^ (z >> 31)
     assert mix(0) == m0
     assert O.kmeans_hash(0, 0) == mix(mix(0))
+
+
+def _mix64(z):
+    z = (z + 0x9E3779B97F4A7C15) & (2**64 - 1)
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
+    return z ^ (z >> 31)
+
+
+def _init_perm(n, nlist, seed):
+    # reading C31 / SURVEY §8(c) step 9: partial Fisher-Yates, j = i + H(seed, i) mod (n - i),
+    # H(s, i) = mix64(s ^ mix64(i)) (mix64 pinned by test_kmeans_init_hash_pinned)
+    perm = list(range(n))
+    for i in range(nlist):
+        j = i + _mix64(seed ^ _mix64(i)) % (n - i)
+        perm[i], perm[j] = perm[j], perm[i]
+    return perm
+
+
+def _empty_cluster_case(nlist, seed):
+    """Hand-built 1-D data (2nd coordinate 0) with known initial centroids:
+    X[perm[0]] = 0, X[perm[1..nlist)] = 100 (duplicates: clusters 2.. start empty),
+    the other four points, in ascending index order, = 1, 90, 96, 104."""
+    n = nlist + 4
+    perm = _init_perm(n, nlist, seed)
+    X = np.zeros((n, 2), np.float32)
+    X[perm[0], 0] = 0.0
+    for l in range(1, nlist):
+        X[perm[l], 0] = 100.0
+    rest = sorted(perm[nlist:])
+    for i, v in zip(rest, (1.0, 90.0, 96.0, 104.0)):
+        X[i, 0] = v
+    return X
+
+
+@pytest.mark.parametrize("seed", [3, 17, 0x51F7])
+def test_kmeans_empty_cluster_rule_hand_derived(seed):
+    # S:184 / reading C31: an empty cluster e (ascending) takes, from the LARGEST cluster
+    # (ties: lowest list), its point FARTHEST from that cluster's centroid (ties: lowest
+    # point index).  One iteration by hand, nlist = 3: c = (0, 100, 100); assignment
+    # (ties to the lower list): cluster 0 = {0, 1}, cluster 1 = {100, 100, 90, 96, 104},
+    # cluster 2 empty; the farthest member of cluster 1 from 100 is 90 (distance 100)
+    # -> c = (0.5, (100+100+96+104)/4, 90) = (0.5, 100, 90).  Wrong readings give:
+    # nearest point -> (0.5, 97.5, 100); smallest/first cluster -> (0, 100, 1).
+    X = _empty_cluster_case(3, seed)
+    C = O.kmeans(X, 3, 1, seed)
+    assert C[:, 0].tolist() == [0.5, 100.0, 90.0] and (C[:, 1] == 0).all()
+    # nlist = 4: c = (0, 100, 100, 100), clusters 2 and 3 empty, cluster 1 = {100 x3, 90,
+    # 96, 104}.  e = 2: L = 1 (6 members) gives 90; e = 3: L = 1 again (5 vs 2), farthest
+    # of {100 x3, 96, 104} from 100 is a tie 96 / 104 (distance 16) -> the lower point
+    # index, which holds 96 (values placed in ascending index order)
+    # -> c = (0.5, (100+100+100+104)/4, 90, 96) = (0.5, 101, 90, 96)
+    # (the highest index instead would give (0.5, 99, 90, 104)).
+    X4 = _empty_cluster_case(4, seed)
+    C4 = O.kmeans(X4, 4, 1, seed)
+    assert C4[:, 0].tolist() == [0.5, 101.0, 90.0, 96.0]
+
+
+def test_topk_candidates_equals_search_on_probed_members():
+    # the restricted scan used by the sampled H check: over exactly the live members of
+    # the probed lists it must reproduce or_search (and pad with (+inf, -1))
+    g = Generator(sift_shape(seed=0x100A, dim=16))
+    X = g.range(0, 2000)
+    C = O.kmeans(X, 32, 3, 5)
+    o = O.Index(16, 32, 2000)
+    o.set_centroids(C)
+    o.insert(np.arange(2000), X)
+    o.delete(np.arange(0, 2000, 3))
+    loi, _ = o.dump_state()
+    Q = g.queries(0, 10)
+    d, i, p = o.search(Q, 10, 4)
+    for q in range(10):
+        mem = np.nonzero(np.isin(loi, p[q]))[0]
+        dd, ii = O.topk_candidates(Q[q], X[mem], mem, 10)
+        assert np.array_equal(dd, d[q]) and np.array_equal(ii, i[q])
+    dd, ii = O.topk_candidates(Q[0], X[:3], np.array([5, 6, 7]), 5)
+    assert ii[3:].tolist() == [-1, -1] and np.isinf(dd[3:]).all()
