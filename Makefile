@@ -34,11 +34,29 @@ datagen/libsivfgen_cuda.so: datagen/datagen_cuda.cu datagen/sivf_datagen.h
 oracle/libsivf_oracle.so: oracle/sivf_oracle.cpp oracle/sivf_oracle.h
 	$(CXX) $(HOSTFP) -std=c++17 -shared -o $@ oracle/sivf_oracle.cpp
 
-$(PKG)/lib/libsivf.so: $(SIVF_SRCS) $(SIVF_HDRS)
-	@mkdir -p $(PKG)/lib build
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SIVF_SRCS) 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
+# one object per translation unit (make -j compiles them in parallel), then one link
+SIVF_OBJS := $(patsubst $(CSRC)/%.cu,build/obj/%.o,$(SIVF_SRCS))
+build/obj/%.o: $(CSRC)/%.cu $(SIVF_HDRS)
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/ptxas_$*.log || (cat build/ptxas_$*.log; exit 1)
+
+$(PKG)/lib/libsivf.so: $(SIVF_OBJS)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(ARCH) -shared -o $@ $(SIVF_OBJS)
+	@cat build/ptxas_*.log > build/ptxas.log 2>/dev/null || true
 
 clean:
 	rm -f datagen/libsivfgen.so datagen/libsivfgen_cuda.so oracle/libsivf_oracle.so $(PKG)/lib/libsivf.so
 
 .PHONY: all datagen datagen_cuda oracle sivf clean
+
+# profiling variants (experiments only; loaded with SIVF_LIB_PATH=...): per-role clock
+# traces of k_scan_tc block 0 (+ slow-path counters in _prof, none in _proft)
+build/libsivf_prof.so: $(SIVF_SRCS) $(SIVF_HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -DSIVF_TC_PROF -shared -o $@ $(SIVF_SRCS) 2> build/ptxas_prof.log || (cat build/ptxas_prof.log; exit 1)
+build/libsivf_proft.so: $(SIVF_SRCS) $(SIVF_HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -DSIVF_TC_PROF -DSIVF_TC_NOCOUNT -shared -o $@ $(SIVF_SRCS) 2> build/ptxas_proft.log || (cat build/ptxas_proft.log; exit 1)
+prof: build/libsivf_prof.so build/libsivf_proft.so
+.PHONY: prof

@@ -110,7 +110,7 @@ def test_search_graph_cache_replay():
     # replay it: each replay must read the current queries and index state
     gen = Generator(sift_shape(seed=0x51F7))
     C = O.kmeans(gen.train(4000), 64, 8, 9)
-    g, o = make_pair(128, 64, 40000, C, max_batch=4000, max_queries=256)
+    g, o = make_pair(128, 64, 40000, C, max_batch=20000, max_queries=256)
     ins(g, o, np.arange(20000), gen.range(0, 20000))
     q_d = torch.empty(256, 128, device="cuda")
     out = (torch.empty(256, 10, device="cuda"), torch.empty(256, 10, dtype=torch.int64, device="cuda"))
