@@ -60,3 +60,7 @@ build/libsivf_proft.so: $(SIVF_SRCS) $(SIVF_HDRS)
 	$(NVCC) $(NVFLAGS) -DSIVF_TC_PROF -DSIVF_TC_NOCOUNT -shared -o $@ $(SIVF_SRCS) 2> build/ptxas_proft.log || (cat build/ptxas_proft.log; exit 1)
 prof: build/libsivf_prof.so build/libsivf_proft.so
 .PHONY: prof
+# watchdog build (experiments only): a scan wait that spins too long reports its barrier and traps
+build/libsivf_wd.so: $(SIVF_SRCS) $(SIVF_HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -DSIVF_TC_WATCHDOG -shared -o $@ $(SIVF_SRCS) 2> build/ptxas_wd.log || (cat build/ptxas_wd.log; exit 1)

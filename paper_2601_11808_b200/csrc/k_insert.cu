@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256) k_append(DevState st, const int64_t* __re
         const int nc4 = st.Dp >> 2;
         float nrm = 0.f;
         bool integral = true, over = false;
-        uint16_t* dst16 = st.payload16 ? st.payload16 + (size_t)slab * kSlot * st.Dh : nullptr;
+        uint16_t* dst16 = st.payload16 ? st.payload16 + (size_t)slab * (rec16_bytes(st.Dh) >> 1) : nullptr;
         for (int c4 = lane; c4 < nc4; c4 += 32) {
           float4 v;
           if ((st.D & 3) == 0 && 4 * c4 + 3 < st.D) {
@@ -391,6 +391,11 @@ __global__ void __launch_bounds__(256) k_append(DevState st, const int64_t* __re
           if (!integral) atomicAnd(&st.slab_flag[slab], ~kFlagIntegral);
           if (over) atomicOr(&st.slab_flag[slab], kFlagF16Over);
           st.slab_ids[(size_t)slab * kSlot + o] = (uint32_t)ids[i];
+          if (dst16) {  // the scan record's copies of the norm and the id
+            *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(dst16) + rec16_norm_off(st.Dh, o)) = nrm;
+            *reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst16) + rec16_id_off(st.Dh, o)) =
+                (uint32_t)ids[i];
+          }
           st.att[u] = ((uint64_t)(uint32_t)slab << 32) | (uint32_t)o;  // Eq. att_encoding
           st.claim[u] = kClaimEmpty;
         }

@@ -12,38 +12,42 @@
 //
 // Why groups of 4 slabs: one MMA re-reads the whole A tile, so an N=32 (one
 // slab) instruction costs as much as N=128 (tools/mma_probe.cu).  The B
-// operand must be K-major SWIZZLE_NONE with a uniform 8-row-group stride.  The
-// fp16 copy is stored as exactly that (pay16_off(): [4 row groups][Dh/8][8
-// slots][8 halves], LBO = 128 B, SBO = 16 Dh B), so each slab of a group is
-// ONE contiguous cp.async.bulk of 8 KB into consecutive stage slots and the
-// four together are the N = 128 operand.  No gather, no shared-memory
-// transpose (bulk copies stream 2x faster than TMA tile::gather4 from L2,
-// tools/g4_probe.cu).
+// operand must be K-major SWIZZLE_NONE with a uniform 8-row-group stride.  A
+// slab's scan record (rec16_bytes(), written by k_append) is exactly that:
+// 4 row groups of [Dh/8][8 slots][8 halves] core matrices, each followed by
+// its 8 slots' norms and ids (SBO = 16 Dh + 64 B, LBO = 128 B), so each slab of
+// a group is ONE contiguous cp.async.bulk into consecutive stage slots and the
+// four together are the N = 128 operand, norms and ids included.  No gather,
+// no shared-memory transpose (bulk copies stream 2x faster than TMA
+// tile::gather4 from L2, tools/g4_probe.cu).
 //
-// Roles (1 persistent CTA per SM, 15 warps, no CTA-wide barrier after setup;
+// Roles (1 persistent CTA per SM, 16 warps, no CTA-wide barrier after setup;
 // every hand-off is an mbarrier):
 //   warp 0      scheduler: claims work items (up to NITEM - 1 ahead, in an
 //               item ring) and walks each list's slab directory ahead of
 //               the producer, keeping the live slabs (bitmap != 0, Eq.
 //               slot_valid at slab granularity) with their flags
-//   warp 14     producer: per group of 4 live slabs, bulk copies of the fp16
-//               payloads, slot norms and ids into an nst-stage ring; a stage
-//               is refilled once the group that used it has completed
-//   warp 1      MMA: per group turns the bitmap into a NaN mask on the slot
-//               norms (group metadata for the epilogue), then one lane
-//               issues Dh/16 tcgen05.mma into one of NB = 3 TMEM accumulators;
-//               one tcgen05.commit per group (each costs ~200 cycles of
-//               tensor pipe) signals the epilogue and frees the stage
+//   warp 14     producer: per group of 4 live slabs, lanes 0-3 each issue
+//               one bulk copy of a slab record into an nst-stage ring
+//               (nst <= MAXST, as many as fit); a stage is refilled once the
+//               epilogue of the group that used it is done
+//   warp 15     group metadata: once a stage lands, NaN-masks the slot norms
+//               in place by the bitmap and computes each slab's max norm
+//   warp 1      MMA: one lane issues Dh/16 tcgen05.mma per group into one of
+//               NB = 3 TMEM accumulators; one tcgen05.commit per group (each
+//               costs ~200 cycles of tensor pipe) signals the epilogue
 //   warps 2-5   query loaders: the next item's 128 query rows as fp16 into
 //               the spare one of two TMEM A buffers (double-buffered across
 //               items), with ||q||^2 (fp32), the integrality and fp16-range
 //               flags (QInfo ring: up to NQI items ahead of the epilogue)
-//   warps 6-13  epilogue: thread = (query row, slab half); per slab,
-//               t = ||x||^2 - 2 q.x is one FFMA and the slab's filter one
-//               FMNMX per candidate; only chunks whose min passes the row's
-//               threshold take the per-lane slow path (exact distance, then
-//               a sorted register top-k of (dist, id) keys); the two halves
-//               of a row merge at the item's end
+//   warps 6-13  epilogue: two sets of 4 warps, set h takes the groups g with
+//               g & 1 == h (consecutive groups in flight at once); thread =
+//               query row, 4 chunks of 32 columns per group; per chunk,
+//               t = ||x||^2 - 2 q.x is one FFMA and the filter one FMNMX per
+//               candidate; only chunks whose min passes the row's threshold
+//               take the per-lane slow path (exact distance, then a sorted
+//               register top-k of (dist, id) keys); the two sets' lists of a
+//               row merge at the item's end
 // TMEM columns: A[0] [0,64), A[1] [64,128), D[b] = [128 + 128 b, 256 + 128 b), b < 3.
 //
 // Exactness (BASELINE.json tolerances): when query and slab values are
@@ -76,10 +80,10 @@ constexpr int GN = GS * kSlot;
 constexpr int NITEM = 8;  // work-item ring
 constexpr int NQI = 4;    // QInfo buffers: the loaders may run NQI items ahead of the epilogue
 constexpr int NB = 3;     // TMEM accumulator buffers (3 x 128 columns after the two 64-column A buffers)
-constexpr int MAXST = NB; // group ring depth cap (stages are freed through the accumulator barriers)
+constexpr int MAXST = 8;  // stage ring depth cap (a stage is freed by the epilogue, not by the MMA commit)
 constexpr int NLD = 4, NEPI = 8;
-constexpr int W_SCHED = 0, W_MMA = 1, W_LD0 = 2, W_EPI0 = W_LD0 + NLD, W_TMA = W_EPI0 + NEPI;
-constexpr int TTHREADS = 32 * (W_TMA + 1);
+constexpr int W_SCHED = 0, W_MMA = 1, W_LD0 = 2, W_EPI0 = W_LD0 + NLD, W_TMA = W_EPI0 + NEPI, W_META = W_TMA + 1;
+constexpr int TTHREADS = 32 * (W_META + 1);
 constexpr int MAXS = 64;  // live slabs per item prefetched by the scheduler (the producer walks the rest)
 
 struct TcArgs {
@@ -94,7 +98,7 @@ struct TcArgs {
   uint32_t* gthr;
   int phase;  // 0: every work item; 1: bucket 0 only; 2: bucket 1 only (phased scan)
   int dbg;  // experiments only (SIVF_OPT_DEBUG): bit0 skip the slow path, bit1 skip the fast path,
-            // bit2 skip the MMAs, bit3 skip the B copies, bit4 skip the A loads
+            // bit2 skip the MMAs, bit3 skip the B copies, bit4 skip the A loads, bit7 no per-group bound sharing
 };
 
 struct ItemRec {
@@ -103,19 +107,15 @@ struct ItemRec {
   int32_t dir_pos;     // directory position where the prefetch stopped (-1: complete)
   int32_t len, pad[2];
 };
+// Per stage: written by the producer (slab, bm, flag, nvalid, last) before the
+// stage's full barrier, and by the meta warp (xnmax) before meta_ready.
 struct StageMeta {
   int32_t slab[GS];  // -1: padding position
   uint32_t bm[GS];
   uint32_t flag[GS];
-  int32_t last, pad[3];
-};
-struct GroupMeta {
-  float xnm[GN];     // ||x||^2 per slot, NaN where the validity bit is clear
-  uint32_t id[GN];
   float xnmax[GS];   // max ||x||^2 over the slab's valid slots
-  uint32_t flag[GS];
-  int32_t slab[GS];
-  int32_t last, pad[3];
+  float sxmax[GS];   // sqrt(xnmax)
+  int32_t nvalid, last, pad[2];
 };
 struct QInfo {
   float qn;
@@ -125,21 +125,45 @@ struct QInfo {
 };
 
 struct TcPlan {
-  size_t stage_bytes, off_meta, off_gm, off_q, off_items, off_thr, off_mrg, off_bar, total;
+  size_t stage_bytes, off_meta, off_q, off_items, off_thr, off_mrg, off_ring, off_bar, total;
 };
 __host__ __device__ inline TcPlan tc_plan(int Dh, int nst, int KP) {
   TcPlan p;
-  p.stage_bytes = ((size_t)GN * Dh * 2 + 2 * GN * 4 + 1023) & ~(size_t)1023;  // fp16 payload + slot norms + ids
+  p.stage_bytes = ((size_t)GS * rec16_bytes(Dh) + 1023) & ~(size_t)1023;  // GS slab scan records (rec16_bytes)
   p.off_meta = (size_t)nst * p.stage_bytes;
-  p.off_gm = p.off_meta + MAXST * sizeof(StageMeta);
-  p.off_q = p.off_gm + NB * sizeof(GroupMeta);
+  p.off_q = p.off_meta + MAXST * sizeof(StageMeta);
   p.off_items = p.off_q + NQI * TM * sizeof(QInfo);
   p.off_thr = p.off_items + NITEM * (sizeof(ItemRec) + MAXS * sizeof(uint2));
   p.off_mrg = p.off_thr + 2 * TM * 8;
-  p.off_bar = p.off_mrg + (size_t)TM * KP * 8;
-  p.total = p.off_bar + (2 * MAXST + 2 * NB + 4 + 2 * NQI + 2 * NITEM + 2) * 8 + 1024;  // + alignment slack
+  p.off_ring = p.off_mrg + (size_t)TM * KP * 8;
+  p.off_bar = p.off_ring + 128 * sizeof(uint2);
+  p.total = p.off_bar + (3 * MAXST + 2 * NB + 4 + 2 * NQI + 2 * NITEM + 2) * 8 + 1024;  // + alignment slack
   return p;
 }
+
+#ifdef SIVF_TC_WATCHDOG
+// debug builds: a wait that spins too long reports (block, warp, barrier, parity) and traps
+__device__ __forceinline__ void scan_wait(uint64_t* bar, uint32_t phase, int tag) {
+  for (long long it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+    if (it == (1ll << 22)) {
+      printf("scan watchdog: block %d warp %d lane %d tag %d parity %u\n", blockIdx.x, threadIdx.x >> 5,
+             threadIdx.x & 31, tag, phase);
+      __trap();
+    }
+  }
+}
+#define MBW(bar, ph, tag) scan_wait(bar, ph, tag)
+#else
+#define MBW(bar, ph, tag) mbar_wait(bar, ph)
+#endif
 
 template <int KP>
 __device__ __forceinline__ void topk_reg_insert(u64 (&keys)[KP], u64 c) {
@@ -198,6 +222,15 @@ __device__ unsigned long long g_scnt[4];  // slow-path entries, survivors, inser
 #define PW(slot, stmt) stmt
 #endif
 
+// Pipeline (one persistent CTA per SM, 16 warps; every hand-off is an mbarrier):
+//   group g uses stage g % nst (fp16 payload, slot norms, ids; StageMeta) and
+//   TMEM accumulator g % NB.  producer -> full[stage] -> meta warp (NaN mask of
+//   the norms by the bitmap, xnmax) -> meta_ready[stage]; MMA warp waits
+//   full[stage] + acc_free[acc] -> MMAs -> one commit -> d_full[acc]; the
+//   epilogue set g & 1 processes group g (all 128 columns of its rows) while
+//   the other set processes g + 1, then both arrive on acc_free and stage_free
+//   (the stage is refilled only after its group's epilogue, so the producer
+//   can run nst groups ahead of the epilogue, nst up to MAXST).
 template <int KP>
 __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -206,43 +239,40 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   const int Dp = st.Dp, nq4 = Dp >> 2, Dh = st.Dh, nst = a.nst, k = a.k;
   const TcPlan p = tc_plan(Dh, nst, KP);
   StageMeta* smeta = reinterpret_cast<StageMeta*>(smem + p.off_meta);
-  GroupMeta* gm = reinterpret_cast<GroupMeta*>(smem + p.off_gm);
-  QInfo* qinfo = reinterpret_cast<QInfo*>(smem + p.off_q);  // [2][TM]
+  QInfo* qinfo = reinterpret_cast<QInfo*>(smem + p.off_q);  // [NQI][TM]
   ItemRec* items = reinterpret_cast<ItemRec*>(smem + p.off_items);
   uint2* irec = reinterpret_cast<uint2*>(items + NITEM);  // [NITEM][MAXS] (slab | flags << 30, bitmap)
   u64* thr_sh = reinterpret_cast<u64*>(smem + p.off_thr);    // [2][TM] (item << 32 | k-th bound bits)
   u64* mrg = reinterpret_cast<u64*>(smem + p.off_mrg);       // [TM][KP] half-list hand-over
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);  // [MAXST] producer -> MMA (tx bytes)
-  uint64_t* meta_full = full + MAXST;                              // [MAXST] producer -> MMA (stage metadata)
-  uint64_t* d_full = meta_full + MAXST;                            // [NB] MMA commit -> epilogue, producer
-  uint64_t* grp_free = d_full + NB;                                // [NB] epilogue -> MMA
-  uint64_t* a_full = grp_free + NB;                                 // [2] loaders -> MMA, epilogue
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);  // [MAXST] producer -> MMA, meta (tx bytes)
+  uint64_t* meta_ready = full + MAXST;                             // [MAXST] meta warp -> epilogue
+  uint64_t* stage_free = meta_ready + MAXST;                       // [MAXST] epilogue -> producer
+  uint64_t* d_full = stage_free + MAXST;                           // [NB] MMA commit -> epilogue
+  uint64_t* acc_free = d_full + NB;                                // [NB] epilogue -> MMA
+  uint64_t* a_full = acc_free + NB;                                // [2] loaders -> MMA
   uint64_t* a_free = a_full + 2;                                   // [2] MMA commit -> loaders
   uint64_t* q_read = a_free + 2;                                   // [NQI] epilogue -> loaders (QInfo consumed)
   uint64_t* q_full = q_read + NQI;                                 // [NQI] loaders -> epilogue (QInfo written)
   uint64_t* item_full = q_full + NQI;                              // [NITEM] scheduler -> all
   uint64_t* item_empty = item_full + NITEM;                        // [NITEM] epilogue -> scheduler
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(item_empty + NITEM);
-  auto stage_x = [&](int s) { return reinterpret_cast<uint16_t*>(smem + (size_t)s * p.stage_bytes); };
-  auto stage_nrm = [&](int s) {
-    return reinterpret_cast<float*>(smem + (size_t)s * p.stage_bytes + (size_t)GN * Dh * 2);
-  };
-  auto stage_id = [&](int s) {
-    return reinterpret_cast<uint32_t*>(smem + (size_t)s * p.stage_bytes + (size_t)GN * Dh * 2 + GN * 4);
-  };
+  // stage s: GS slab scan records back to back (slab j at j * rbytes)
+  auto stage_x = [&](int s) { return smem + (size_t)s * p.stage_bytes; };
+  const uint32_t rbytes = (uint32_t)rec16_bytes(Dh), sbo = (uint32_t)rec16_sbo(Dh);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef SIVF_TC_PROF
-  long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long pw[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const long long tstart = clock64();
 #endif
   if (threadIdx.x == 0) {
     for (int i = 0; i < MAXST; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&meta_full[i], 1);
+      mbar_init(&meta_ready[i], 1);
+      mbar_init(&stage_free[i], NEPI);
     }
     for (int b = 0; b < NB; ++b) {
-      mbar_init(&d_full[b], 2);
-      mbar_init(&grp_free[b], NEPI);
+      mbar_init(&d_full[b], 1);
+      mbar_init(&acc_free[b], NEPI / 2);  // the processing set only (see the epilogue)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a_full[b], NLD);
@@ -269,12 +299,12 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     // ------------------------------------------------------------ scheduler
     // claims work items and walks each list's slab directory ahead of the
     // producer (up to NITEM - 1 items ahead): the dependent loads (item ->
-    // directory -> bitmap -> flag) leave the TMA issue path
+    // directory -> bitmap -> flag) leave the copy issue path
     const int ntiles = st.ictr[a.phase == 1 ? I_NTILES0 : I_NTILES];
     const unsigned lt = (1u << lane) - 1u;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      if (lane == 0) PW(0, mbar_wait(&item_empty[slot], ((i / NITEM) & 1u) ^ 1u));
+      if (lane == 0) PW(0, MBW(&item_empty[slot], ((i / NITEM) & 1u) ^ 1u, 1));
       int w = 0;
       if (lane == 0) w = atomicAdd(&st.ictr[a.phase == 2 ? I_WORK2 : I_WORK], 1);
       w = __shfl_sync(kFull, w, 0);
@@ -312,109 +342,112 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     }
   } else if (warp == W_TMA) {
     // ------------------------------------------------------------ producer
+    // lane-parallel: one bulk copy per slab (its whole scan record) by lanes
+    // 0..GS-1.  Live slab records go through a 128-entry ring: the item's
+    // prefetched records, then (long lists) the rest of its directory; a group
+    // is emitted as not-last only while at least one more record follows it
+    uint2* pring = reinterpret_cast<uint2*>(smem + p.off_ring);
+    const unsigned lt = (1u << lane) - 1u;
     uint32_t gseq = 0;
-    // group slabs are held lane-distributed: lanes 0-3 the group being filled,
-    // lanes 4-7 the completed group waiting to learn whether it is the item's last
-    int my_s = 0;
-    uint32_t my_bm = 0u, my_fl = 0u;
-    auto emit = [&](int base, int nvalid, int last) {
+    auto emit = [&](uint32_t head, int nvalid, int last) {  // records pring[head, head + nvalid)
       const int stg = (int)(gseq % (uint32_t)nst);
-      // the stage is free once group gseq - nst has completed: its accumulator
-      // commit (d_full, the group's only tcgen05.commit) also frees its stage;
-      // nst <= NB, so that barrier cannot have moved on to a later phase
-      if (lane == 0 && gseq >= (uint32_t)nst) {
-        const uint32_t g0 = gseq - (uint32_t)nst;
-        PW(1, mbar_wait(&d_full[g0 % NB], (g0 / NB) & 1u));
-      }
+      if (lane == 0) PW(1, MBW(&stage_free[stg], ((gseq / (uint32_t)nst) & 1u) ^ 1u, 2));
       if (lane == 0) TR(0, gseq, clock64());
       __syncwarp();
-      const int sl = __shfl_sync(kFull, my_s, base + (lane & 3));
-      const uint32_t bmv = __shfl_sync(kFull, my_bm, base + (lane & 3));
-      const uint32_t flv = __shfl_sync(kFull, my_fl, base + (lane & 3));
       StageMeta& m = smeta[stg];
+      const uint2 r = lane < nvalid ? pring[(head + (uint32_t)lane) & 127u] : make_uint2(0u, 0u);
+      const int sl = (int)(r.x & 0x3fffffffu);
       if (lane < GS) {
         m.slab[lane] = lane < nvalid ? sl : -1;
-        m.bm[lane] = lane < nvalid ? bmv : 0u;
-        m.flag[lane] = lane < nvalid ? flv : 0u;
+        m.bm[lane] = r.y;
+        m.flag[lane] = r.x >> 30;
       }
-      if (lane == 0) m.last = last;
-      __syncwarp();
-      const uint32_t sbytes = (uint32_t)(kSlot * Dh * 2);
       if (lane == 0) {
-        mbar_arrive(&meta_full[stg]);
-        mbar_arrive_expect_tx(&full[stg], (a.dbg & 8) ? 0u : (uint32_t)nvalid * (sbytes + 2u * kSlot * 4u));
+        m.nvalid = nvalid;
+        m.last = last;
       }
       __syncwarp();
-      if (a.dbg & 8) nvalid = 0;  // experiment: no B traffic
-      // padding positions are not copied: their stale (finite) or uninitialised
-      // columns only reach D columns whose slot norm is the NaN mask
-      if (lane < nvalid) {
-        bulk_g2s(stage_x(stg) + (size_t)lane * kSlot * Dh, st.payload16 + (size_t)sl * kSlot * Dh, sbytes, &full[stg]);
-        bulk_g2s(stage_nrm(stg) + lane * kSlot, st.slab_norm + (size_t)sl * kSlot, kSlot * 4, &full[stg]);
-        bulk_g2s(stage_id(stg) + lane * kSlot, st.slab_ids + (size_t)sl * kSlot, kSlot * 4, &full[stg]);
-      }
+      if (lane == 0) mbar_arrive_expect_tx(&full[stg], (a.dbg & 8) ? 0u : (uint32_t)nvalid * rbytes);
+      __syncwarp();
+      if (lane < nvalid && !(a.dbg & 8))
+        bulk_g2s(stage_x(stg) + (size_t)lane * rbytes, reinterpret_cast<const unsigned char*>(st.payload16) +
+                                                           (size_t)sl * rbytes, rbytes, &full[stg]);
       ++gseq;
-    };
-    int cnt = 0;
-    bool has_pend = false;
-    auto feed = [&](int ss, uint32_t sbm, uint32_t sfl) {  // warp-uniform arguments
-      if (cnt == GS) {
-        if (has_pend) emit(4, GS, 0);
-        const int ps = __shfl_sync(kFull, my_s, lane & 3);
-        const uint32_t pb = __shfl_sync(kFull, my_bm, lane & 3), pf = __shfl_sync(kFull, my_fl, lane & 3);
-        if (lane >= 4 && lane < 8) {
-          my_s = ps;
-          my_bm = pb;
-          my_fl = pf;
-        }
-        has_pend = true;
-        cnt = 0;
-      }
-      if (lane == cnt) {
-        my_s = ss;
-        my_bm = sbm;
-        my_fl = sfl;
-      }
-      ++cnt;
     };
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      PW(4, mbar_wait(&item_full[slot], (i / NITEM) & 1u));
+      PW(4, MBW(&item_full[slot], (i / NITEM) & 1u, 3));
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
-      cnt = 0;
-      has_pend = false;
+      uint32_t head = 0u, tail = 0u;  // warp-uniform ring cursors
       const uint2* rr = irec + slot * MAXS;
-      for (int r = 0; r < rec.npre; ++r) {
-        const uint2 x = rr[r];
-        feed((int)(x.x & 0x3fffffffu), x.y, x.x >> 30);
+      for (int r0 = 0; r0 < rec.npre; r0 += 32)
+        if (r0 + lane < rec.npre) pring[(uint32_t)(r0 + lane) & 127u] = rr[r0 + lane];
+      tail = (uint32_t)rec.npre;
+      __syncwarp();
+      while (tail - head > (uint32_t)GS) {
+        emit(head, GS, 0);
+        head += GS;
       }
       if (rec.dir_pos >= 0) {  // long list: walk the rest of the directory here
         const int32_t* dir = st.dir_arena + st.dir_off[rec.l];
         for (int j0 = rec.dir_pos; j0 < rec.len; j0 += 32) {
           const int j = j0 + lane;
-          int s = 0;
+          int sl = 0;
           uint32_t bm = 0u, fl = 0u;
           if (j < rec.len) {
-            s = dir[j];
-            bm = st.bitmap[s];
-            if (bm) fl = st.slab_flag[s] & 3u;
+            sl = dir[j];
+            bm = st.bitmap[sl];
+            if (bm) fl = st.slab_flag[sl] & 3u;
           }
-          unsigned live = __ballot_sync(kFull, bm != 0u);
-          while (live) {
-            const int src = __ffs(live) - 1;
-            live &= live - 1;
-            feed(__shfl_sync(kFull, s, src), __shfl_sync(kFull, bm, src), __shfl_sync(kFull, fl, src));
+          const unsigned live = __ballot_sync(kFull, bm != 0u);
+          if (bm) pring[(tail + (uint32_t)__popc(live & lt)) & 127u] = make_uint2((uint32_t)sl | (fl << 30), bm);
+          tail += (uint32_t)__popc(live);
+          __syncwarp();
+          while (tail - head > (uint32_t)GS) {
+            emit(head, GS, 0);
+            head += GS;
           }
         }
       }
-      if (cnt > 0) {
-        if (has_pend) emit(4, GS, 0);
-        emit(0, cnt, 1);
-      } else if (has_pend) {
-        emit(4, GS, 1);
-      } else {
-        emit(0, 0, 1);  // no live slab: one fully masked group keeps the roles in step
+      emit(head, (int)(tail - head), 1);  // 0..GS records (0: the item has no live slab, an empty group)
+    }
+  } else if (warp == W_META) {
+    // ------------------------------------------------------------ group metadata
+    // per group, after its copies land: slot norms NaN-masked in place by the
+    // validity bitmap (Eq. slot_valid) and the per-slab max ||x||^2 for the
+    // epilogue's error bound, off the MMA issue path
+    uint32_t gseq = 0;
+    for (uint32_t i = 0;; ++i) {
+      const int slot = (int)(i % NITEM);
+      MBW(&item_full[slot], (i / NITEM) & 1u, 4);
+      if (items[slot].l < 0) break;
+      for (;;) {
+        const int stg = (int)(gseq % (uint32_t)nst);
+        PW(0, MBW(&full[stg], (gseq / (uint32_t)nst) & 1u, 5));
+        StageMeta& m = smeta[stg];
+        const int nv = m.nvalid;
+        unsigned char* sb = stage_x(stg) + rec16_norm_off(Dh, lane);
+#pragma unroll
+        for (int j = 0; j < GS; ++j) {
+          if (j < nv) {
+            const bool v = ((m.bm[j] >> lane) & 1u) != 0u;
+            float* np = reinterpret_cast<float*>(sb + (size_t)j * rbytes);
+            const float xn = *np;
+            *np = v ? xn : __int_as_float(0x7fc00000);
+            const uint32_t mx = __reduce_max_sync(kFull, v ? __float_as_uint(fmaxf(xn, 0.f)) : 0u);
+            if (lane == 0) {
+              m.xnmax[j] = __uint_as_float(mx);
+              m.sxmax[j] = sqrtf(__uint_as_float(mx));
+            }
+          }
+        }
+        const int last = m.last;
+        fence_proxy_async_smem();  // generic writes of the stage ordered before its next bulk refill
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&meta_ready[stg]);
+        ++gseq;
+        if (last) break;
       }
     }
   } else if (warp == W_MMA) {
@@ -423,63 +456,32 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     uint32_t gseq = 0;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      PW(6, mbar_wait(&item_full[slot], (i / NITEM) & 1u));
+      PW(6, MBW(&item_full[slot], (i / NITEM) & 1u, 6));
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       const uint32_t ab = i & 1u;
-      PW(1, mbar_wait(&a_full[ab], (i >> 1) & 1u));
+      PW(1, MBW(&a_full[ab], (i >> 1) & 1u, 7));
       for (;;) {
         const int stg = (int)(gseq % (uint32_t)nst);
         const uint32_t b = gseq % NB;
-        PW(0, mbar_wait(&meta_full[stg], (gseq / (uint32_t)nst) & 1u));
-        const StageMeta& sm = smeta[stg];
-        float xnv[GS];
-        uint32_t idv[GS];
-        PW(2, mbar_wait(&full[stg], (gseq / (uint32_t)nst) & 1u));
+        PW(2, MBW(&full[stg], (gseq / (uint32_t)nst) & 1u, 8));
+        const int last = smeta[stg].last, nv = smeta[stg].nvalid;
+        PW(3, MBW(&acc_free[b], ((gseq / NB) & 1u) ^ 1u, 9));
         if (lane == 0) TR(1, gseq, clock64());
-#pragma unroll
-        for (int j = 0; j < GS; ++j) {  // staged with the payload (garbage at padding positions: masked)
-          xnv[j] = stage_nrm(stg)[j * kSlot + lane];
-          idv[j] = stage_id(stg)[j * kSlot + lane];
-        }
-        PW(3, mbar_wait(&grp_free[b], ((gseq / NB) & 1u) ^ 1u));
-        if (lane == 0) TR(2, gseq, clock64());
-        GroupMeta& g = gm[b];
 #ifdef SIVF_TC_PROF
         long long _tm0 = clock64();
-#endif
-#pragma unroll
-        for (int j = 0; j < GS; ++j) {
-          const bool v = ((sm.bm[j] >> lane) & 1u) != 0u;
-          const float xn = xnv[j];
-          g.xnm[j * kSlot + lane] = v ? xn : __int_as_float(0x7fc00000);
-          g.id[j * kSlot + lane] = idv[j];
-          const uint32_t mx = __reduce_max_sync(kFull, v ? __float_as_uint(fmaxf(xn, 0.f)) : 0u);
-          if (lane == 0) {
-            g.xnmax[j] = __uint_as_float(mx);
-            g.flag[j] = sm.flag[j];
-            g.slab[j] = sm.slab[j];
-          }
-        }
-        const int last = sm.last;
-        if (lane == 0) g.last = last;
-        __syncwarp();
-#ifdef SIVF_TC_PROF
-        pw[5] += clock64() - _tm0;
-        _tm0 = clock64();
 #endif
         if (lane == 0) {
           tc_fence_after();
           const uint32_t bsm = smem_u32(stage_x(stg));
           const uint32_t dt = tbase + 128u + b * 128u, at = tbase + ab * 64u;
           // kind::f16: A (fp16 query tile) in TMEM, 8 columns per K = 16 step;
-          // B (fp16 slab copies) K-major SWIZZLE_NONE, LBO = 128 B, SBO = 16 Dh B
-          for (int kk = 0; kk < ((a.dbg & 4) ? 0 : (Dh >> 4)); ++kk)
-            umma_f16_ts(dt, at + (uint32_t)(8 * kk), umma_sdesc(bsm + (uint32_t)kk * 256u, 128u, (uint32_t)Dh * 16u),
+          // B (fp16 slab records) K-major SWIZZLE_NONE, LBO = 128 B, SBO = 16 Dh + 64 B
+          const int nk = ((a.dbg & 4) || nv == 0) ? 0 : (Dh >> 4);
+          for (int kk = 0; kk < nk; ++kk)
+            umma_f16_ts(dt, at + (uint32_t)(8 * kk), umma_sdesc(bsm + (uint32_t)kk * 256u, 128u, sbo),
                         idesc, kk > 0 ? 1u : 0u);
-          umma_commit(&d_full[b]);    // accumulator ready and stage stg free (one commit per group:
-                                      // each tcgen05.commit costs ~200 cycles of tensor pipe, mma_probe)
-          mbar_arrive(&d_full[b]);    // group metadata written
+          umma_commit(&d_full[b]);  // accumulator ready (one commit per group)
           if (last) umma_commit(&a_free[ab]);  // A[ab] may be overwritten once these MMAs are done
         }
         __syncwarp();
@@ -501,7 +503,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     const int nc8 = Dh >> 3;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      mbar_wait(&item_full[slot], (i / NITEM) & 1u);
+      MBW(&item_full[slot], (i / NITEM) & 1u, 10);
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       const uint32_t ab = i & 1u;
@@ -512,9 +514,6 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       const uint32_t ta = tbase + ((uint32_t)(32 * qw) << 16) + ab * 64u;
       float nrm = 0.f;
       uint32_t integ = 1u, over = 0u;
-#ifdef SIVF_TC_PROF
-      long long _tl0 = clock64();
-#endif
       for (int h0 = 0; h0 < nc8; h0 += 8) {
         float x[8][8];
 #pragma unroll
@@ -531,7 +530,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           }
         }
         if (h0 == 0) {
-          PW(4, mbar_wait(&a_free[ab], ((i >> 1) & 1u) ^ 1u));
+          PW(4, MBW(&a_free[ab], ((i >> 1) & 1u) ^ 1u, 11));
           tc_fence_after();
         }
 #pragma unroll
@@ -554,16 +553,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           }
         }
       }
-#ifdef SIVF_TC_PROF
-      pw[1] += clock64() - _tl0;
-      _tl0 = clock64();
-#endif
       tmem_st_wait();
-#ifdef SIVF_TC_PROF
-      pw[2] += clock64() - _tl0;
-#endif
       const int qb = (int)(i % NQI);
-      PW(5, mbar_wait(&q_read[qb], ((i / NQI) & 1u) ^ 1u));  // item i - NQI's QInfo has been read
+      PW(5, MBW(&q_read[qb], ((i / NQI) & 1u) ^ 1u, 12));  // item i - NQI's QInfo has been read
       qinfo[qb * TM + row] = QInfo{nrm, pair, integ, over};
       tc_fence_before();
       __syncwarp();
@@ -574,9 +566,11 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    // thread = (query row, slab half h): slabs 2h, 2h+1 of every group; the two
-    // halves of a row keep separate top-k lists (merged at the item's end) and
-    // share their k-th distance bounds through shared memory every group
+    // two sets of 4 warps; set h processes the groups g with g & 1 == h, thread
+    // = query row, all 4 slabs (128 columns) of the group: the two sets work
+    // on consecutive groups concurrently.  Each set keeps its own per-row
+    // top-k (merged at the item's end) and the two share their k-th distance
+    // bounds through shared memory every group
     const int qw = warp & 3, row = 32 * qw + lane, h = (warp - W_EPI0) >> 2;
     // certified band of the fp16 filter (u = 2^-11, RN): eps1 bounds the
     // relative error of q.x from the operand roundings (2u + u^2 <= 2^-9 +
@@ -586,14 +580,14 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     const float eps1 = 0x1p-9f + 0x1p-19f + (float)Dh * 0x1p-23f;
     const float eps2 = (float)(2 * Dp + 10) * 0x1p-24f;
     const float esub = 0x1p-23f * 1.001f * sqrtf((float)Dh);
+    const int dbg = a.dbg;
     uint32_t gseq = 0;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
-      PW(4, mbar_wait(&item_full[slot], (i / NITEM) & 1u));
+      PW(4, MBW(&item_full[slot], (i / NITEM) & 1u, 13));
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
-      const uint32_t ab = i & 1u;
-      PW(1, mbar_wait(&q_full[i % NQI], (i / NQI) & 1u));
+      PW(1, MBW(&q_full[i % NQI], (i / NQI) & 1u, 14));
       const QInfo qi = qinfo[(i % NQI) * TM + row];
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_read[i % NQI]);
@@ -609,156 +603,166 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       u64 kth = kPadKey;
       for (;;) {
         const uint32_t b = gseq % NB;
-        PW(5, mbar_wait(&d_full[b], (gseq / NB) & 1u));
-        if (lane == 0 && warp == W_EPI0 + 2) TR(3, gseq, clock64());
-        if (lane == 0 && warp == W_EPI0 + 6) TR(5, gseq, clock64());
-        tc_fence_after();
-        const GroupMeta& g = gm[b];
-        if (wact) {
-          const u64 ps = thr_sh[(1 - h) * TM + row];  // partner half's bound, tagged with its item
-          if ((uint32_t)(ps >> 32) == i) thr = fminf(thr, __uint_as_float((uint32_t)ps));
-          thr = fminf(thr, gnext);  // other items of the same query (read one group ago)
-          if (rv) gnext = __uint_as_float(__ldcg(a.gthr + qglob));
-          // one chunk = one slab = 32 TMEM columns of this row
-          auto chunk = [&](const int j, const uint32_t(&v)[32]) {
-            const float xm = g.xnmax[j], sxm = sqrtf(xm);
-            const float rs = sqn + sxm;
-            const bool ex = qi.qint != 0u && (g.flag[j] & kFlagIntegral) != 0u && rs * rs < 16000000.f;
-            // no finite fp16 copy of the query or the slab: every valid slot is re-ranked exactly
-            const bool unsafe = qi.qover != 0u || (g.flag[j] & kFlagF16Over) != 0u;
-            float E = 0.f;
-            if (!ex) {
-              const float cs = sqn * sxm;
-              E = 2.f * (2.f * eps1 * cs + eps2 * (qn + xm + 2.f * cs)) + esub * rs;
-            }
-            float tadj = ex ? __fsub_ru(thr, qn) : __fadd_ru(__fsub_ru(thr, qn), E);
-            const float4* x4 = reinterpret_cast<const float4*>(g.xnm + 32 * j);
-            float m8[8];
+        const int stg = (int)(gseq % (uint32_t)nst);
+        const bool mine = (gseq & 1u) == (uint32_t)h;
+        PW(5, MBW(&meta_ready[stg], (gseq / (uint32_t)nst) & 1u, 15));
+        const StageMeta& m = smeta[stg];
+        const int last = m.last;
+        if (mine) {
+          PW(6, MBW(&d_full[b], (gseq / NB) & 1u, 16));
+          if (lane == 0 && warp == W_EPI0 + 2) TR(3, gseq, clock64());
+          tc_fence_after();
+          const int nv = m.nvalid;
+          if (wact && nv > 0) {
+            const u64 ps = thr_sh[(1 - h) * TM + row];  // other set's bound, tagged with its item
+            if ((uint32_t)(ps >> 32) == i) thr = fminf(thr, __uint_as_float((uint32_t)ps));
+            thr = fminf(thr, gnext);  // other items of the same query (read one group ago)
+            if (rv && !(dbg & 128)) gnext = __uint_as_float(__ldcg(a.gthr + qglob));
+            const unsigned char* sbase = stage_x(stg);
+            // one chunk = one slab = 32 TMEM columns of this row
+            auto chunk = [&](const int j, const uint32_t(&v)[32]) {
+              const unsigned char* rb = sbase + (size_t)j * rbytes;  // slab j's record
+              const uint32_t fl = m.flag[j];
+              const float sxm = m.sxmax[j];
+              const float rs = sqn + sxm;
+              const bool ex = qi.qint != 0u && (fl & kFlagIntegral) != 0u && rs * rs < 16000000.f;
+              // no finite fp16 copy of the query or the slab: every valid slot is re-ranked exactly
+              const bool unsafe = qi.qover != 0u || (fl & kFlagF16Over) != 0u;
+              float E = 0.f;
+              if (!ex) {
+                const float xm = m.xnmax[j];
+                const float cs = sqn * sxm;
+                E = 2.f * (2.f * eps1 * cs + eps2 * (qn + xm + 2.f * cs)) + esub * rs;
+              }
+              float tadj = ex ? __fsub_ru(thr, qn) : __fadd_ru(__fsub_ru(thr, qn), E);
+              // norms of slots 4 c4 .. 4 c4 + 3 (row group c4 / 2), NaN where the slot is not valid
+              auto x4 = [&](int c4) {
+                return *reinterpret_cast<const float4*>(rb + (size_t)(c4 >> 1) * sbo + (size_t)16 * Dh + (c4 & 1) * 16);
+              };
+              float m8[8];
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              const float4 xx = x4[c4];
-              const float t0 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 0]), xx.x);
-              const float t1 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 1]), xx.y);
-              const float t2 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 2]), xx.z);
-              const float t3 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 3]), xx.w);
-              m8[c4] = fminf(fminf(t0, t1), fminf(t2, t3));
-            }
-            const float mn = fminf(fminf(fminf(m8[0], m8[1]), fminf(m8[2], m8[3])),
-                                   fminf(fminf(m8[4], m8[5]), fminf(m8[6], m8[7])));
-            if (!unsafe && (!(mn <= tadj) || (a.dbg & 1))) return;
-            // slow path (per lane): survivors of this slab, exact distance, register top-k
+              for (int c4 = 0; c4 < 8; ++c4) {
+                const float4 xx = x4(c4);
+                const float t0 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 0]), xx.x);
+                const float t1 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 1]), xx.y);
+                const float t2 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 2]), xx.z);
+                const float t3 = fmaf(-2.f, __uint_as_float(v[4 * c4 + 3]), xx.w);
+                m8[c4] = fminf(fminf(t0, t1), fminf(t2, t3));
+              }
+              const float mn = fminf(fminf(fminf(m8[0], m8[1]), fminf(m8[2], m8[3])),
+                                     fminf(fminf(m8[4], m8[5]), fminf(m8[6], m8[7])));
+              if (!unsafe && (!(mn <= tadj) || (dbg & 1))) return;
+              // slow path (per lane): survivors of this slab, exact distance, register top-k
 #ifdef SIVF_TC_PROF
-            long long _ts = clock64();
+              long long _ts = clock64();
+              SCNT_ADD(&g_scnt[0], 1ull);
+              const bool cold = !(thr < INFINITY);
 #endif
-#ifdef SIVF_TC_PROF
-            SCNT_ADD(&g_scnt[0], 1ull);
-#endif
-            uint32_t pm = 0u;
-            if (unsafe) {
-#pragma unroll
-              for (int c = 0; c < 32; ++c) pm |= (g.xnm[32 * j + c] == g.xnm[32 * j + c] ? 1u : 0u) << c;  // valid
-            } else
-#pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              if (!(m8[c4] <= tadj)) continue;  // the quad's minimum already fails
-              const float4 xx = x4[c4];
-              pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 0]), xx.x) <= tadj ? 1u : 0u) << (4 * c4);
-              pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 1]), xx.y) <= tadj ? 1u : 0u) << (4 * c4 + 1);
-              pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 2]), xx.z) <= tadj ? 1u : 0u) << (4 * c4 + 2);
-              pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 3]), xx.w) <= tadj ? 1u : 0u) << (4 * c4 + 3);
-            }
-#ifdef SIVF_TC_PROF
-            SCNT_ADD(&g_scnt[1], (unsigned long long)__popc(pm));
-#endif
-            while (pm) {
-              const int c = __ffs(pm) - 1;
-              pm &= pm - 1;
-              const float t = fmaf(-2.f, __uint_as_float(pick32(v, c)), g.xnm[32 * j + c]);
-              if (!unsafe && !(t <= tadj)) continue;  // the threshold may have tightened
-              float d;
-              if (ex) {
-                d = qn + t;  // exact: every term an integer < 2^24
+              uint32_t pm = 0u;
+              if (unsafe) {
+                pm = m.bm[j];  // every valid slot
               } else {
-                const float* xs = st.payload + (size_t)g.slab[j] * kSlot * Dp;
-                const float* qr = a.Q + (int64_t)qglob * st.D;
-                float acc = 0.f;
-                for (int i4 = 0; i4 < nq4; ++i4) {
-                  const float4 xv = __ldg(reinterpret_cast<const float4*>(xs + pay_off(Dp, c, i4)));
-                  float qv[4];
 #pragma unroll
-                  for (int e = 0; e < 4; ++e) qv[e] = 4 * i4 + e < st.D ? __ldg(qr + 4 * i4 + e) : 0.f;
-                  float tt;
-                  tt = qv[0] - xv.x; acc = fmaf(tt, tt, acc);
-                  tt = qv[1] - xv.y; acc = fmaf(tt, tt, acc);
-                  tt = qv[2] - xv.z; acc = fmaf(tt, tt, acc);
-                  tt = qv[3] - xv.w; acc = fmaf(tt, tt, acc);
+                for (int c4 = 0; c4 < 8; ++c4) {
+                  if (!(m8[c4] <= tadj)) continue;  // the quad's minimum already fails
+                  const float4 xx = x4(c4);
+                  pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 0]), xx.x) <= tadj ? 1u : 0u) << (4 * c4);
+                  pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 1]), xx.y) <= tadj ? 1u : 0u) << (4 * c4 + 1);
+                  pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 2]), xx.z) <= tadj ? 1u : 0u) << (4 * c4 + 2);
+                  pm |= (fmaf(-2.f, __uint_as_float(v[4 * c4 + 3]), xx.w) <= tadj ? 1u : 0u) << (4 * c4 + 3);
                 }
-                d = acc;
-              }
-              d = fmaxf(d, 0.f);
-              if (!(d <= thr)) continue;
-              const u64 key = make_key(d, g.id[32 * j + c]);
-              if (key >= kth) continue;
-              topk_reg_insert<KP>(keys, key);
-              kth = keys[KP - 1];
-              if (kth != kPadKey) {
-                thr = fminf(thr, key_dist(kth));
-                tadj = ex ? __fsub_ru(thr, qn) : __fadd_ru(__fsub_ru(thr, qn), E);
               }
 #ifdef SIVF_TC_PROF
-              pw[7]++;
-              SCNT_ADD(&g_scnt[2], 1ull);
+              SCNT_ADD(&g_scnt[1], (unsigned long long)__popc(pm));
 #endif
-            }
+              while (pm) {
+                const int c = __ffs(pm) - 1;
+                pm &= pm - 1;
+                const float t = fmaf(-2.f, __uint_as_float(pick32(v, c)),
+                                     *reinterpret_cast<const float*>(rb + rec16_norm_off(Dh, c)));
+                if (!unsafe && !(t <= tadj)) continue;  // the threshold may have tightened
+                float d;
+                if (ex) {
+                  d = qn + t;  // exact: every term an integer < 2^24
+                } else {
+                  const float* xs = st.payload + (size_t)m.slab[j] * kSlot * Dp;
+                  const float* qr = a.Q + (int64_t)qglob * st.D;
+                  float acc = 0.f;
+                  for (int i4 = 0; i4 < nq4; ++i4) {
+                    const float4 xv = __ldg(reinterpret_cast<const float4*>(xs + pay_off(Dp, c, i4)));
+                    float qv[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) qv[e] = 4 * i4 + e < st.D ? __ldg(qr + 4 * i4 + e) : 0.f;
+                    float tt;
+                    tt = qv[0] - xv.x; acc = fmaf(tt, tt, acc);
+                    tt = qv[1] - xv.y; acc = fmaf(tt, tt, acc);
+                    tt = qv[2] - xv.z; acc = fmaf(tt, tt, acc);
+                    tt = qv[3] - xv.w; acc = fmaf(tt, tt, acc);
+                  }
+                  d = acc;
+                }
+                d = fmaxf(d, 0.f);
+                if (!(d <= thr)) continue;
+                const u64 key = make_key(d, *reinterpret_cast<const uint32_t*>(rb + rec16_id_off(Dh, c)));
+                if (key >= kth) continue;
+                topk_reg_insert<KP>(keys, key);
+                kth = keys[KP - 1];
+                if (kth != kPadKey) {
+                  thr = fminf(thr, key_dist(kth));
+                  tadj = ex ? __fsub_ru(thr, qn) : __fadd_ru(__fsub_ru(thr, qn), E);
+                }
 #ifdef SIVF_TC_PROF
-            pw[6] += clock64() - _ts;
+                pw[7]++;
+                SCNT_ADD(&g_scnt[2], 1ull);
+                if (cold) SCNT_ADD(&g_scnt[3], 1ull);
 #endif
-          };
-          const uint32_t dcol = tbase + ((uint32_t)(32 * qw) << 16) + 128u + b * 128u + (uint32_t)(64 * h);
+              }
 #ifdef SIVF_TC_PROF
-          long long _tg = clock64();
+              pw[2] += clock64() - _ts;
+#endif
+            };
+            const uint32_t dcol = tbase + ((uint32_t)(32 * qw) << 16) + 128u + b * 128u;
+#ifdef SIVF_TC_PROF
+            long long _tg = clock64();
 #endif
 #pragma unroll 1
-          for (int jj = 0; jj < 2; ++jj) {
-            uint32_t v[32];
-#ifdef SIVF_TC_PROF
-            long long _tq = clock64();
-#endif
-            if (!(a.dbg & 32)) {
-              tmem_ld32(dcol + 32u * (uint32_t)jj, v);
+            for (int j = 0; j < nv; ++j) {
+              uint32_t v[32];
+              tmem_ld32(dcol + 32u * (uint32_t)j, v);
               tmem_ld_wait();
-            } else {
-#pragma unroll
-              for (int c = 0; c < 32; ++c) v[c] = 0x7f800000u;
+              if (!(dbg & 2)) chunk(j, v);
             }
 #ifdef SIVF_TC_PROF
-            pw[3] += clock64() - _tq;
+            pw[0] += clock64() - _tg;
 #endif
-            if (!(a.dbg & 2)) chunk(2 * h + jj, v);
+            thr_sh[h * TM + row] = ((u64)i << 32) | __float_as_uint(thr);
+            if (rv && thr < tpub && !(dbg & 128)) {  // share the bound with the query's other items right away
+              atomicMin(a.gthr + qglob, __float_as_uint(thr));
+              tpub = thr;
+            }
           }
-#ifdef SIVF_TC_PROF
-          pw[0] += clock64() - _tg;
-#endif
-          thr_sh[h * TM + row] = ((u64)i << 32) | __float_as_uint(thr);
-          if (rv && thr < tpub) {  // share the bound with the query's other items right away
-            atomicMin(a.gthr + qglob, __float_as_uint(thr));
-            tpub = thr;
-          }
+          if (lane == 0 && warp == W_EPI0 + 2) TR(4, gseq, clock64());
+          tc_fence_before();
+          __syncwarp();
+          // only the processing set frees the accumulator: an early arrival of
+          // the other set could land in the previous phase of the barrier (its
+          // arrival for group g is not ordered after the completion of g - NB)
+          if (lane == 0) mbar_arrive(&acc_free[b]);
         }
-        const int last = g.last;
-        if (lane == 0 && warp == W_EPI0 + 2) TR(4, gseq, clock64());
-        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&grp_free[b]);
+        // both sets free the stage, each after reading its metadata: every
+        // arrival for group g follows meta_ready(g), hence the refill for g,
+        // hence the completion of the stage's phase for g - nst
+        if (lane == 0) mbar_arrive(&stage_free[stg]);
         ++gseq;
         if (last) break;
       }
-      // merge the two halves of each row: h = 1 hands its list over in smem
+      // merge the two sets' lists of each row: h = 1 hands its list over in smem
       if (h == 1 && rv) {
 #pragma unroll
         for (int t = 0; t < KP; ++t) mrg[row * KP + t] = keys[t];
       }
-      PW(2, named_bar_sync(1 + qw, 64));
+      PW(3, named_bar_sync(1 + qw, 64));
       if (h == 0 && rv) {
         for (int t = KP - k; t < KP; ++t) {
           const u64 key = mrg[row * KP + t];
@@ -779,8 +783,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   }
 #ifdef SIVF_TC_PROF
   if (blockIdx.x < 2 && lane == 0)
-    printf("blk %d warp %d total %lld | p0 %lld p1 %lld p2 %lld p3 %lld p4 %lld p5 %lld slow %lld ins %lld\n",
-           blockIdx.x, warp, clock64() - tstart, pw[0], pw[1], pw[2], pw[3], pw[4], pw[5], pw[6], pw[7]);
+    printf("blk %d warp %d total %lld | p0 %lld p1 %lld p2 %lld p3 %lld p4 %lld p5 %lld p6 %lld ins %lld p8 %lld p9 %lld\n",
+           blockIdx.x, warp, clock64() - tstart, pw[0], pw[1], pw[2], pw[3], pw[4], pw[5], pw[6], pw[7], pw[8], pw[9]);
 #endif
   tc_fence_before();
   __syncthreads();
@@ -849,7 +853,8 @@ int tc_stages(const Index& ix, int KP) {
   const size_t fixed = tc_plan(ix.st.Dh, 0, KP).total;
   if (ix.smem_optin < fixed) return 0;
   int n = (int)((ix.smem_optin - fixed) / sb);
-  return n > NB ? NB : n;  // the producer reuses the accumulator barriers: nst <= NB
+  if (ix.tc_max_stages > 0 && n > ix.tc_max_stages) n = ix.tc_max_stages;  // experiments (SIVF_OPT_TC_STAGES)
+  return n > MAXST ? MAXST : n;
 }
 
 }  // namespace

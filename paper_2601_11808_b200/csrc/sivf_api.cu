@@ -76,7 +76,7 @@ Layout make_layout(const sivf_config* c) {
   L.max_work = (npairs + 7) / 8 + 2 * nl + 1;
 
   L.payload = take(L, (size_t)S * kSlot * L.Dp * 4);
-  L.payload16 = take(L, (size_t)S * kSlot * L.Dh * 2);
+  L.payload16 = take(L, L.Dh ? (size_t)S * rec16_bytes((int)L.Dh) : 0);
   L.slab_ids = take(L, (size_t)S * kSlot * 4);
   L.slab_norm = take(L, (size_t)S * kSlot * 4);
   L.slab_flag = take(L, (size_t)S * 4);
@@ -608,7 +608,7 @@ sivf_rc sivf_stats(sivf_index h, sivf_stats_t* out, sivf_stream_t stream) {
   out->overhead_actual =
       live_bytes > 0 ? (16.0 * out->slabs_in_use + 8.0 * (double)ix->st.cap_local) / live_bytes : 0.0;
   out->overhead_scan_copy =
-      live_bytes > 0 ? 2.0 * ix->st.Dh * kSlot * (double)out->slabs_in_use / live_bytes : 0.0;
+      live_bytes > 0 && ix->st.Dh ? (double)rec16_bytes(ix->st.Dh) * (double)out->slabs_in_use / live_bytes : 0.0;
   return SIVF_OK;
 }
 
@@ -628,6 +628,7 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
     case SIVF_OPT_COARSE_SELECT: ix->coarse_select = value != 0 && ix->coarse_select_ok; return SIVF_OK;
     case SIVF_OPT_RANK_SPLIT: ix->rank_split = value < 0 ? 0 : (int)value; return SIVF_OK;
     case 99: ix->dbg = (int)value; return SIVF_OK;  // SIVF_OPT_DEBUG: experiments only
+    case 98: ix->tc_max_stages = (int)value; return SIVF_OK;  // experiments only: scan stage-ring cap
     case SIVF_OPT_SEED_SLABS:
       if (value < 0 || value > (1 << 20)) return SIVF_E_INVALID_ARG;
       ix->seed_slabs = (int)value;

@@ -19,11 +19,23 @@ constexpr int kSlot = 32;                          // slab capacity C = 32 (P:15
 __host__ __device__ __forceinline__ size_t pay_off(int Dp, int n, int c4) {
   return ((size_t)((n >> 3) * (Dp >> 2) + c4) * 8 + (n & 7)) * 4;
 }
-// The fp16 scan copy has the same structure with 16-B chunks of 8 halves:
-// half offset of chunk c8 of slot n (LBO = 128 B, SBO = 16 Dh B).
+// The fp16 scan record of a slab (reading C35): 4 row groups, each the 8
+// slots' fp16 copy as [Dh/8 chunks][8 slots][8 halves] core matrices (16 Dh B)
+// followed by the 8 slots' ||x||^2 (f32[8]) and ids (u32[8]), 16 Dh + 64 B.
+// One contiguous bulk copy per slab stages everything the scan reads of it;
+// 4 slabs copied back to back are one N = 128 UMMA B operand (K-major,
+// SWIZZLE_NONE, LBO = 128 B, uniform SBO = 16 Dh + 64 B per 8 slots).
+__host__ __device__ __forceinline__ size_t rec16_sbo(int Dh) { return (size_t)16 * Dh + 64; }
+__host__ __device__ __forceinline__ size_t rec16_bytes(int Dh) { return 4 * rec16_sbo(Dh); }
+// half offset of chunk c8 of slot n inside its record
 __host__ __device__ __forceinline__ size_t pay16_off(int Dh, int n, int c8) {
-  return ((size_t)((n >> 3) * (Dh >> 3) + c8) * 8 + (n & 7)) * 8;
+  return (size_t)(n >> 3) * (rec16_sbo(Dh) >> 1) + ((size_t)c8 * 8 + (n & 7)) * 8;
 }
+// byte offsets of slot n's norm and id inside its record
+__host__ __device__ __forceinline__ size_t rec16_norm_off(int Dh, int n) {
+  return (size_t)(n >> 3) * rec16_sbo(Dh) + (size_t)16 * Dh + (n & 7) * 4;
+}
+__host__ __device__ __forceinline__ size_t rec16_id_off(int Dh, int n) { return rec16_norm_off(Dh, n) + 32; }
 // slab_flag bits
 constexpr uint32_t kFlagIntegral = 1u;  // every value an integer with |v| <= 2048 (exact in tf32 and fp16)
 constexpr uint32_t kFlagF16Over = 2u;   // some value has |v| > 65504 (no finite fp16 copy): scan re-ranks all
@@ -45,7 +57,7 @@ struct DevState {
   int32_t D, Dp, Dh, nlist, G, rank;  // Dh: fp16 scan copy dims (D rounded up to 16; 0 = no copy)
   int64_t cap, cap_local, num_slabs;
   float* payload;        // [num_slabs][4][Dp/4][8][4]  see pay_off(): a slab is one UMMA B core-matrix block
-  uint16_t* payload16;   // [num_slabs][4][Dh/8][8][8]  fp16 (RN) copy for the tensor-core scan, pay16_off()
+  uint16_t* payload16;   // [num_slabs] scan records of rec16_bytes(Dh): fp16 (RN) copy + norms + ids, pay16_off()
   uint32_t* slab_ids;    // [num_slabs][32] user ids (u32)
   float* slab_norm;      // [num_slabs][32] ||x||^2 (fp32), for the tensor-core distance expansion
   uint32_t* slab_flag;   // [num_slabs] bit0: every payload value is an integer with |x| <= 2048 (tf32-exact)

@@ -51,13 +51,13 @@ def test_arena_bytes_and_validation(L):
     c.shard_rank, c.shard_count = 0, 1
     n = ctypes.c_size_t()
     assert L.sivf_arena_bytes(ctypes.byref(c), ctypes.byref(n)) == 0
-    payload = 46_024 * 32 * 128 * (4 + 2)  # fp32 slabs + their fp16 scan copy
+    payload = 46_024 * 32 * 128 * (4 + 2)  # fp32 slabs + their fp16 scan records
     partial = 10_000 * 128 * 128 * 8  # per-(query, probe) top-k scratch at the max_* limits
     assert payload + partial < n.value < (payload + partial) * 1.3
     full = n.value
-    c.flags = S.CFG_NO_SCAN_COPY  # no fp16 scan copy: exactly its 46,024 x 32 x 128 x 2 bytes less
+    c.flags = S.CFG_NO_SCAN_COPY  # no scan records: exactly 46,024 x (32 x 128 x 2 + 256) bytes less
     assert L.sivf_arena_bytes(ctypes.byref(c), ctypes.byref(n)) == 0
-    assert full - n.value == 46_024 * 32 * 128 * 2
+    assert full - n.value == 46_024 * (32 * 128 * 2 + 256)  # fp16 copy + the records' norm and id copies
     c.flags = 2  # unknown flag bit
     assert L.sivf_arena_bytes(ctypes.byref(c), ctypes.byref(n)) == -1
     c.flags = 0

@@ -278,7 +278,8 @@ def test_no_scan_copy_flag():
     Q = gen.queries(0, 200)
     assert srch(g, o, Q, 10, 8) == 0 and srch(g2, o2, Q, 10, 8) == 0
     s, s2 = g.stats(), g2.stats()
-    want = 2.0 * 128 * 32 * s2["slabs_in_use"] / (s2["live"] * (4.0 * 128 + 4.0))  # 2 Dh B per slot in use
+    # per slab in use: the fp16 copy (2 Dh B per slot) + the record's norm and id copies (8 B per slot)
+    want = (2.0 * 128 + 8.0) * 32 * s2["slabs_in_use"] / (s2["live"] * (4.0 * 128 + 4.0))
     assert s["overhead_scan_copy"] == 0.0 and abs(s2["overhead_scan_copy"] - want) < 1e-12
     assert s["overhead_actual"] == s2["overhead_actual"] and g2.arena_bytes > g.arena_bytes
 

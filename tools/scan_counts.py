@@ -22,4 +22,4 @@ for split, seed in ((1, 0), (1, 1), (1, 4)):
         S.lib().sivf_debug_scnt(c.ctypes.data_as(ctypes.c_void_p), 1)
         ix.search(Q, 10, npb); torch.cuda.synchronize()
         S.lib().sivf_debug_scnt(c.ctypes.data_as(ctypes.c_void_p), 1)
-        print(f"seed {seed} split {split} nprobe {npb}: slow entries/query {c[0]/NQ:.1f} survivors/query {c[1]/NQ:.1f} insertions/query {c[2]/NQ:.1f}")
+        print(f"seed {seed} split {split} nprobe {npb}: slow entries/query {c[0]/NQ:.1f} survivors/query {c[1]/NQ:.1f} insertions/query {c[2]/NQ:.1f} (with the row bound still +inf: {c[3]/NQ:.1f})")

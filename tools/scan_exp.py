@@ -25,8 +25,14 @@ del X
 Q = torch.from_numpy(gen.queries(0, NQ)).cuda()
 configs = os.environ.get("CONFIGS", "0,1,3,35,39,43,47,63,64,16").split(",")
 splits = [int(v) for v in os.environ.get("SPLITS", "1").split(",")]
+stages = [int(v) for v in os.environ.get("STAGES", "0").split(",")]
+seeds = [int(v) for v in os.environ.get("SEEDS", "0").split(",")]
 for npb in [int(v) for v in os.environ.get("NPROBES", "32,16").split(",")]:
     for split in splits:
+      for nstg in stages:
+       ix.set_option(98, nstg)
+       for sd in seeds:
+        ix.set_option(S.OPT_SEED_SLABS, sd)
         for c in configs:
             dbg = int(c)
             ix.set_option(S.OPT_RANK_SPLIT, split)
@@ -43,5 +49,5 @@ for npb in [int(v) for v in os.environ.get("NPROBES", "32,16").split(",")]:
             p = ix.profile_read()
             ix.profile(False)
             t = {k: v[0] / v[1] for k, v in p.items() if v[1]}
-            print(f"nprobe {npb} split {split} dbg {dbg:3d}: scan {t['scan']:.4f} ms  "
+            print(f"nprobe {npb} split {split} stages {nstg} seed {sd} dbg {dbg:3d}: scan {t['scan']:.4f} ms  "
                   f"coarse {t['coarse']:.4f} invmap {t['invmap']:.4f} merge {t['merge']:.4f}", flush=True)
