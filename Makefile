@@ -64,3 +64,6 @@ prof: build/libsivf_prof.so build/libsivf_proft.so
 build/libsivf_wd.so: $(SIVF_SRCS) $(SIVF_HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -DSIVF_TC_WATCHDOG -shared -o $@ $(SIVF_SRCS) 2> build/ptxas_wd.log || (cat build/ptxas_wd.log; exit 1)
+build/libsivf_sleep.so: $(SIVF_SRCS) $(SIVF_HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -DSIVF_TC_SLEEPWAIT -shared -o $@ $(SIVF_SRCS) 2> build/ptxas_sleep.log || (cat build/ptxas_sleep.log; exit 1)

@@ -98,7 +98,8 @@ struct TcArgs {
   uint32_t* gthr;
   int phase;  // 0: every work item; 1: bucket 0 only; 2: bucket 1 only (phased scan)
   int dbg;  // experiments only (SIVF_OPT_DEBUG): bit0 skip the slow path, bit1 skip the fast path,
-            // bit2 skip the MMAs, bit3 skip the B copies, bit4 skip the A loads, bit7 no per-group bound sharing
+            // bit2 skip the MMAs, bit3 skip the B copies, bit4 skip the A loads, bit7 no per-group bound
+            // sharing, bit8 the epilogue only waits and frees, bit9 the metadata warp only forwards
 };
 
 struct ItemRec {
@@ -108,8 +109,11 @@ struct ItemRec {
   int32_t len, pad[2];
 };
 // Per stage: written by the producer (slab, bm, flag, nvalid, last) before the
-// stage's full barrier, and by the meta warp (xnmax) before meta_ready.
+// stage's full barrier, and by the meta warp (xnm, xnmax, sxmax) before
+// meta_ready.  The masked norms live here, not in the bulk-copied records: no
+// generic-proxy write ever touches the async-proxy copy destination.
 struct StageMeta {
+  float xnm[GN];     // ||x||^2 per slot, NaN where the validity bit is clear
   int32_t slab[GS];  // -1: padding position
   uint32_t bm[GS];
   uint32_t flag[GS];
@@ -161,6 +165,8 @@ __device__ __forceinline__ void scan_wait(uint64_t* bar, uint32_t phase, int tag
   }
 }
 #define MBW(bar, ph, tag) scan_wait(bar, ph, tag)
+#elif defined(SIVF_TC_SLEEPWAIT)
+#define MBW(bar, ph, tag) mbar_wait_sleep(bar, ph)
 #else
 #define MBW(bar, ph, tag) mbar_wait(bar, ph)
 #endif
@@ -426,24 +432,26 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
         const int stg = (int)(gseq % (uint32_t)nst);
         PW(0, MBW(&full[stg], (gseq / (uint32_t)nst) & 1u, 5));
         StageMeta& m = smeta[stg];
-        const int nv = m.nvalid;
-        unsigned char* sb = stage_x(stg) + rec16_norm_off(Dh, lane);
+        const int nv = (a.dbg & 512) ? 0 : m.nvalid;
+        const unsigned char* sb = stage_x(stg) + rec16_norm_off(Dh, lane);
+        float xn[GS];
+        uint32_t mx[GS];
+#pragma unroll
+        for (int j = 0; j < GS; ++j) {  // loads first, then the reductions: independent chains
+          const bool v = j < nv && ((m.bm[j] >> lane) & 1u) != 0u;
+          xn[j] = v ? *reinterpret_cast<const float*>(sb + (size_t)j * rbytes) : __int_as_float(0x7fc00000);
+        }
 #pragma unroll
         for (int j = 0; j < GS; ++j) {
-          if (j < nv) {
-            const bool v = ((m.bm[j] >> lane) & 1u) != 0u;
-            float* np = reinterpret_cast<float*>(sb + (size_t)j * rbytes);
-            const float xn = *np;
-            *np = v ? xn : __int_as_float(0x7fc00000);
-            const uint32_t mx = __reduce_max_sync(kFull, v ? __float_as_uint(fmaxf(xn, 0.f)) : 0u);
-            if (lane == 0) {
-              m.xnmax[j] = __uint_as_float(mx);
-              m.sxmax[j] = sqrtf(__uint_as_float(mx));
-            }
-          }
+          m.xnm[j * kSlot + lane] = xn[j];
+          mx[j] = __reduce_max_sync(kFull, xn[j] == xn[j] ? __float_as_uint(fmaxf(xn[j], 0.f)) : 0u);
+        }
+        if (lane < GS) {
+          const float x = __uint_as_float(lane == 0 ? mx[0] : lane == 1 ? mx[1] : lane == 2 ? mx[2] : mx[3]);
+          m.xnmax[lane] = x;
+          m.sxmax[lane] = sqrtf(x);
         }
         const int last = m.last;
-        fence_proxy_async_smem();  // generic writes of the stage ordered before its next bulk refill
         __syncwarp();
         if (lane == 0) mbar_arrive(&meta_ready[stg]);
         ++gseq;
@@ -613,12 +621,20 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           if (lane == 0 && warp == W_EPI0 + 2) TR(3, gseq, clock64());
           tc_fence_after();
           const int nv = m.nvalid;
-          if (wact && nv > 0) {
+          if (wact && nv > 0 && !(dbg & 256)) {
+#ifdef SIVF_TC_PROF
+            long long _tb = clock64();
+#endif
             const u64 ps = thr_sh[(1 - h) * TM + row];  // other set's bound, tagged with its item
             if ((uint32_t)(ps >> 32) == i) thr = fminf(thr, __uint_as_float((uint32_t)ps));
             thr = fminf(thr, gnext);  // other items of the same query (read one group ago)
             if (rv && !(dbg & 128)) gnext = __uint_as_float(__ldcg(a.gthr + qglob));
             const unsigned char* sbase = stage_x(stg);
+#ifdef SIVF_TC_PROF
+            __syncwarp();
+            if (thr == 12345.f) pw[7] += 1;  // consume thr: the wait on the bound loads is timed here
+            pw[8] += clock64() - _tb;
+#endif
             // one chunk = one slab = 32 TMEM columns of this row
             auto chunk = [&](const int j, const uint32_t(&v)[32]) {
               const unsigned char* rb = sbase + (size_t)j * rbytes;  // slab j's record
@@ -635,10 +651,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
                 E = 2.f * (2.f * eps1 * cs + eps2 * (qn + xm + 2.f * cs)) + esub * rs;
               }
               float tadj = ex ? __fsub_ru(thr, qn) : __fadd_ru(__fsub_ru(thr, qn), E);
-              // norms of slots 4 c4 .. 4 c4 + 3 (row group c4 / 2), NaN where the slot is not valid
-              auto x4 = [&](int c4) {
-                return *reinterpret_cast<const float4*>(rb + (size_t)(c4 >> 1) * sbo + (size_t)16 * Dh + (c4 & 1) * 16);
-              };
+              // norms of slots 4 c4 .. 4 c4 + 3, NaN where the slot is not valid
+              const float4* xq = reinterpret_cast<const float4*>(m.xnm + kSlot * j);
+              auto x4 = [&](int c4) { return xq[c4]; };
               float m8[8];
 #pragma unroll
               for (int c4 = 0; c4 < 8; ++c4) {
@@ -678,8 +693,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
               while (pm) {
                 const int c = __ffs(pm) - 1;
                 pm &= pm - 1;
-                const float t = fmaf(-2.f, __uint_as_float(pick32(v, c)),
-                                     *reinterpret_cast<const float*>(rb + rec16_norm_off(Dh, c)));
+                const float t = fmaf(-2.f, __uint_as_float(pick32(v, c)), m.xnm[kSlot * j + c]);
                 if (!unsafe && !(t <= tadj)) continue;  // the threshold may have tightened
                 float d;
                 if (ex) {
@@ -757,6 +771,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
         ++gseq;
         if (last) break;
       }
+#ifdef SIVF_TC_PROF
+      long long _te = clock64();
+#endif
       // merge the two sets' lists of each row: h = 1 hands its list over in smem
       if (h == 1 && rv) {
 #pragma unroll
@@ -779,6 +796,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       if (lane == 0) {
         mbar_arrive(&item_empty[slot]);
       }
+#ifdef SIVF_TC_PROF
+      pw[9] += clock64() - _te;
+#endif
     }
   }
 #ifdef SIVF_TC_PROF

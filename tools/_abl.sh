@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-CONFIGS=0,1 NPROBES=32 SPLITS=0,1,2,3,4,6,12,16 timeout 300 python tools/scan_exp.py > gpurun_out/r02n_scanexp.txt 2>&1
-cat gpurun_out/r02n_scanexp.txt
+CONFIGS=815,831,1,0 NPROBES=32 timeout 300 python tools/scan_exp.py > gpurun_out/r02s_scanexp.txt 2>&1
+SIVF_LIB_PATH=build/libsivf_sleep.so CONFIGS=815,831,1,0 NPROBES=32 timeout 300 python tools/scan_exp.py >> gpurun_out/r02s_scanexp.txt 2>&1
+cat gpurun_out/r02s_scanexp.txt
