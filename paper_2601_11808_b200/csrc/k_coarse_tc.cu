@@ -631,13 +631,17 @@ __global__ void __launch_bounds__(128) k_coarse_rerank(const float* __restrict__
 
 // Per-row selection over the stored A matrix (warp per row; lane owns the
 // columns lane + 32 i).  With E the certified bound of the file comment:
-//   U = the m-th smallest upper bound max(A + E, 0) (m = 1: the minimum; else a
-//       bisection on the fp32 bit pattern: the smallest t with #{ub <= t} >= m),
+//   U = the m-th smallest upper bound max(A + E, 0),
 //   candidates = {l : A_l - E_l <= U} (every member of the exact top-m, ties
 //       included, has lower bound <= its dist32 <= U),
 // then the canonical dist32 of each candidate and the exact top-m by
 // (dist32, l).  MODE 0: best[row] = smallest key (assignment); MODE 1:
 // probes[row][0..m) sorted.  More than CCAP candidates: every list is re-ranked.
+// U and the candidates are found on a superset S of few columns: with U' the
+// m-th smallest A and Emax >= every E_l of the row, U <= U' + Emax and every
+// candidate has A_l <= U + E_l <= U' + 2 Emax, so S = {l : A_l <= U' + 2 Emax}
+// (rounded up) holds every column that decides U and every candidate; E, the
+// bounds and U are then evaluated exactly as on the full row, on S only.
 constexpr int CCAP = 256;
 // Fused first step of the search's inverse probe map (k_search.cu k_inv_count): per
 // probe rank j of a row, one count in bucket (j >= r0) of its list; the row's k-th
@@ -669,13 +673,76 @@ __device__ unsigned long long g_selclk[2][8];
 #endif
 constexpr int SELW = 8;  // rows (warps) per block
 __host__ __device__ inline size_t select_smem_per_warp(int Dp) {
-  return (size_t)Dp * 4 + 2 * CCAP * 4 + 2 * 32 * 8;
+  return (size_t)Dp * 4 + 5 * CCAP * 4 + 2 * 32 * 8;
 }
+constexpr int QCAP = SELW * 64;  // block re-rank queue: <= 64 uncertain candidates per row
 __host__ __device__ inline size_t select_smem(int Dp, int nlist, int mode = 1) {
-  return SELW * select_smem_per_warp(Dp) + (size_t)(2 + (mode ? SELW : 0)) * nlist * 4;  // + per-warp E rows
+  (void)mode;
+  return SELW * select_smem_per_warp(Dp) + (size_t)2 * nlist * 4 + 16;
+}
+// order-preserving map of a (non-NaN) float to uint32
+__device__ __forceinline__ uint32_t fkey(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+// the m-th smallest (1 <= m <= 32) of the warp's values v0 (all lanes) and, when
+// two, v1, with 0xFFFFFFFF padding: two warp bitonic sorts and one bitonic merge
+__device__ __forceinline__ uint32_t warp_mth64(uint32_t a0, uint32_t a1, bool two, int m) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint32_t o0 = __shfl_xor_sync(kFull, a0, stride);
+      const uint32_t o1 = two ? __shfl_xor_sync(kFull, a1, stride) : 0u;
+      const bool up = (lane & size) == 0 || size == 32, lower = (lane & stride) == 0;
+      a0 = (lower == up) ? min(a0, o0) : max(a0, o0);
+      if (two) a1 = (lower == up) ? min(a1, o1) : max(a1, o1);
+    }
+  }
+  uint32_t b = two ? min(a0, __shfl_sync(kFull, a1, 31 - lane)) : a0;  // bitonic: the 32 smallest
+  if (two) {
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+      const uint32_t o = __shfl_xor_sync(kFull, b, j);
+      b = (lane & j) ? max(b, o) : min(b, o);
+    }
+  }
+  return __shfl_sync(kFull, b, m - 1);
+}
+// the (j+1)-th smallest (0 <= j < 64) of the warp's 64 values v0, v1 (0xFFFFFFFF padding):
+// a full bitonic sort of 64 (two warp sorts and a merge network across both halves)
+__device__ __forceinline__ uint32_t warp_kth64(uint32_t a0, uint32_t a1, int j) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint32_t o0 = __shfl_xor_sync(kFull, a0, stride), o1 = __shfl_xor_sync(kFull, a1, stride);
+      const bool up = (lane & size) == 0, lower = (lane & stride) == 0;
+      // a0 sorted ascending (size 32 stage: ascending), a1 descending: together bitonic
+      const bool up0 = up || size == 32, up1 = up && size != 32;
+      a0 = (lower == up0) ? min(a0, o0) : max(a0, o0);
+      a1 = (lower == up1) ? min(a1, o1) : max(a1, o1);
+    }
+  }
+  // a0 ascending, a1 descending: a bitonic sequence of 64; half-cleaner across halves
+  const uint32_t lo = min(a0, a1), hi = max(a0, a1);
+  uint32_t b0 = lo, b1 = hi;  // b0 holds the 32 smallest (bitonic), b1 the 32 largest (bitonic)
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    const uint32_t o0 = __shfl_xor_sync(kFull, b0, stride), o1 = __shfl_xor_sync(kFull, b1, stride);
+    const bool lower = (lane & stride) == 0;
+    b0 = lower ? min(b0, o0) : max(b0, o0);
+    b1 = lower ? min(b1, o1) : max(b1, o1);
+  }
+  return j < 32 ? __shfl_sync(kFull, b0, j) : __shfl_sync(kFull, b1, j - 32);
 }
 template <int NPL, int MODE>
-__global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __restrict__ mat,
+__global__ void __launch_bounds__(32 * SELW, 3) k_coarse_select(const float* __restrict__ mat,
                                                              const float* __restrict__ X, int64_t n, int D,
                                                              int nlist, int m, const float* __restrict__ xnorm,
                                                              const float* __restrict__ ccsa,
@@ -688,148 +755,215 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* csa_s = reinterpret_cast<float*>(sm_sel + SELW * select_smem_per_warp(Dp));
   float* cnb_s = csa_s + nlist;
+  uint32_t* cmax = reinterpret_cast<uint32_t*>(cnb_s + nlist);  // [2] max csa, max cnb (bits; >= 0)
+  __shared__ int q_cnt;            // block re-rank queue (MODE 1): entries (warp, list) -> dist32
+  __shared__ uint8_t q_w[QCAP];
+  __shared__ int32_t q_l[QCAP];
+  __shared__ float q_d[QCAP];
+  if (threadIdx.x < 2) cmax[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) q_cnt = 0;
+  __syncthreads();
+  uint32_t ma = 0u, mb = 0u;
   for (int c = threadIdx.x; c < nlist; c += blockDim.x) {
-    csa_s[c] = __ldg(ccsa + c);
-    cnb_s[c] = __ldg(ccnb + c);
+    const float va = __ldg(ccsa + c), vb = __ldg(ccnb + c);
+    csa_s[c] = va;
+    cnb_s[c] = vb;
+    ma = max(ma, __float_as_uint(va));
+    mb = max(mb, __float_as_uint(vb));
+  }
+  ma = __reduce_max_sync(kFull, ma);
+  mb = __reduce_max_sync(kFull, mb);
+  if (lane == 0) {
+    atomicMax(&cmax[0], ma);
+    atomicMax(&cmax[1], mb);
   }
   __syncthreads();
   const int64_t row = (int64_t)blockIdx.x * SELW + w;
-  if (row >= n) return;  // warp-uniform
-#ifdef SIVF_TC_PROF
-  long long _t0 = clock64();
-#endif
   unsigned char* base = sm_sel + (size_t)w * select_smem_per_warp(Dp);
   float* xs = reinterpret_cast<float*>(base);
   int32_t* cand = reinterpret_cast<int32_t*>(xs + Dp);
   float* capx = reinterpret_cast<float*>(cand + CCAP);  // approximate distance of each candidate
-  unsigned long long* top = reinterpret_cast<unsigned long long*>(capx + CCAP);
+  int32_t* scol = reinterpret_cast<int32_t*>(capx + CCAP);  // the superset S (columns)
+  float* clb = reinterpret_cast<float*>(scol + CCAP);       // candidate lower / upper bounds
+  float* cub = clb + CCAP;
+  unsigned long long* top = reinterpret_cast<unsigned long long*>(cub + CCAP);
   unsigned long long* tmp = top + 32;
+  const bool vec = (Dp & 3) == 0;
+  int path = 0;                 // MODE 1: 1 = batched exact re-rank of the uncertain candidates
+  int qbase = 0, nu = 0, nce = 0, ncand = 0;
+  uint32_t lbm = 0u;            // (m+1)-th smallest lower-bound key among the candidates
+  do {  // MODE 1 leaves by break (the block barriers below), MODE 0 may return
+  if (row >= n) break;  // warp-uniform
+#ifdef SIVF_TC_PROF
+  long long _t0 = clock64();
+#endif
   // lane owns the columns lane + 32 i (coalesced 128-B row segments)
   const float* arow = mat + (size_t)row * nlist;
   float A[NPL];
 #pragma unroll
   for (int i = 0; i < NPL; ++i) A[i] = lane + 32 * i < nlist ? __ldcs(arow + lane + 32 * i) : INFINITY;
   const float qn = xnorm[row], sq = sqrtf(qn), qnb = kb * qn;
-  // the certified half-width E of column lane + 32 i, computed once into the warp's
-  // shared row and read back by the later passes (only A stays in registers)
-  // (MODE 0, the argmin of an insert, makes two passes: it recomputes E inline)
-  float* e_row = cnb_s + nlist + (size_t)w * nlist;
-  if (MODE == 1) {
+  auto Ecol = [&](int c) { return fmaf(sq, csa_s[c], qnb + cnb_s[c]); };  // the per-column form
+  const float Emax = __fmaf_ru(sq, __uint_as_float(cmax[0]), __fadd_ru(qnb, __uint_as_float(cmax[1])));
+  const float* xr = X + row * (int64_t)D;
+  for (int k = lane; k < Dp; k += 32) xs[k] = k < D ? __ldg(xr + k) : 0.f;
+  const unsigned lt = (1u << lane) - 1u;
+  SELCLK(0);
+  // 1. U' = the m-th smallest A of the row (m = 1: the minimum)
+  float Up;
+  {
+    float mn = INFINITY;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) mn = fminf(mn, A[i]);
+    if (m == 1) {
+      Up = fkey_inv(__reduce_min_sync(kFull, fkey(mn)));
+    } else {
+      // >= 32 >= m values are <= the largest of the lanes' minima: compact those
+      const uint32_t hi = __reduce_max_sync(kFull, fkey(mn));
+      uint32_t* sv = reinterpret_cast<uint32_t*>(cand);  // scratch
+      int nv = 0;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) {
+        const uint32_t kk = fkey(A[i]);
+        const bool keep = kk <= hi;
+        const unsigned pm = __ballot_sync(kFull, keep);
+        const int pos = nv + __popc(pm & lt);
+        if (keep && pos < CCAP) sv[pos] = kk;
+        nv += __popc(pm);
+      }
+      __syncwarp();
+      if (nv <= 64) {
+        Up = fkey_inv(warp_mth64(lane < nv ? sv[lane] : 0xFFFFFFFFu, lane + 32 < nv ? sv[lane + 32] : 0xFFFFFFFFu,
+                                 nv > 32, m));
+      } else {
+        // bisection on the key bits over the compacted values (or the row)
+        uint32_t lo = __reduce_min_sync(kFull, fkey(mn)), h2 = hi;
+        if (nv <= CCAP) {
+          uint32_t u[CCAP / 32];
+#pragma unroll
+          for (int t = 0; t < CCAP / 32; ++t) u[t] = lane + 32 * t < nv ? sv[lane + 32 * t] : 0xFFFFFFFFu;
+          while (lo < h2) {
+            const uint32_t mid = lo + ((h2 - lo) >> 1);
+            int c = 0;
+#pragma unroll
+            for (int t = 0; t < CCAP / 32; ++t) c += u[t] <= mid ? 1 : 0;
+            if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) h2 = mid;
+            else lo = mid + 1;
+          }
+        } else {
+          while (lo < h2) {
+            const uint32_t mid = lo + ((h2 - lo) >> 1);
+            int c = 0;
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) c += fkey(A[i]) <= mid ? 1 : 0;
+            if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) h2 = mid;
+            else lo = mid + 1;
+          }
+        }
+        Up = fkey_inv(h2);
+      }
+      __syncwarp();
+    }
+  }
+  // 2. the superset S = {l : A_l <= U' + 2 Emax} (rounded up, with slack)
+  const float thr = __fadd_ru(__fadd_ru(__fadd_ru(Up, Emax), Emax), fabsf(Up) * 0x1p-20f + Emax * 0x1p-10f);
+  int ns = 0;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const bool keep = A[i] <= thr;
+    const unsigned pm = __ballot_sync(kFull, keep);
+    const int pos = ns + __popc(pm & lt);
+    if (keep && pos < CCAP) scol[pos] = lane + 32 * i;
+    ns += __popc(pm);
+  }
+  __syncwarp();
+  const bool sall = ns > CCAP;  // S too large: the whole row (the lane's register columns)
+  SELCLK(1);
+  // 3. U = the m-th smallest upper bound max(A + E, 0), over S
+  uint32_t Ub;
+  {
+    auto ub_of = [&](float a, int c) { return __float_as_uint(fmaxf(a + Ecol(c), 0.f)); };
+    if (!sall && ns <= 64) {
+      uint32_t u0 = 0xFFFFFFFFu, u1 = 0xFFFFFFFFu;
+      if (lane < ns) u0 = ub_of(__ldcs(arow + scol[lane]), scol[lane]);
+      if (lane + 32 < ns) u1 = ub_of(__ldcs(arow + scol[lane + 32]), scol[lane + 32]);
+      Ub = (m == 1) ? __reduce_min_sync(kFull, min(u0, u1)) : warp_mth64(u0, u1, ns > 32, m);
+    } else {
+      uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+      auto each = [&](auto&& f) {
+        if (sall) {
+#pragma unroll
+          for (int i = 0; i < NPL; ++i)
+            if (lane + 32 * i < nlist) f(ub_of(A[i], lane + 32 * i));
+        } else {
+          for (int t = lane; t < ns; t += 32) f(ub_of(__ldcs(arow + scol[t]), scol[t]));
+        }
+      };
+      each([&](uint32_t u) {
+        lo = min(lo, u);
+        hi = max(hi, u);
+      });
+      lo = __reduce_min_sync(kFull, lo);
+      hi = __reduce_max_sync(kFull, hi);
+      while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        int c = 0;
+        each([&](uint32_t u) { c += u <= mid ? 1 : 0; });
+        if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) hi = mid;
+        else lo = mid + 1;
+      }
+      Ub = hi;
+    }
+  }
+  SELCLK(2);
+  const float U = __uint_as_float(Ub);
+  // 4. candidates: lower bound <= U, from S
+  int nc = 0;
+  if (sall) {
 #pragma unroll
     for (int i = 0; i < NPL; ++i) {
       const int c = lane + 32 * i;
-      if (c < nlist) e_row[c] = fmaf(sq, csa_s[c], qnb + cnb_s[c]);
+      const float e = c < nlist ? Ecol(c) : 0.f;
+      const bool pass = c < nlist && A[i] - e <= U;
+      const unsigned pm = __ballot_sync(kFull, pass);
+      const int pos = nc + __popc(pm & lt);
+      if (pass && pos < CCAP) {
+        cand[pos] = c;
+        capx[pos] = fmaxf(A[i], 0.f);  // the midpoint of the band
+        clb[pos] = A[i] - e;
+        cub[pos] = fmaxf(A[i] + e, 0.f);
+      }
+      nc += __popc(pm);
     }
-    __syncwarp();
-  }
-  auto Eat = [&](int i) {
-    const int c = lane + 32 * i;
-    if (MODE == 1) return c < nlist ? e_row[c] : 0.f;
-    return c < nlist ? fmaf(sq, csa_s[c], qnb + cnb_s[c]) : 0.f;
-  };
-  auto ubat = [&](int i) { return __float_as_uint(fmaxf(A[i] + Eat(i), 0.f)); };  // +inf beyond nlist
-  const float* xr = X + row * (int64_t)D;
-  for (int k = lane; k < Dp; k += 32) xs[k] = k < D ? __ldg(xr + k) : 0.f;
-  SELCLK(0);
-  uint32_t Ub;
-  if (MODE == 0 || m == 1) {
-    uint32_t mn = 0x7F800000u;
-#pragma unroll
-    for (int i = 0; i < NPL; ++i) mn = min(mn, ubat(i));
-    Ub = __reduce_min_sync(kFull, mn);
   } else {
-    // hi = the largest of the lanes' minima: >= 32 >= m upper bounds are <= hi, so
-    // U lies among the values <= hi; those are compacted (shared memory) and the
-    // m-th smallest found by bisection on the fp32 bit pattern
-    uint32_t mn = 0x7F800000u;
-#pragma unroll
-    for (int i = 0; i < NPL; ++i) mn = min(mn, ubat(i));
-    uint32_t hi = m <= 32 ? __reduce_max_sync(kFull, mn) : 0x7F800000u;
-    uint32_t lo = __reduce_min_sync(kFull, mn);
-    uint32_t* sv = reinterpret_cast<uint32_t*>(cand);  // scratch, reused for candidates below
-    int ns = 0;
-    const unsigned ltm = (1u << lane) - 1u;
-#pragma unroll
-    for (int i = 0; i < NPL; ++i) {
-      const uint32_t ub = ubat(i);
-      const bool keep = ub <= hi;
-      const unsigned pm = __ballot_sync(kFull, keep);
-      const int pos = ns + __popc(pm & ltm);
-      if (keep && pos < CCAP) sv[pos] = ub;
-      ns += __popc(pm);
+    for (int t0 = 0; t0 < ns; t0 += 32) {
+      const int t = t0 + lane;
+      int c = 0;
+      float a = INFINITY;
+      if (t < ns) {
+        c = scol[t];
+        a = __ldcs(arow + c);
+      }
+      const float e = t < ns ? Ecol(c) : 0.f;
+      const bool pass = t < ns && a - e <= U;
+      const unsigned pm = __ballot_sync(kFull, pass);
+      const int pos = nc + __popc(pm & lt);
+      if (pass && pos < CCAP) {
+        cand[pos] = c;
+        capx[pos] = fmaxf(a, 0.f);
+        clb[pos] = a - e;
+        cub[pos] = fmaxf(a + e, 0.f);
+      }
+      nc += __popc(pm);
     }
-    __syncwarp();
-    if (ns <= 64 && m <= 32) {
-      // <= 64 values: the m-th smallest (m <= 32) by sorting, not bisection: two warp
-      // bitonic sorts, the 32 smallest of both by one bitonic merge
-      uint32_t a0 = lane < ns ? sv[lane] : 0xFFFFFFFFu;
-      uint32_t a1 = lane + 32 < ns ? sv[lane + 32] : 0xFFFFFFFFu;
-#pragma unroll
-      for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          const uint32_t o0 = __shfl_xor_sync(kFull, a0, stride), o1 = __shfl_xor_sync(kFull, a1, stride);
-          const bool up = (lane & size) == 0 || size == 32, lower = (lane & stride) == 0;
-          a0 = (lower == up) ? min(a0, o0) : max(a0, o0);
-          a1 = (lower == up) ? min(a1, o1) : max(a1, o1);
-        }
-      }
-      uint32_t b = min(a0, __shfl_sync(kFull, a1, 31 - lane));  // bitonic: the 32 smallest
-#pragma unroll
-      for (int j = 16; j > 0; j >>= 1) {
-        const uint32_t o = __shfl_xor_sync(kFull, b, j);
-        b = (lane & j) ? max(b, o) : min(b, o);
-      }
-      lo = hi = __shfl_sync(kFull, b, m - 1);
-    } else if (ns <= CCAP) {
-      uint32_t u[CCAP / 32];
-#pragma unroll
-      for (int t = 0; t < CCAP / 32; ++t) u[t] = lane + 32 * t < ns ? sv[lane + 32 * t] : 0xFFFFFFFFu;
-      while (lo < hi) {
-        const uint32_t mid = lo + ((hi - lo) >> 1);
-        int c = 0;
-#pragma unroll
-        for (int t = 0; t < CCAP / 32; ++t) c += u[t] <= mid ? 1 : 0;
-        if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) hi = mid;
-        else lo = mid + 1;
-      }
-    } else {
-      while (lo < hi) {
-        const uint32_t mid = lo + ((hi - lo) >> 1);
-        int c = 0;
-#pragma unroll
-        for (int i = 0; i < NPL; ++i) c += ubat(i) <= mid ? 1 : 0;
-        if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) hi = mid;
-        else lo = mid + 1;
-      }
-    }
-    __syncwarp();
-    Ub = hi;
-  }
-  SELCLK(1);
-  const float U = __uint_as_float(Ub);
-  // candidates: lower bound <= U (columns beyond nlist have A = +inf)
-  int nc = 0;
-  const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const bool pass = A[i] - Eat(i) <= U;  // lower bound (+inf beyond nlist)
-    const unsigned pm = __ballot_sync(kFull, pass);
-    const int pos = nc + __popc(pm & lt);
-    if (pass && pos < CCAP) {
-      cand[pos] = lane + 32 * i;
-      capx[pos] = fmaxf(A[i], 0.f);  // the midpoint of the band
-    }
-    nc += __popc(pm);
   }
   __syncwarp();
 #ifdef SIVF_TC_PROF
   if (lane == 0) atomicAdd(&g_selhist[MODE][nc < 63 ? nc : 63], 1u);
 #endif
-  SELCLK(2);
+  SELCLK(3);
   const bool all = nc > CCAP;
   const int total = all ? nlist : nc;
-  const bool vec = (Dp & 3) == 0;
   unsigned long long bestk = ~0ull;
   if (MODE == 0 && nc == 1 && !need_dist) {
     // a single candidate is certainly the argmin; the insert path needs only the list
@@ -845,35 +979,40 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
       probes[row * probes_ld + lane] = (int32_t)key_id(k0);
       inv_count_row(ic, nlist, row, lane, (int32_t)key_id(k0));
     }
-    SELCLK(3);
-    return;
+    SELCLK(4);
+    break;
   }
   if (MODE == 1 && total <= 64) {
-    // <= 64 candidates: exact keys, two warp sorts and one bitonic merge
-    unsigned long long k0 = kPadKey, k1 = kPadKey;
-    if (lane < total) {
-      const int l0 = cand[lane], l1 = lane + 32 < total ? cand[lane + 32] : l0;
-      float d0, d1;
-      dist32_rows2(xs, C + (size_t)l0 * Dp, C + (size_t)l1 * Dp, D, vec, d0, d1);
-      k0 = make_key(d0, (uint32_t)l0);
-      if (lane + 32 < total) k1 = make_key(d1, (uint32_t)l1);
+    // m < nc <= 64 candidates.  Candidate t is certainly in the top-m when fewer
+    // than m others can reach it: ub_t < L, L the (m+1)-th smallest lower bound
+    // (every list with lb <= ub_t is then among the m smallest lower bounds, t
+    // included).  Only the other (uncertain) candidates need the canonical dist32;
+    // they go to the block's re-rank queue (their exact keys pick the remaining
+    // m - #certain slots after the block barrier)
+    const uint32_t k0 = lane < nc ? fkey(clb[lane]) : 0xFFFFFFFFu;
+    const uint32_t k1 = lane + 32 < nc ? fkey(clb[lane + 32]) : 0xFFFFFFFFu;
+    lbm = warp_kth64(k0, k1, m);  // 0-based m: the (m+1)-th smallest
+    const bool u0 = lane < nc && !(fkey(cub[lane]) < lbm);
+    const bool u1 = lane + 32 < nc && !(fkey(cub[lane + 32]) < lbm);
+    const unsigned b0 = __ballot_sync(kFull, u0), b1 = __ballot_sync(kFull, u1);
+    nu = __popc(b0) + __popc(b1);
+    nce = nc - nu;
+    ncand = nc;
+    if (lane == 0) qbase = atomicAdd(&q_cnt, nu);
+    qbase = __shfl_sync(kFull, qbase, 0);
+    if (u0) {
+      const int e = qbase + __popc(b0 & lt);
+      q_w[e] = (uint8_t)w;
+      q_l[e] = cand[lane];
     }
-    k0 = warp_sort32(k0);
-    if (total > 32) {
-      k1 = warp_sort32(k1);
-      k0 = umin64(k0, __shfl_sync(kFull, k1, 31 - lane));  // bitonic: the 32 smallest of both
-#pragma unroll
-      for (int j = 16; j > 0; j >>= 1) {
-        const unsigned long long o = __shfl_xor_sync(kFull, k0, j);
-        k0 = (lane & j) ? umax64(k0, o) : umin64(k0, o);
-      }
+    if (u1) {
+      const int e = qbase + __popc(b0) + __popc(b1 & lt);
+      q_w[e] = (uint8_t)w;
+      q_l[e] = cand[lane + 32];
     }
-    if (lane < m) {
-      probes[row * probes_ld + lane] = (int32_t)key_id(k0);
-      inv_count_row(ic, nlist, row, lane, (int32_t)key_id(k0));
-    }
-    SELCLK(4);
-    return;
+    path = 1;
+    SELCLK(5);
+    break;
   }
   if (MODE == 1) warp_topk_init(top, m);
   for (int i0 = 0; i0 < total; i0 += 32) {
@@ -894,6 +1033,57 @@ __global__ void __launch_bounds__(32 * SELW, 4) k_coarse_select(const float* __r
     for (int j = lane; j < m; j += 32) {
       probes[row * probes_ld + j] = (int32_t)key_id(top[j]);
       inv_count_row(ic, nlist, row, j, (int32_t)key_id(top[j]));
+    }
+  }
+  } while (0);
+  if (MODE == 1) {
+    __syncthreads();  // the queue is complete
+    const int qn = q_cnt;
+    for (int e = threadIdx.x; e < qn; e += blockDim.x) {
+      const float* xw = reinterpret_cast<const float*>(sm_sel + (size_t)q_w[e] * select_smem_per_warp(Dp));
+      q_d[e] = dist32_rows(xw, C + (size_t)q_l[e] * Dp, D, vec);
+    }
+    __syncthreads();
+    if (path == 1) {
+      // the m - nce best uncertain by (dist32, list), then all m probes sorted
+      // (certain ones by their approximate distance: the order only steers the scan)
+      unsigned long long e0 = lane < nu ? make_key(q_d[qbase + lane], (uint32_t)q_l[qbase + lane]) : kPadKey;
+      unsigned long long e1 = lane + 32 < nu ? make_key(q_d[qbase + lane + 32], (uint32_t)q_l[qbase + lane + 32]) : kPadKey;
+      e0 = warp_sort32(e0);
+      if (nu > 32) {
+        e1 = warp_sort32(e1);
+        e0 = umin64(e0, __shfl_sync(kFull, e1, 31 - lane));
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+          const unsigned long long o = __shfl_xor_sync(kFull, e0, j);
+          e0 = (lane & j) ? umax64(e0, o) : umin64(e0, o);
+        }
+      }
+      // lane j < m - nce holds the j-th chosen uncertain key; the certain ones are
+      // compacted behind them
+      unsigned long long fk = lane < m - nce ? e0 : kPadKey;
+      int pos = m - nce;
+      const unsigned lt = (1u << lane) - 1u;
+      for (int t0 = 0; t0 < ncand; t0 += 32) {
+        const int t = t0 + lane;
+        const bool cert = t < ncand && fkey(cub[t]) < lbm;
+        const unsigned bm = __ballot_sync(kFull, cert);
+        const int p = pos + __popc(bm & lt);
+        // route the certain key to lane p (p < m <= 32)
+        const unsigned long long ck = cert ? make_key(capx[t], (uint32_t)cand[t]) : kPadKey;
+        for (int src = 0; src < 32; ++src) {
+          if (!((bm >> src) & 1u)) continue;
+          const unsigned long long v = __shfl_sync(kFull, ck, src);
+          const int ps = __shfl_sync(kFull, p, src);
+          if (lane == ps) fk = v;
+        }
+        pos += __popc(bm);
+      }
+      fk = warp_sort32(fk);
+      if (lane < m) {
+        probes[row * probes_ld + lane] = (int32_t)key_id(fk);
+        inv_count_row(ic, nlist, row, lane, (int32_t)key_id(fk));
+      }
     }
   }
 }

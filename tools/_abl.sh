@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-CONFIGS=815,831,1,0 NPROBES=32 timeout 300 python tools/scan_exp.py > gpurun_out/r02s_scanexp.txt 2>&1
-SIVF_LIB_PATH=build/libsivf_sleep.so CONFIGS=815,831,1,0 NPROBES=32 timeout 300 python tools/scan_exp.py >> gpurun_out/r02s_scanexp.txt 2>&1
-cat gpurun_out/r02s_scanexp.txt
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/r02w_pytest.txt 2>&1; tail -2 gpurun_out/r02w_pytest.txt
+HIST=1 SIVF_LIB_PATH=build/libsivf_prof.so timeout 300 python tools/coarse_probe.py 2>&1 | grep -v "^blk" | tail -3
+timeout 300 python tools/coarse_probe.py 2>&1 | grep SEL
+NPROBE=8 timeout 300 python tools/coarse_probe.py 2>&1 | grep SEL

@@ -40,5 +40,5 @@ if os.environ.get("HIST"):
         print("mode", mode, "nc histogram", nz)
     c = np.zeros((2, 8), np.uint64)
     S.lib().sivf_debug_selclk(c.ctypes.data_as(ctypes.c_void_p))
-    print("clk mode1 [loads, bisect, compact, approx-sort path, exact<=64 path]:", c[1][:5].tolist())
-    print("clk mode0:", c[0][:5].tolist())
+    print("clk mode1 [loads, U', superset+U, candidates, approx-sort path, exact<=64 path]:", c[1][:6].tolist())
+    print("clk mode0:", c[0][:6].tolist())
