@@ -142,24 +142,57 @@ def dist_env():
 
 
 # ----------------------------------------------------------------------------- reference arm
-def oracle_sample(n_cores: int, budget_steps: int, warmup: int, log):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_sample(n_cores: int, budget_steps: int, warmup: int, log, centroids=None):
     """Time the CPU oracle on a bounded sample of the step: 1/10 of the inserts
     and deletes and 1/100 of the queries per sampled step, on a 1M-vector
-    oracle index; the step time is scaled back to the full step."""
+    oracle index; the step time is scaled back to the full step (labelled
+    "extrapolated" in the line).  The timed samples run on ONE thread pinned to
+    one host core (n_cores = 1); the untimed 1M build uses every core.  The
+    quantizer is the GPU-trained one when given (the same configuration as the
+    GPU arm), else a 20-iteration oracle k-means on the same training sample."""
     import oracle as O
     from datagen import Generator, sift_shape
 
-    O.set_threads(n_cores)
+    O.set_threads(os.cpu_count() or 1)
     gen = Generator(sift_shape(seed=SEED))
     t0 = time.time()
-    Xt = gen.train(N_TRAIN // 4)
-    C = O.kmeans(Xt, NLIST, 2, SEED)  # quantizer for the oracle index (setup, untimed)
+    if centroids is not None:
+        C = np.ascontiguousarray(centroids, dtype=np.float32)
+    else:
+        C = O.kmeans(gen.train(N_TRAIN), NLIST, N_ITER, SEED)  # setup, untimed
     ref = O.Index(DIM, NLIST, N_BASE + (budget_steps + warmup + 2) * BATCH)
     ref.set_centroids(C)
     for b0 in range(0, N_BASE, 100_000):
         ref.insert(np.arange(b0, b0 + 100_000), gen.range(b0, 100_000))
-    log(f"oracle build {time.time() - t0:.1f}s on {n_cores} threads")
+    log(f"oracle build {time.time() - t0:.1f}s on {os.cpu_count()} threads (untimed setup)")
+    O.set_threads(n_cores)
+    aff = None
+    if n_cores == 1 and hasattr(os, "sched_setaffinity"):
+        aff = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {min(aff)})  # the timed oracle runs on one pinned core
     si, sd, sq = BATCH // 10, BATCH // 10, NQ // 100
+    times = []
+    try:
+        times = _oracle_steps(ref, gen, si, sd, sq, warmup, budget_steps)
+    finally:
+        if aff is not None:
+            os.sched_setaffinity(0, aff)
+        O.set_threads(os.cpu_count() or 1)
+    return times
+
+
+def _oracle_steps(ref, gen, si, sd, sq, warmup, budget_steps):
     times = []
     for t in range(warmup + budget_steps):
         new = np.arange(N_BASE + t * si, N_BASE + (t + 1) * si)
@@ -178,7 +211,7 @@ def oracle_sample(n_cores: int, budget_steps: int, warmup: int, log):
         if t >= warmup:
             full = (b - a) * (BATCH / si) + (c - b) * (BATCH / sd) + (d - c) * (NQ / sq) + (e - d)
             times.append({"insert_1k": b - a, "delete_1k": c - b, "search_100q": d - c, "reclaim": e - d,
-                          "full_step_s": full})
+                          "sample_step_s": e - a, "full_step_s": full})
     return times
 
 
@@ -186,21 +219,25 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    n_cores = os.cpu_count() or 1
+    n_cores = 1
     log = lambda m: print(f"[bench:reference] {m}", file=sys.stderr, flush=True)
     steps = max(1, min(args.steps, 5))
     times = oracle_sample(n_cores, steps, min(args.warmup, 1), log)
     full = [t["full_step_s"] for t in times]
     mean = statistics.mean(full)
     value = 1.0 / mean
-    sample = ("per step: 1k inserts + 1k deletes + 100 queries (k=10, nprobe=32) + reclaim on a 1M-vector oracle "
-              "index, scaled x10/x10/x100 to the full 10k/10k/10k step")
+    sample = ("per timed step: 1k inserts + 1k deletes + 100 queries (k=10, nprobe=32) + reclaim on a 1M-vector "
+              "oracle index (one thread pinned to one core); value and ms_per_step are EXTRAPOLATED x10/x10/x100 "
+              "to the full 10k/10k/10k step (sample_ms_per_step is the measured time of the sampled step)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus,
         "steps": len(full), "warmup": min(args.warmup, 1), "ms_per_step": mean * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "oracle": "oracle/ (plain C++17, -O2 -ffp-contract=off)"},
-        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": n_cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": n_cores, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model(), "extrapolated": True},
+        "sample_ms_per_step": statistics.mean(t["sample_step_s"] for t in times) * 1e3,
+        "extrapolated": True,
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "breakdown_s": {k: statistics.mean(t[k] for t in times) for k in times[0]},
         "metrics": {"inserts_per_s": BATCH / statistics.mean(t["insert_1k"] * BATCH / (BATCH // 10) for t in times),
@@ -526,17 +563,46 @@ def run_sivf(args):
         "merge (hbm, nprobe*k*8 + k*12 B/query)": hfrac((NPROBE * K * 8.0 + K * 12.0) * NQ, ph_ms["merge"]),
     }
     share = {p: (ph_ms[p] / ms_per_step if ms_per_step else None) for p in ph_ms}
+    # latency roofline of the small-batch ops (their HBM fractions above are tiny: they are
+    # launch- and dependent-load-bound, not bandwidth-bound)
+    lat = None
+    if G == 1:
+        fl = latency_floors(S, dev, log)
+        hop_us = fl["dram_dependent_load_ns"] / 1e3
+        k_step = launches / Kst if Kst else 0
+        # the phase timers bracket ops inside a busy stream: the floor of one kernel there is
+        # empty_launch_busy_stream_us (events included)
+        floor_del = fl["empty_launch_busy_stream_us"] + 2 * hop_us  # ATT read -> atomicAnd on the bitmap word
+        n_ins = 9  # claim, rows_tiles, gemm, select, chunk_rank, chunk_prefix, reserve, dir_update, append
+        floor_ins = fl["empty_launch_busy_stream_us"] + (n_ins - 1) * fl["launch_in_stream_us"] + n_ins * hop_us
+        floor_step = fl["graph_replay_1_kernel_us"] + (k_step - 1) * fl["graph_node_us"] + k_step * hop_us
+        meas_ins = (ph_ms["assign"] + ph_ms["append"]) * 1e3
+        lat = {"floors": fl,
+               "delete_10k": {"measured_us": ph_ms["delete"] * 1e3, "floor_us": floor_del,
+                              "frac": floor_del / (ph_ms["delete"] * 1e3) if ph_ms["delete"] else None,
+                              "floor": "one launch + 2 dependent DRAM loads (ATT -> bitmap atomicAnd)"},
+               "insert_10k": {"measured_us": meas_ins, "floor_us": floor_ins,
+                              "frac": floor_ins / meas_ins if meas_ins else None,
+                              "floor": f"{n_ins} dependent kernels (launch floor each) + one dependent DRAM load each"},
+               "step_graph": {"measured_us": ms_per_step * 1e3, "floor_us": floor_step,
+                              "frac": floor_step / (ms_per_step * 1e3), "kernels_per_step": k_step,
+                              "floor": "one graph replay of the step's kernel chain (per-node floor) + one "
+                                       "dependent DRAM load per kernel"}}
+        roofline["latency"] = lat
 
     # ---------------- cpu baseline (oracle, rank 0, N=1 only)
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu:
-        n_cores = os.cpu_count() or 1
+        n_cores = 1
         try:
-            times = oracle_sample(n_cores, 2, 0, log)
+            times = oracle_sample(n_cores, 2, 0, log, centroids=ix.get_centroids().cpu().numpy())
             mean = statistics.mean(t["full_step_s"] for t in times)
             cpu = {"value": 1.0 / mean, "unit": "steps/s", "cores": n_cores, "kind": "oracle",
-                   "sample": "2 sampled steps: 1k inserts + 1k deletes + 100 queries on a 1M oracle index, "
-                             "scaled x10/x10/x100 to the full step",
+                   "sample": "2 sampled steps: 1k inserts + 1k deletes + 100 queries on a 1M oracle index with the "
+                             "GPU-trained quantizer, one thread pinned to one core; EXTRAPOLATED x10/x10/x100 to the "
+                             "full step",
+                   "extrapolated": True, "cpu_model": cpu_model(),
+                   "sample_step_ms": statistics.mean(t["sample_step_s"] for t in times) * 1e3,
                    "step_ms": mean * 1e3}
         except Exception as e:  # the baseline must not kill the GPU line
             cpu = {"value": None, "unit": "steps/s", "cores": n_cores, "kind": "oracle", "sample": f"failed: {e}"}
@@ -606,6 +672,76 @@ def _ev():
     import torch
 
     return torch.cuda.Event(enable_timing=True)
+
+
+def latency_floors(S, dev, log):
+    """SURVEY §8(d) "Latency roofline for small batches": the floors a small-batch op cannot
+    beat, measured on this GPU with CUDA events: one empty kernel bracketed by events on an
+    idle stream, and on a busy stream (between two runs of 50 back-to-back launches: how the
+    phase timers see one kernel inside a step), the per-launch time of 200 back-to-back empty
+    kernels, one CUDA-graph replay of one empty kernel and the per-node time of a replayed
+    20-kernel chain, and the dependent-load latency (one thread chasing a random single-cycle
+    permutation: 1 GB, far beyond the 126 MB L2 = DRAM; 4 MB = L2)."""
+    import torch
+
+    def med_ms(fn, reps=30):
+        out = []
+        for _ in range(reps):
+            a, b = _ev(), _ev()
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            out.append(a.elapsed_time(b))
+        return statistics.median(out)
+
+    S.probe_launch(10)
+    torch.cuda.synchronize()
+    one = med_ms(lambda: S.probe_launch(1))
+    many = med_ms(lambda: S.probe_launch(200), reps=10) / 200
+    busy = []
+    for _ in range(30):
+        a, b = _ev(), _ev()
+        S.probe_launch(50)
+        a.record()
+        S.probe_launch(1)
+        b.record()
+        S.probe_launch(50)
+        torch.cuda.synchronize()
+        busy.append(a.elapsed_time(b))
+    busy = statistics.median(busy)
+    g1, g20 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g1, stream=side):
+            S.probe_launch(1)
+        with torch.cuda.graph(g20, stream=side):
+            S.probe_launch(20)
+    torch.cuda.synchronize()
+    g1.replay()
+    g20.replay()
+    torch.cuda.synchronize()
+    rep1 = med_ms(g1.replay)
+    rep20 = med_ms(g20.replay)
+    out = torch.zeros(1, dtype=torch.int32, device=dev)
+    hops = {}
+    for name, n in (("dram", 256 << 20), ("l2", 1 << 20)):
+        perm = torch.randperm(n, device=dev, dtype=torch.int64)
+        nxt = torch.empty(n, dtype=torch.int32, device=dev)
+        nxt[perm] = torch.roll(perm, -1).to(torch.int32)
+        del perm
+        S.probe_chase(nxt, 1000, out)
+        torch.cuda.synchronize()
+        t = med_ms(lambda: S.probe_chase(nxt, 4000, out), reps=5) - med_ms(lambda: S.probe_chase(nxt, 0, out), reps=5)
+        hops[name] = t * 1e6 / 4000  # ns per dependent load
+        del nxt
+    torch.cuda.empty_cache()
+    res = {"empty_launch_us": one * 1e3, "empty_launch_busy_stream_us": busy * 1e3,
+           "launch_in_stream_us": many * 1e3, "graph_replay_1_kernel_us": rep1 * 1e3,
+           "graph_node_us": (rep20 - rep1) / 19 * 1e3, "dram_dependent_load_ns": hops["dram"],
+           "l2_dependent_load_ns": hops["l2"]}
+    log("latency floors: " + ", ".join(f"{k} {v:.2f}" for k, v in res.items()))
+    return res
 
 
 def leg_window(S, dev, C, steps, log):
@@ -691,7 +827,7 @@ def leg_gist(S, dev, log):
 
     N, D, KG = 1_000_000, 960, 100
     gen = Generator(gist_shape())
-    reps = 30
+    reps = 61
     cap = N + (reps + 2) * BATCH
     ix = S.Index(D, NLIST, cap, S.num_slabs_for(N + (reps + 2) * BATCH, NLIST), max_batch=65536, max_queries=NQ,
                  max_k=KG, max_nprobe=64, max_train=N_TRAIN, seed=0x6157, device=dev)
@@ -740,6 +876,7 @@ def leg_gist(S, dev, log):
     # mutation latencies: 30 delete batches of 10k random live ids, 30 insert batches of 10k new ids
     rng = np.random.default_rng(0x6157)
     perm = torch.from_numpy(rng.permutation(N)[: reps * BATCH].astype(np.int64)).to(dev)
+    Xr = X[: BATCH].clone()  # re-inserted payload (new ids): the insert timing does not depend on values
     del_ms, ins_ms = [], []
     for r in range(reps):
         a, b = _ev(), _ev()
@@ -748,7 +885,7 @@ def leg_gist(S, dev, log):
         b.record()
         c, d = _ev(), _ev()
         c.record()
-        ix.insert(ids[N + r * BATCH:N + (r + 1) * BATCH], X[r * BATCH:(r + 1) * BATCH])
+        ix.insert(ids[N + r * BATCH:N + (r + 1) * BATCH], Xr)
         d.record()
         del_ms.append((a, b))
         ins_ms.append((c, d))
@@ -759,8 +896,10 @@ def leg_gist(S, dev, log):
     assert st["live"] == N and st["device_errors"] == 0, st
     res = {"workload": "BASELINE configs[2]: GIST1M-shaped 1M x 960 fp32, nlist=1024 (GPU-trained, 262144 samples, "
                        "20 iters)",
-           "delete_10k_ms_p50": pct(del_ms, 50), "delete_10k_ms_p99": pct(del_ms, 99),
-           "deletes_per_s": BATCH / (pct(del_ms, 50) / 1e3),
+           # the first call of the leg is reported apart (cold: first touch of the delete path)
+           "delete_10k_ms_p50": pct(del_ms[1:], 50), "delete_10k_ms_p99": pct(del_ms[1:], 99),
+           "delete_10k_first_call_ms": del_ms[0], "delete_samples": len(del_ms) - 1,
+           "deletes_per_s": BATCH / (pct(del_ms[1:], 50) / 1e3),
            "insert_10k_ms_p50": pct(ins_ms, 50), "insert_10k_ms_p99": pct(ins_ms, 99),
            "inserts_per_s_10k_batches": BATCH / (pct(ins_ms, 50) / 1e3),
            "inserts_per_s_bulk_64k_batches": build_rate,
@@ -912,9 +1051,113 @@ def leg_h(S, dev, log, G, rank, pg, n_total):
            "recall_truth": f"exact top-10 of {NGT} queries (fp32 GEMM over every generated batch)",
            "scaling": "strong (the global index is fixed; each rank holds n/G)"}
     log(f"H: qps@32 {sweep[32]['qps']:.0f} r={sweep[32]['recall10']:.3f}; delete80k {del_ms:.3f} ms")
+    Ch = ix.get_centroids()
+    base = h_phase_ms(ix, Qg)
     del ix
     torch.cuda.empty_cache()
+    if G == 1:
+        res["projection"] = h_projection(S, dev, log, gen, Ch, Qg, n_total, base, sweep[32]["ms"])
     return res
+
+
+def h_phase_ms(ix, Qg, reps=3):
+    """Per-phase device times of a search of Qg (k=10, nprobe=32) on ix, launched directly
+    with the library's phase events."""
+    import torch
+
+    ix.search(Qg, K, NPROBE)
+    torch.cuda.synchronize()
+    ix.profile(True)
+    ix.profile_read()
+    for _ in range(reps):
+        ix.search(Qg, K, NPROBE)
+    torch.cuda.synchronize()
+    p = ix.profile_read()
+    ix.profile(False)
+    return {k: v[0] / v[1] for k, v in p.items() if v[1]}
+
+
+def h_projection(S, dev, log, gen, C, Qg, n_total, base, base_ms, nvlink_gbs=400.0, coll_us=20.0):
+    """BASELINE configs[4] on one GPU: for G in {2, 4, 8}, shard 0 of the G-way id sharding
+    (owner = id mod G, n/G vectors, the replicated quantizer) is built and searched here, one
+    after another; every shard holds a statistically identical 1/G of the ids.  Measured per
+    shard: build rate and the search phases; the merge of G per-shard top-k lists
+    (sivf_merge_topk) is measured on [G][nq][k] inputs.  PROJECTED G-GPU search time = shard
+    search + all-gather (modelled: bytes / nvlink_gbs + coll_us per collective, NCCL all-gather
+    over NVLink 5; no second GPU here) + merge; the replicated coarse step is the Amdahl term."""
+    import torch
+
+    from datagen import TRAIN_BASE  # noqa: F401  (same generator family as the H leg)
+
+    NLH = C.shape[0]
+    out = {"method": "PROJECTION from measured single-shard runs on one B200 (no multi-GPU measurement): "
+                     "T(G) = shard search (measured) + all-gather (model) + merge (measured)",
+           "allgather_model": {"gbs": nvlink_gbs, "latency_us_per_collective": coll_us, "collectives": 2},
+           "G1": {"search_ms": base_ms, "phases_ms": base}}
+    for Gp in (2, 4, 8):
+        local_n = (n_total + Gp - 1) // Gp
+        ix = S.Index(DIM, NLH, n_total + 64, S.num_slabs_for(local_n + 1, NLH), max_batch=1 << 20,
+                     max_queries=Qg.shape[0], max_k=K, max_nprobe=128, shard_rank=0, shard_count=Gp, seed=0x100A,
+                     device=dev)
+        ix.set_centroids(C)
+        B = 1 << 20
+        Xb = torch.empty(B, DIM, dtype=torch.float32, device=dev)
+        ins_ms = 0.0
+        for j0 in range(0, local_n, B):
+            nb = min(B, local_n - j0)
+            gen.range_into(Xb[:nb], j0 * Gp, Gp)  # ids 0, G, 2G, ... (shard 0)
+            ids = Gp * torch.arange(j0, j0 + nb, device=dev, dtype=torch.int64)
+            a, b = _ev(), _ev()
+            a.record()
+            ix.insert(ids, Xb[:nb])
+            b.record()
+            b.synchronize()
+            ins_ms += a.elapsed_time(b)
+        del Xb
+        st = ix.stats()
+        assert st["live"] == local_n and st["device_errors"] == 0, st
+        for _ in range(2):
+            ix.search(Qg, K, NPROBE)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(3):
+            a, b = _ev(), _ev()
+            a.record()
+            d, i = ix.search(Qg, K, NPROBE)
+            b.record()
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        shard_ms = statistics.median(times)
+        ph = h_phase_ms(ix, Qg)
+        del ix
+        torch.cuda.empty_cache()
+        nq = Qg.shape[0]
+        gd = d[None].expand(Gp, nq, K).contiguous()
+        gi = i[None].expand(Gp, nq, K).contiguous()
+        S.merge_topk(gd, gi)
+        torch.cuda.synchronize()
+        mt = []
+        for _ in range(5):
+            a, b = _ev(), _ev()
+            a.record()
+            S.merge_topk(gd, gi)
+            b.record()
+            torch.cuda.synchronize()
+            mt.append(a.elapsed_time(b))
+        merge_ms = statistics.median(mt)
+        ag_bytes = Gp * nq * K * (4 + 8)  # gathered per rank: dist f32 + id i64 of every shard
+        ag_ms = (ag_bytes * (Gp - 1) / Gp) / (nvlink_gbs * 1e9) * 1e3 + 2 * coll_us / 1e3
+        t_ms = shard_ms + ag_ms + merge_ms
+        out[f"G{Gp}"] = {"local_n": local_n, "build_inserts_per_s_shard": local_n / (ins_ms / 1e3),
+                         "search_ms_shard": shard_ms, "phases_ms_shard": ph, "merge_ms": merge_ms,
+                         "allgather_bytes_per_rank": ag_bytes, "allgather_ms_model": ag_ms,
+                         "projected_search_ms": t_ms, "projected_qps": nq / (t_ms / 1e3),
+                         "projected_speedup_vs_G1": base_ms / t_ms,
+                         "amdahl_coarse_share": ph.get("coarse", 0.0) / t_ms}
+        log(f"H projection G={Gp}: shard search {shard_ms:.3f} ms (coarse {ph.get('coarse', 0):.3f}, scan "
+            f"{ph.get('scan', 0):.3f}), merge {merge_ms:.3f}, all-gather model {ag_ms:.3f} -> projected "
+            f"{nq / (t_ms / 1e3) / 1e6:.2f}M QPS, x{base_ms / t_ms:.2f} vs G=1")
+    return out
 
 
 def h_oracle_sample(ix, dev, dgen, local_n, G, rank, Qg, log, n_ids=10_000, n_q=100):

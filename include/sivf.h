@@ -188,6 +188,20 @@ int64_t sivf_local_capacity(sivf_index ix);
 /* Number of kernel launches this handle has enqueued so far (bench bookkeeping). */
 int64_t sivf_launch_count(sivf_index ix);
 
+/* Latency floors for measurement (bench.py roofline.latency; SURVEY §8(d)
+ * "Latency roofline for small batches"); neither touches an index.
+ *   sivf_probe_launch: enqueues n (>= 1) launches of an empty kernel on stream
+ *     (the per-launch floor of a stream of dependent kernels).
+ *   sivf_probe_chase: one thread follows `hops` dependent 4-byte loads through
+ *     the caller's int32 array d_next[0..n) (device memory; a single cycle that
+ *     the caller lays out, larger than L2 for DRAM latency) starting at index 0,
+ *     and stores the final index to *d_out (device pointer): hops x the
+ *     dependent-load latency, the floor of an op whose work is a chain of
+ *     dependent reads (delete: ATT -> bitmap).
+ * Both return SIVF_E_INVALID_ARG on bad arguments (nothing enqueued). */
+sivf_rc sivf_probe_launch(int32_t n, sivf_stream_t stream);
+sivf_rc sivf_probe_chase(const int32_t* d_next, int64_t n, int32_t hops, int32_t* d_out, sivf_stream_t stream);
+
 /* Phase timing for measurement (bench.py roofline): when enabled, every
  * phase below is bracketed by CUDA events recorded on the call's stream.
  * sivf_profile_read synchronises on the recorded events, adds their elapsed

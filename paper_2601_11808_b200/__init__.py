@@ -75,6 +75,8 @@ EXPORTS = {
     "sivf_stats": (_i32, [_P, ctypes.POINTER(Stats), _P]),
     "sivf_local_capacity": (_i64, [_P]),
     "sivf_launch_count": (_i64, [_P]),
+    "sivf_probe_launch": (_i32, [ctypes.c_int32, _P]),
+    "sivf_probe_chase": (_i32, [_P, ctypes.c_int64, ctypes.c_int32, _P, _P]),
     "sivf_rc_string": (ctypes.c_char_p, [_i32]),
     "sivf_profile_enable": (_i32, [_P, _i32]),
     "sivf_profile_read": (_i32, [_P, _P, _P]),
@@ -301,3 +303,17 @@ def merge_topk(dist_g: torch.Tensor, ids_g: torch.Tensor, stream=None):
     _check(lib().sivf_merge_topk(_ptr(dist_g), _ptr(ids_g), G, nq, k, _ptr(dist), _ptr(ids), _stream(stream)),
            "sivf_merge_topk")
     return dist, ids
+
+
+def probe_launch(n: int, stream=None):
+    """Enqueue n empty-kernel launches (latency floor measurement; sivf_probe_launch)."""
+    _check(lib().sivf_probe_launch(int(n), _stream(stream)), "sivf_probe_launch")
+
+
+def probe_chase(next_idx: torch.Tensor, hops: int, out: torch.Tensor, stream=None):
+    """One thread follows `hops` dependent loads through next_idx (int32, device); the final
+    index lands in out[0] (sivf_probe_chase)."""
+    next_idx = _dev(next_idx, torch.int32, "next_idx")
+    out = _dev(out, torch.int32, "out")
+    _check(lib().sivf_probe_chase(_ptr(next_idx), next_idx.numel(), int(hops), _ptr(out), _stream(stream)),
+           "sivf_probe_chase")

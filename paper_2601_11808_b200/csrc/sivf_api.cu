@@ -179,6 +179,16 @@ sivf_rc cuda_rc(cudaError_t e) { return e == cudaSuccess ? SIVF_OK : SIVF_E_CUDA
 
 using namespace sivf;
 
+namespace sivf {
+// measurement probes (sivf_probe_*): an empty kernel, and a dependent-load chain
+__global__ void k_probe_empty() {}
+__global__ void k_probe_chase(const int32_t* __restrict__ next, int64_t n, int32_t hops, int32_t* __restrict__ out) {
+  int32_t i = 0;
+  for (int32_t h = 0; h < hops; ++h) i = __ldcg(next + (i < n && i >= 0 ? i : 0));
+  *out = i;
+}
+}  // namespace sivf
+
 extern "C" {
 
 const char* sivf_rc_string(sivf_rc rc) {
@@ -615,6 +625,18 @@ sivf_rc sivf_stats(sivf_index h, sivf_stats_t* out, sivf_stream_t stream) {
 int64_t sivf_local_capacity(sivf_index h) { return h ? reinterpret_cast<Index*>(h)->st.cap_local : -1; }
 
 int64_t sivf_launch_count(sivf_index h) { return h ? reinterpret_cast<Index*>(h)->launches : -1; }
+
+sivf_rc sivf_probe_launch(int32_t n, sivf_stream_t stream) {
+  if (n < 1) return SIVF_E_INVALID_ARG;
+  for (int32_t i = 0; i < n; ++i) sivf::k_probe_empty<<<1, 32, 0, (cudaStream_t)stream>>>();
+  return cudaGetLastError() == cudaSuccess ? SIVF_OK : SIVF_E_CUDA;
+}
+
+sivf_rc sivf_probe_chase(const int32_t* d_next, int64_t n, int32_t hops, int32_t* d_out, sivf_stream_t stream) {
+  if (!d_next || !d_out || n < 1 || hops < 0) return SIVF_E_INVALID_ARG;
+  sivf::k_probe_chase<<<1, 1, 0, (cudaStream_t)stream>>>(d_next, n, hops, d_out);
+  return cudaGetLastError() == cudaSuccess ? SIVF_OK : SIVF_E_CUDA;
+}
 
 sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
   if (!h) return SIVF_E_INVALID_ARG;
