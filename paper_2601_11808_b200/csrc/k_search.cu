@@ -146,12 +146,17 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
         ++it;
       }
     } else {
-      // ---------------- compute warps
-      const int lq = lane >> 3, ls = lane & 7;
-      const int qrow = warp * kQPW + lq;
+      // ---------------- compute warps: lane = slot, kQPW = 4 queries per lane (the query
+      // loads are warp-wide broadcasts, each slab float4 feeds 4 queries: shared-memory
+      // traffic per distance term ~4x lower than one query x 4 slots per lane)
+      const int sj = lane >> 3, ls = lane & 7;  // the slot's row group and position in it
       const bool warp_active = warp * kQPW < nqt;
-      const float* qp = qs + qrow * Dq;
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* qp = qs + (warp * kQPW) * Dq;
+      // packed fp32x2 arithmetic (FFMA2/FADD2): two partial sums per query (even and odd
+      // dimensions), t = q - x and t*t + acc per pair of dimensions in one instruction each
+      float2 acc[kQPW];
+#pragma unroll
+      for (int j = 0; j < kQPW; ++j) acc[j] = make_float2(0.f, 0.f);
       unsigned long long* mycand = cand + warp * kQPW * kSlot;
       for (;; ++it) {
         const int stg = it % kNS;
@@ -164,31 +169,30 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
           break;
         }
         if (warp_active) {
-          const float* xs = stage_x + stg * kCH * kSlot;
+          const float* xs = stage_x + stg * kCH * kSlot + (sj * (kCH / 4) * 8 + ls) * 4;
           const int cw = min(kCH, Dp - m.chunk * kCH);
           const float* qc = qp + m.chunk * kCH;
 #pragma unroll 4
           for (int i4 = 0; i4 < (cw >> 2); ++i4) {
-            const float4 qv = *reinterpret_cast<const float4*>(qc + 4 * i4);
+            const float4 xv = *reinterpret_cast<const float4*>(xs + i4 * 32);
+            const float2 nx01 = make_float2(-xv.x, -xv.y), nx23 = make_float2(-xv.z, -xv.w);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float4 xv = *reinterpret_cast<const float4*>(xs + ((j * (kCH / 4) + i4) * 8 + ls) * 4);
-              float t;
-              t = qv.x - xv.x; acc[j] = fmaf(t, t, acc[j]);
-              t = qv.y - xv.y; acc[j] = fmaf(t, t, acc[j]);
-              t = qv.z - xv.z; acc[j] = fmaf(t, t, acc[j]);
-              t = qv.w - xv.w; acc[j] = fmaf(t, t, acc[j]);
+            for (int j = 0; j < kQPW; ++j) {
+              const float4 qv = *reinterpret_cast<const float4*>(qc + j * Dq + 4 * i4);
+              const float2 t01 = __fadd2_rn(make_float2(qv.x, qv.y), nx01);
+              const float2 t23 = __fadd2_rn(make_float2(qv.z, qv.w), nx23);
+              acc[j] = __ffma2_rn(t01, t01, acc[j]);
+              acc[j] = __ffma2_rn(t23, t23, acc[j]);
             }
           }
           if (m.last) {
             const uint32_t* ids = stage_id + stg * kSlot;
-            const bool qvalid = qrow < nqt;
+            const bool valid = ((m.bitmap >> lane) & 1u) != 0u;  // Eq. slot_valid
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int slot = ls + 8 * j;
-              const bool valid = qvalid && ((m.bitmap >> slot) & 1u);  // Eq. slot_valid
-              mycand[lq * kSlot + slot] = valid ? make_key(acc[j], ids[slot]) : kPadKey;
-              acc[j] = 0.f;
+            for (int j = 0; j < kQPW; ++j) {
+              const bool qvalid = warp * kQPW + j < nqt;
+              mycand[j * kSlot + lane] = (valid && qvalid) ? make_key(acc[j].x + acc[j].y, ids[lane]) : kPadKey;
+              acc[j] = make_float2(0.f, 0.f);
             }
           }
         }
