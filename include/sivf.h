@@ -56,7 +56,10 @@ typedef enum {
   SIVF_ST_POOL_EXHAUSTED = 1,  /* no free slab (Alg. 2 "If the pool is exhausted") */
   SIVF_ST_DUPLICATE = 2,       /* id live, or repeated earlier in the same batch */
   SIVF_ST_ID_OUT_OF_RANGE = 3, /* id outside [0, id_capacity) */
-  SIVF_ST_WRONG_SHARD = 4      /* id % shard_count != shard_rank */
+  SIVF_ST_WRONG_SHARD = 4,     /* id % shard_count != shard_rank */
+  SIVF_ST_DIR_FULL = 5,        /* sivf_insert_concurrent: the list has no spare directory entry
+                                  (sivf_reserve_directories before the concurrent phase) */
+  SIVF_ST_RETRY_LIMIT = 6      /* sivf_insert_concurrent: 1000 attempts without a slot (C10) */
 } sivf_item_status;
 
 /* sivf_config.flags */
@@ -65,7 +68,11 @@ enum {
    * payload + ids + metadata) and search scans on CUDA cores.  By default
    * (dim <= 128) the arena also holds an fp16 (RN) copy of every slab that the
    * tensor-core scan reads (+50 % of the payload bytes at dim 128; reading C35). */
-  SIVF_CFG_NO_SCAN_COPY = 1
+  SIVF_CFG_NO_SCAN_COPY = 1,
+  /* Room for concurrent phases (NEXT-2): the directory arena gets 256 extra
+   * entries per list so that sivf_reserve_directories can give every list up to
+   * 256 spare entries (1 MB per 1024 lists). */
+  SIVF_CFG_CONCURRENT = 2
 };
 
 typedef struct {
@@ -97,6 +104,8 @@ typedef struct {
   double overhead_actual;       /* this build: (16 B metadata/slab * slabs_in_use + 8 B * id slots) / (live payload+id bytes) */
   double overhead_scan_copy;    /* the scan records (fp16 copy 2 Dh B + norm and id copies 8 B per slot of slabs_in_use) / (live payload+id bytes); 0 without */
   int64_t dir_compactions;      /* times the list directories were repacked into the idle arena half (k_reserve) */
+  int64_t leaked_slabs;         /* slabs leaked by lost publication CASes of sivf_insert_concurrent */
+  int64_t leaked_recycled;      /* of those, returned to the pool by sivf_reclaim */
 } sivf_stats_t;
 
 /* Bytes of device memory the index needs for `cfg` (host-only, pure). */
@@ -188,6 +197,52 @@ int64_t sivf_local_capacity(sivf_index ix);
 /* Number of kernel launches this handle has enqueued so far (bench bookkeeping). */
 int64_t sivf_launch_count(sivf_index ix);
 
+/* ---- NEXT-2: concurrent mutation + search across streams (Alg. 2) ----
+ *
+ * A handle is stream-serialised.  For concurrency, VIEWS of an index share its
+ * state (payload, bitmaps, ATT, directories, free stack, counters) and own
+ * their scratch, so several views can run on several streams at once:
+ *   sivf_search, sivf_delete and sivf_insert_concurrent on views (and on the
+ *   owner) may overlap one another in any combination;
+ *   everything else (sivf_insert, sivf_reclaim, sivf_sliding_window_step,
+ *   sivf_train_centroids, sivf_set_centroids, sivf_reserve_directories,
+ *   sivf_dump_*) is quiescent: owner only, with no view call in flight.
+ * Contract (the paper's publish protocol): an insert becomes visible when its
+ * validity bit is set, after its payload, id and ATT entry (__threadfence before
+ * the atomicOr); a search returns a hit only for a slot whose bit it observed as
+ * set (so never a torn payload), and a concurrent delete makes an id disappear
+ * as soon as its bit is cleared (lazy eviction: a hit implies the bit was set at
+ * some instant during the search).  Searches on a view use acquire loads of the
+ * directory lengths and bitmaps (sivf_set_option SIVF_OPT_CONCURRENT, on by
+ * default for views).
+ *
+ * sivf_view_arena_bytes: bytes of a view's arena for an owner created with cfg.
+ * sivf_create_view: a view of `owner` in the caller's arena (256-B aligned,
+ *   >= sivf_view_arena_bytes); it reads the owner's centroids on `stream` (create
+ *   views after training; views must be destroyed before the owner and recreated
+ *   after the centroids change).  SIVF_E_ARENA_TOO_SMALL / SIVF_E_INVALID_ARG.
+ * sivf_insert_concurrent: sivf_insert's contract with the paper's lock-free
+ *   protocol per vector: CAS slot reservation on the list's tail slab (Eq.
+ *   cas_count), speculative slab expansion published by CAS on the list's next
+ *   directory entry (Eq. cas_head), leak-on-failure (leaked slabs are counted
+ *   and recycled by the next sivf_reclaim), fence + atomicOr publish.  In-flight
+ *   ids are claimed by CAS on the ATT (a live or in-flight id: SIVF_ST_DUPLICATE).
+ *   Extra statuses: SIVF_ST_DIR_FULL (no spare directory entry), SIVF_ST_RETRY_LIMIT.
+ *   The owner must have called sivf_reserve_directories since its last quiescent
+ *   mutation (else SIVF_E_UNSUPPORTED).  Order of slots within a list is
+ *   nondeterministic; the resulting (list, live) state is not.
+ * sivf_reserve_directories (quiescent, owner): every list gets >= `spare` free
+ *   directory entries (one per slab a concurrent phase may add to that list;
+ *   0 <= spare <= 256, else SIVF_E_INVALID_ARG).  Synchronises `stream`;
+ *   SIVF_E_UNSUPPORTED when the directory arena cannot hold them (nothing
+ *   changed; unreachable with SIVF_CFG_CONCURRENT). */
+sivf_rc sivf_view_arena_bytes(const sivf_config* cfg, size_t* bytes);
+sivf_rc sivf_create_view(sivf_index owner, void* d_arena, size_t arena_bytes, sivf_stream_t stream,
+                         sivf_index* out);
+sivf_rc sivf_insert_concurrent(sivf_index ix, const int64_t* d_ids, const float* d_x, int64_t n, int32_t* d_status,
+                               int32_t* d_list, sivf_stream_t stream);
+sivf_rc sivf_reserve_directories(sivf_index owner, int32_t spare, sivf_stream_t stream);
+
 /* Latency floors for measurement (bench.py roofline.latency; SURVEY §8(d)
  * "Latency roofline for small batches"); neither touches an index.
  *   sivf_probe_launch: enqueues n (>= 1) launches of an empty kernel on stream
@@ -222,6 +277,10 @@ enum {
 sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
 
 /* Kernel-path switches (tests compare every path against the oracle).
+ *   SIVF_OPT_CONCURRENT (default 0 on an owner, 1 on a view): searches use
+ *                      acquire loads of directory lengths and bitmaps and order
+ *                      them before the bulk copies of the slab records (needed
+ *                      when sivf_insert_concurrent may run at the same time).
  *   SIVF_OPT_TC_SCAN   (default 1): slab scan on tcgen05 tensor cores (kind::f16
  *                      over the fp16 slab copy) when dim <= 128 and k <= 32;
  *                      0 = CUDA-core scan.
@@ -256,7 +315,7 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
  *                      m-th upper bound by bisection, candidates, exact dist32
  *                      re-rank); 0 = the fused two-pass epilogue.  Same results. */
 enum { SIVF_OPT_TC_SCAN = 1, SIVF_OPT_TC_TWO_PHASE = 2, SIVF_OPT_TC_COARSE = 3, SIVF_OPT_SEED_SLABS = 4,
-       SIVF_OPT_RANK_SPLIT = 5, SIVF_OPT_COARSE_SELECT = 6, SIVF_OPT_STEP_GRAPH = 7 };
+       SIVF_OPT_RANK_SPLIT = 5, SIVF_OPT_COARSE_SELECT = 6, SIVF_OPT_STEP_GRAPH = 7, SIVF_OPT_CONCURRENT = 8 };
 sivf_rc sivf_set_option(sivf_index ix, int32_t option, int64_t value);
 sivf_rc sivf_profile_read(sivf_index ix, double* h_ms, int64_t* h_count);
 

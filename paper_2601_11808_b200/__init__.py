@@ -18,6 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SIVF_LIB_PATH") or os.path.join(_HERE, "lib", "libsivf.so")  # override: experiments
 
 ST_OK, ST_POOL_EXHAUSTED, ST_DUPLICATE, ST_ID_OUT_OF_RANGE, ST_WRONG_SHARD = 0, 1, 2, 3, 4
+ST_DIR_FULL, ST_RETRY_LIMIT = 5, 6  # sivf_insert_concurrent only
 
 _i32, _i64, _u64, _P = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p
 
@@ -54,6 +55,8 @@ class Stats(ctypes.Structure):
         ("overhead_actual", ctypes.c_double),
         ("overhead_scan_copy", ctypes.c_double),
         ("dir_compactions", _i64),
+        ("leaked_slabs", _i64),
+        ("leaked_recycled", _i64),
     ]
 
 
@@ -76,6 +79,10 @@ EXPORTS = {
     "sivf_local_capacity": (_i64, [_P]),
     "sivf_launch_count": (_i64, [_P]),
     "sivf_probe_launch": (_i32, [ctypes.c_int32, _P]),
+    "sivf_view_arena_bytes": (_i32, [ctypes.POINTER(Config), ctypes.POINTER(ctypes.c_size_t)]),
+    "sivf_create_view": (_i32, [_P, _P, ctypes.c_size_t, _P, ctypes.POINTER(_P)]),
+    "sivf_insert_concurrent": (_i32, [_P, _P, _P, ctypes.c_int64, _P, _P, _P]),
+    "sivf_reserve_directories": (_i32, [_P, ctypes.c_int32, _P]),
     "sivf_probe_chase": (_i32, [_P, ctypes.c_int64, ctypes.c_int32, _P, _P]),
     "sivf_rc_string": (ctypes.c_char_p, [_i32]),
     "sivf_profile_enable": (_i32, [_P, _i32]),
@@ -84,6 +91,7 @@ EXPORTS = {
 }
 
 CFG_NO_SCAN_COPY = 1  # sivf_config.flags: no fp16 scan copy (paper footprint, CUDA-core scan)
+CFG_CONCURRENT = 2  # sivf_config.flags: directory room for sivf_reserve_directories (NEXT-2)
 OPT_TC_SCAN = 1
 OPT_TC_TWO_PHASE = 2
 OPT_TC_COARSE = 3
@@ -91,6 +99,7 @@ OPT_SEED_SLABS = 4
 OPT_RANK_SPLIT = 5
 OPT_COARSE_SELECT = 6
 OPT_STEP_GRAPH = 7
+OPT_CONCURRENT = 8
 
 PHASES = ("assign", "append", "delete", "coarse", "invmap", "scan", "merge", "reclaim")
 
@@ -181,6 +190,32 @@ class Index:
                 self._h = None
         except Exception:
             pass
+
+    # ---------------------------------------------------------------- NEXT-2: views, concurrent insert
+    def view(self, stream=None) -> "IndexView":
+        """A view sharing this index's state with its own scratch (sivf_create_view): views on
+        different streams may run search / delete / insert_concurrent at the same time."""
+        return IndexView(self, stream)
+
+    def reserve_directories(self, spare: int, stream=None):
+        """Quiescent: every list gets >= spare free directory entries (sivf_reserve_directories;
+        synchronises the stream)."""
+        _check(lib().sivf_reserve_directories(self._h, int(spare), _stream(stream)), "sivf_reserve_directories")
+
+    def insert_concurrent(self, ids: torch.Tensor, X: torch.Tensor, status: torch.Tensor | None = None,
+                          lists: torch.Tensor | None = None, stream=None):
+        """sivf_insert_concurrent: the paper's lock-free protocol (Alg. 2) per vector."""
+        ids = _dev(ids, torch.int64, "ids")
+        X = _dev(X, torch.float32, "x")
+        n = ids.shape[0]
+        assert X.shape == (n, self.dim)
+        if status is None:
+            status = torch.empty(n, dtype=torch.int32, device=self.device)
+        if lists is None:
+            lists = torch.empty(n, dtype=torch.int32, device=self.device)
+        _check(lib().sivf_insert_concurrent(self._h, _ptr(ids), _ptr(X), n, _ptr(status), _ptr(lists),
+                                            _stream(stream)), "sivf_insert_concurrent")
+        return status, lists
 
     # ---------------------------------------------------------------- quantizer
     def set_centroids(self, C: torch.Tensor, stream=None):
@@ -317,3 +352,25 @@ def probe_chase(next_idx: torch.Tensor, hops: int, out: torch.Tensor, stream=Non
     out = _dev(out, torch.int32, "out")
     _check(lib().sivf_probe_chase(_ptr(next_idx), next_idx.numel(), int(hops), _ptr(out), _stream(stream)),
            "sivf_probe_chase")
+
+
+class IndexView(Index):
+    """A view of an Index (sivf_create_view): shares the owner's index state, owns its scratch.
+    search / delete / insert_concurrent only; the owner must outlive it."""
+
+    def __init__(self, owner: Index, stream=None):  # noqa: super().__init__ is not called (no new index)
+        L = lib()
+        self.owner = owner
+        self.device = owner.device
+        self.cfg = owner.cfg
+        nbytes = ctypes.c_size_t(0)
+        _check(L.sivf_view_arena_bytes(ctypes.byref(owner.cfg), ctypes.byref(nbytes)), "sivf_view_arena_bytes")
+        self.arena_bytes = nbytes.value
+        with torch.cuda.device(self.device):
+            self.arena = torch.empty(max(self.arena_bytes, 256), dtype=torch.uint8, device=self.device)
+            h = ctypes.c_void_p()
+            _check(L.sivf_create_view(owner._h, _ptr(self.arena), self.arena_bytes, _stream(stream), ctypes.byref(h)),
+                   "sivf_create_view")
+        self._h = h
+        self.dim, self.nlist = owner.dim, owner.nlist
+        self.local_capacity = owner.local_capacity

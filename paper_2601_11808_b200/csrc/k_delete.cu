@@ -20,7 +20,8 @@ __global__ void __launch_bounds__(256) k_delete(DevState st, const int64_t* __re
     if (id >= 0 && id < st.cap && id % st.G == st.rank) {
       const int64_t u = id / st.G;
       const uint64_t coord = st.att[u];
-      if (coord != kAttInvalid) {
+      // INVALID: absent; CLAIMED (slab field >= num_slabs): a concurrent insert in flight, not yet present
+      if (coord != kAttInvalid && (coord >> 32) < (uint64_t)st.num_slabs) {
         const uint32_t s = (uint32_t)(coord >> 32), o = (uint32_t)coord & 31u;
         const uint32_t old = atomicAnd(&st.bitmap[s], ~(1u << o));
         if ((old >> o) & 1u) {
@@ -87,6 +88,20 @@ __global__ void k_reclaim(DevState st, unsigned long long* __restrict__ nrec) {
       if (nrec) atomicAdd(nrec, (unsigned long long)freed);
     }
   }
+}
+
+// NEXT-2: slabs leaked by lost publication CASes of concurrent inserts (slab_list
+// == kSlabLeaking, in no directory, not on the free stack) go back to the pool at
+// a quiescent point (thread per slab).
+__global__ void k_reclaim_leaked(DevState st) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= st.num_slabs || st.slab_list[s] != kSlabLeaking) return;
+  const int t = atomicAdd(&st.ictr[I_FREE_TOP], 1);
+  st.free_stack[t] = (int32_t)s;
+  st.slab_list[s] = -1;
+  st.cursor[s] = 0u;
+  st.bitmap[s] = 0u;
+  atomicAdd(&st.ctr[C_LEAKRECL], 1ull);
 }
 
 // ---- state export + invariant check (K10) ----
@@ -161,7 +176,8 @@ __global__ void k_dump_marks(DevState st, const uint32_t* __restrict__ mark, uns
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s == 0 && *live_sum != st.ctr[C_LIVE]) atomicAdd(viol, 1ull);  // sum popc == live counter
   if (s >= st.num_slabs) return;
-  if (mark[s] != 1u) atomicAdd(viol, 1ull);  // each slab: exactly one directory, or the free stack
+  // each slab: exactly one directory, or the free stack, or leaked by a concurrent insert (awaiting reclaim)
+  if (mark[s] != 1u && !(mark[s] == 0u && st.slab_list[s] == kSlabLeaking)) atomicAdd(viol, 1ull);
 }
 
 }  // namespace
@@ -181,6 +197,10 @@ cudaError_t launch_reclaim(Index& ix, int64_t* d_nrec, cudaStream_t s) {
   k_reclaim<<<ceil_div((int64_t)ix.st.nlist * 32, 256), 256, 0, s>>>(ix.st,
                                                                      reinterpret_cast<unsigned long long*>(d_nrec));
   ix.launches += 1;
+  if (ix.conc_used) {  // NEXT-2: slabs leaked by lost publication CASes
+    k_reclaim_leaked<<<ceil_div(ix.st.num_slabs, 256), 256, 0, s>>>(ix.st);
+    ix.launches += 1;
+  }
   return cudaGetLastError();
 }
 

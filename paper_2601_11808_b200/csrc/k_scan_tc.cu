@@ -306,18 +306,18 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     // claims work items and walks each list's slab directory ahead of the
     // producer (up to NITEM - 1 items ahead): the dependent loads (item ->
     // directory -> bitmap -> flag) leave the copy issue path
-    const int ntiles = st.ictr[a.phase == 1 ? I_NTILES0 : I_NTILES];
+    const int ntiles = st.sctr[a.phase == 1 ? I_NTILES0 : I_NTILES];
     const unsigned lt = (1u << lane) - 1u;
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
       if (lane == 0) PW(0, MBW(&item_empty[slot], ((i / NITEM) & 1u) ^ 1u, 1));
       int w = 0;
-      if (lane == 0) w = atomicAdd(&st.ictr[a.phase == 2 ? I_WORK2 : I_WORK], 1);
+      if (lane == 0) w = atomicAdd(&st.sctr[a.phase == 2 ? I_WORK2 : I_WORK], 1);
       w = __shfl_sync(kFull, w, 0);
       ItemRec r{-1, 0, 0, 0, -1, 0, 0, 0};
       if (w < ntiles) {
         const int l = a.work_l[w];
-        const int len = st.dir_len[l];
+        const int len = ld_state_s32(&st.dir_len[l], st.conc);
         const int32_t* dir = st.dir_arena + st.dir_off[l];
         uint2* rec = irec + slot * MAXS;
         int npre = 0, j0 = 0;
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           uint32_t bm = 0u;
           if (j < len) {
             sl = dir[j];
-            bm = st.bitmap[sl];
+            bm = ld_state_u32(&st.bitmap[sl], st.conc);
           }
           const unsigned live = __ballot_sync(kFull, bm != 0u);
           if (npre + __popc(live) > MAXS) break;  // the producer walks the rest
@@ -375,6 +375,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&full[stg], (a.dbg & 8) ? 0u : (uint32_t)nvalid * rbytes);
       __syncwarp();
+      if (st.conc) fence_proxy_async_global();  // the bitmap acquire orders the record copies (NEXT-2)
       if (lane < nvalid && !(a.dbg & 8))
         bulk_g2s(stage_x(stg) + (size_t)lane * rbytes, reinterpret_cast<const unsigned char*>(st.payload16) +
                                                            (size_t)sl * rbytes, rbytes, &full[stg]);
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           uint32_t bm = 0u, fl = 0u;
           if (j < rec.len) {
             sl = dir[j];
-            bm = st.bitmap[sl];
+            bm = ld_state_u32(&st.bitmap[sl], st.conc);
             if (bm) fl = st.slab_flag[sl] & 3u;
           }
           const unsigned live = __ballot_sync(kFull, bm != 0u);
@@ -703,7 +704,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
                   const float* qr = a.Q + (int64_t)qglob * st.D;
                   float acc = 0.f;
                   for (int i4 = 0; i4 < nq4; ++i4) {
-                    const float4 xv = __ldg(reinterpret_cast<const float4*>(xs + pay_off(Dp, c, i4)));
+                    const float4 xv = __ldcg(reinterpret_cast<const float4*>(xs + pay_off(Dp, c, i4)));
                     float qv[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) qv[e] = 4 * i4 + e < st.D ? __ldg(qr + 4 * i4 + e) : 0.f;

@@ -86,11 +86,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
-  const int ntiles = st.ictr[I_NTILES];
+  const int ntiles = st.sctr[I_NTILES];
   uint32_t it = 0;  // stage sequence number (same sequence in producer and consumers)
 
   for (;;) {
-    if (threadIdx.x == 0) ctrl[0] = atomicAdd(&st.ictr[I_WORK], 1);
+    if (threadIdx.x == 0) ctrl[0] = atomicAdd(&st.sctr[I_WORK], 1);
     __syncthreads();
     const int w_item = ctrl[0];
     if (w_item >= ntiles) break;
@@ -117,12 +117,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
     if (warp == NW) {
       // ---------------- producer: one elected lane issues bulk copies
       if (lane == 0) {
-        const int len = st.dir_len[l];
+        const int len = ld_state_s32(&st.dir_len[l], st.conc);
         const int32_t* dir = st.dir_arena + st.dir_off[l];
         for (int j = 0; j < len; ++j) {
           const int s = dir[j];
-          const uint32_t bm = st.bitmap[s];
+          const uint32_t bm = ld_state_u32(&st.bitmap[s], st.conc);
           if (bm == 0u) continue;  // nothing valid in this slab
+          if (st.conc) fence_proxy_async_global();  // the bitmap acquire orders the copies (NEXT-2)
           const float* src = st.payload + (size_t)s * kSlot * Dp;
           for (int c = 0; c < nch; ++c, ++it) {
             const int stg = it % kNS;
@@ -494,7 +495,7 @@ cudaError_t launch_search_front(Index& ix, const SearchPlan& p, const float* d_q
                                                        sc.gthr, (ix.dbg >> 6) & 1);
     ix.launches += 1;
   }
-  k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, p.QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.ictr, nlist,
+  k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, p.QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.sctr, nlist,
                                 sc.work_l, sc.work_p0, sc.work_n);
   k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, p.nb, p.r0, nlist, sc.inv_cursor,
                                                        sc.inv_pairs);

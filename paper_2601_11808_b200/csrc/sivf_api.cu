@@ -16,7 +16,7 @@ constexpr size_t kAlign = 256;
 struct Layout {
   size_t total = 0;
   size_t payload, payload16, slab_ids, slab_norm, slab_flag, bitmap, cursor, slab_list, free_stack, slab_mark, att, claim,
-      dir_off, dir_len, dir_cap, dir_arena, centroids, ctr, ictr, tmp64, gthr;
+      dir_off, dir_len, dir_cap, dir_arena, centroids, ctr, ictr, sctr, tmp64, gthr;
   size_t row_list, row_rank, row_status, row_lid, row_best, chunk_hist, list_cnt, list_tail_free, list_tail_slab,
       list_granted, list_newbase, list_newoff;
   size_t coarse, probes, inv_cnt, inv_off, inv_cursor, inv_pairs, tile_off, work_l, work_p0, work_n, partial;
@@ -45,11 +45,13 @@ bool valid_config(const sivf_config* c) {
   if (c->shard_count < 1 || c->shard_rank < 0 || c->shard_rank >= c->shard_count) return false;
   if (c->max_train > 0 && c->max_train < c->nlist) return false;
   if ((int64_t)c->max_queries * c->max_nprobe > 0x7FFFFFFFll) return false;
-  if (c->flags & ~(int32_t)SIVF_CFG_NO_SCAN_COPY) return false;  // unknown flag bits
+  if (c->flags & ~(int32_t)(SIVF_CFG_NO_SCAN_COPY | SIVF_CFG_CONCURRENT)) return false;  // unknown flag bits
   return true;
 }
 
-Layout make_layout(const sivf_config* c) {
+// view == true: a view's arena (sivf_create_view): the index state arrays are the
+// owner's (zero bytes here), every scratch array is the view's own.
+Layout make_layout(const sivf_config* c, bool view = false) {
   Layout L;
   const int64_t D = c->dim, nl = c->nlist, S = c->num_slabs;
   L.Dp = (D + 7) / 8 * 8;  // tf32 MMA K-step = 8 dims
@@ -58,8 +60,10 @@ Layout make_layout(const sivf_config* c) {
   const int64_t cap = c->id_capacity, G = c->shard_count, r = c->shard_rank;
   L.cap_local = cap > r ? (cap - r + G - 1) / G : 0;
   // directory arena: two halves; a compaction into the idle half needs at most
-  // sum over lists of max(8, 2 len) <= 2 S + 8 nl entries (k_reserve)
-  L.dir_half = 2 * S + 8 * nl + 64;
+  // sum over lists of max(8, 2 len) <= 2 S + 8 nl entries (k_reserve), or of
+  // max(8, 2 len, len + spare) <= 2 S + 264 nl with spare <= 256 (k_reserve_dirs,
+  // SIVF_CFG_CONCURRENT)
+  L.dir_half = 2 * S + ((c->flags & SIVF_CFG_CONCURRENT) ? 264 : 8) * nl + 64;
   L.max_rows = c->max_batch > c->max_train ? c->max_batch : c->max_train;
   if (L.max_rows < 1) L.max_rows = 1;
   L.max_chunks = (L.max_rows + 1023) / 1024;
@@ -75,25 +79,27 @@ Layout make_layout(const sivf_config* c) {
   const int64_t npairs = (int64_t)c->max_queries * c->max_nprobe;
   L.max_work = (npairs + 7) / 8 + 2 * nl + 1;
 
-  L.payload = take(L, (size_t)S * kSlot * L.Dp * 4);
-  L.payload16 = take(L, L.Dh ? (size_t)S * rec16_bytes((int)L.Dh) : 0);
-  L.slab_ids = take(L, (size_t)S * kSlot * 4);
-  L.slab_norm = take(L, (size_t)S * kSlot * 4);
-  L.slab_flag = take(L, (size_t)S * 4);
-  L.bitmap = take(L, (size_t)S * 4);
-  L.cursor = take(L, (size_t)S * 4);
-  L.slab_list = take(L, (size_t)S * 4);
-  L.free_stack = take(L, (size_t)S * 4);
-  L.slab_mark = take(L, (size_t)S * 4);
-  L.att = take(L, (size_t)L.cap_local * 8);
-  L.claim = take(L, (size_t)L.cap_local * 4);
-  L.dir_off = take(L, (size_t)nl * 8);
-  L.dir_len = take(L, (size_t)nl * 4);
-  L.dir_cap = take(L, (size_t)nl * 4);
-  L.dir_arena = take(L, (size_t)2 * L.dir_half * 4);
-  L.centroids = take(L, (size_t)nl * L.Dp * 4);
-  L.ctr = take(L, C_NCTR * 8);
-  L.ictr = take(L, I_NICTR * 4);
+  const size_t sv = view ? 0 : 1;  // state arrays: the owner's in a view
+  L.payload = take(L, sv * (size_t)S * kSlot * L.Dp * 4);
+  L.payload16 = take(L, L.Dh ? sv * (size_t)S * rec16_bytes((int)L.Dh) : 0);
+  L.slab_ids = take(L, sv * (size_t)S * kSlot * 4);
+  L.slab_norm = take(L, sv * (size_t)S * kSlot * 4);
+  L.slab_flag = take(L, sv * (size_t)S * 4);
+  L.bitmap = take(L, sv * (size_t)S * 4);
+  L.cursor = take(L, sv * (size_t)S * 4);
+  L.slab_list = take(L, sv * (size_t)S * 4);
+  L.free_stack = take(L, sv * (size_t)S * 4);
+  L.slab_mark = take(L, sv * (size_t)S * 4);
+  L.att = take(L, sv * (size_t)L.cap_local * 8);
+  L.claim = take(L, sv * (size_t)L.cap_local * 4);
+  L.dir_off = take(L, sv * (size_t)nl * 8);
+  L.dir_len = take(L, sv * (size_t)nl * 4);
+  L.dir_cap = take(L, sv * (size_t)nl * 4);
+  L.dir_arena = take(L, sv * (size_t)2 * L.dir_half * 4);
+  L.centroids = take(L, sv * (size_t)nl * L.Dp * 4);
+  L.ctr = take(L, sv * C_NCTR * 8);
+  L.ictr = take(L, sv * I_NICTR * 4);
+  L.sctr = take(L, I_NICTR * 4);
   L.tmp64 = take(L, 16 * 8);
   L.gthr = take(L, (size_t)(c->max_queries > 0 ? c->max_queries : 1) * 4);
   L.row_list = take(L, (size_t)L.max_rows * 4);
@@ -163,7 +169,10 @@ __global__ void k_init(DevState st) {
     st.dir_cap[i] = 0;
   }
   if (i < C_NCTR) st.ctr[i] = 0ull;
-  if (i < I_NICTR) st.ictr[i] = 0;
+  if (i < I_NICTR) {
+    st.ictr[i] = 0;
+    st.sctr[i] = 0;
+  }
   if (i == 0) st.ictr[I_FREE_TOP] = (int32_t)st.num_slabs;
 }
 
@@ -173,6 +182,60 @@ T* at(void* base, size_t off) {
 }
 
 sivf_rc cuda_rc(cudaError_t e) { return e == cudaSuccess ? SIVF_OK : SIVF_E_CUDA; }
+
+// Scratch carving of an arena (an owner's or a view's; the layout puts every
+// scratch array after the state arrays).
+void carve_scratch(Scratch& sc, void* d_arena, const Layout& L) {
+  sc.max_rows = L.max_rows;
+  sc.row_list = at<int32_t>(d_arena, L.row_list);
+  sc.row_rank = at<int32_t>(d_arena, L.row_rank);
+  sc.row_status = at<int32_t>(d_arena, L.row_status);
+  sc.row_lid = at<int64_t>(d_arena, L.row_lid);
+  sc.row_best = at<unsigned long long>(d_arena, L.row_best);
+  sc.chunk_hist = at<int32_t>(d_arena, L.chunk_hist);
+  sc.max_chunks = L.max_chunks;
+  sc.list_cnt = at<int32_t>(d_arena, L.list_cnt);
+  sc.list_tail_free = at<int32_t>(d_arena, L.list_tail_free);
+  sc.list_tail_slab = at<int32_t>(d_arena, L.list_tail_slab);
+  sc.list_granted = at<int32_t>(d_arena, L.list_granted);
+  sc.list_newbase = at<int32_t>(d_arena, L.list_newbase);
+  sc.list_newoff = at<int64_t>(d_arena, L.list_newoff);
+  sc.coarse = at<float>(d_arena, L.coarse);
+  sc.q_rows = L.q_rows;
+  sc.qx_tiles = at<float>(d_arena, L.qx_tiles);
+  sc.qx_norm = at<float>(d_arena, L.qx_norm);
+  sc.qcoarse = at<float>(d_arena, L.qcoarse);
+  sc.coarse_rows = L.coarse_rows;
+  sc.probes = at<int32_t>(d_arena, L.probes);
+  sc.inv_cnt = at<int32_t>(d_arena, L.inv_cnt);
+  sc.inv_off = at<int32_t>(d_arena, L.inv_off);
+  sc.inv_cursor = at<int32_t>(d_arena, L.inv_cursor);
+  sc.inv_pairs = at<int32_t>(d_arena, L.inv_pairs);
+  sc.tile_off = at<int32_t>(d_arena, L.tile_off);
+  sc.work_l = at<int32_t>(d_arena, L.work_l);
+  sc.work_p0 = at<int32_t>(d_arena, L.work_p0);
+  sc.work_n = at<int32_t>(d_arena, L.work_n);
+  sc.max_work = L.max_work;
+  sc.partial = at<unsigned long long>(d_arena, L.partial);
+  sc.train_perm = at<int32_t>(d_arena, L.train_perm);
+  sc.train_members = at<int32_t>(d_arena, L.train_members);
+  sc.train_off = at<int32_t>(d_arena, L.train_off);
+  sc.slab_mark = at<uint32_t>(d_arena, L.slab_mark);
+  sc.tmp64 = at<long long>(d_arena, L.tmp64);
+  sc.gthr = at<uint32_t>(d_arena, L.gthr);
+  sc.tc_rows = L.tc_rows;
+  sc.x_tiles = at<float>(d_arena, L.x_tiles);
+  sc.x_norm = at<float>(d_arena, L.x_norm);
+  sc.c_tiles = at<float>(d_arena, L.c_tiles);
+  sc.c_norm = at<float>(d_arena, L.c_norm);
+  sc.c_csa = at<float>(d_arena, L.c_csa);
+  sc.c_cnb = at<float>(d_arena, L.c_cnb);
+  sc.cand = at<unsigned long long>(d_arena, L.cand);
+  sc.cand_ubv = at<float>(d_arena, L.cand_ubv);
+  sc.cand_cnt = at<int32_t>(d_arena, L.cand_cnt);
+  sc.cand_cap_assign = (int32_t)L.cap_assign;
+  sc.cand_cap_probe = (int32_t)L.cap_probe;
+}
 
 }  // namespace
 }  // namespace sivf
@@ -253,56 +316,9 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   st.centroids = at<float>(d_arena, L.centroids);
   st.ctr = at<unsigned long long>(d_arena, L.ctr);
   st.ictr = at<int32_t>(d_arena, L.ictr);
-  Scratch& sc = ix->sc;
-  sc.max_rows = L.max_rows;
-  sc.row_list = at<int32_t>(d_arena, L.row_list);
-  sc.row_rank = at<int32_t>(d_arena, L.row_rank);
-  sc.row_status = at<int32_t>(d_arena, L.row_status);
-  sc.row_lid = at<int64_t>(d_arena, L.row_lid);
-  sc.row_best = at<unsigned long long>(d_arena, L.row_best);
-  sc.chunk_hist = at<int32_t>(d_arena, L.chunk_hist);
-  sc.max_chunks = L.max_chunks;
-  sc.list_cnt = at<int32_t>(d_arena, L.list_cnt);
-  sc.list_tail_free = at<int32_t>(d_arena, L.list_tail_free);
-  sc.list_tail_slab = at<int32_t>(d_arena, L.list_tail_slab);
-  sc.list_granted = at<int32_t>(d_arena, L.list_granted);
-  sc.list_newbase = at<int32_t>(d_arena, L.list_newbase);
-  sc.list_newoff = at<int64_t>(d_arena, L.list_newoff);
-  sc.coarse = at<float>(d_arena, L.coarse);
-  sc.q_rows = L.q_rows;
-  sc.qx_tiles = at<float>(d_arena, L.qx_tiles);
-  sc.qx_norm = at<float>(d_arena, L.qx_norm);
-  sc.qcoarse = at<float>(d_arena, L.qcoarse);
-  sc.coarse_rows = L.coarse_rows;
-  sc.probes = at<int32_t>(d_arena, L.probes);
-  sc.inv_cnt = at<int32_t>(d_arena, L.inv_cnt);
-  sc.inv_off = at<int32_t>(d_arena, L.inv_off);
-  sc.inv_cursor = at<int32_t>(d_arena, L.inv_cursor);
-  sc.inv_pairs = at<int32_t>(d_arena, L.inv_pairs);
-  sc.tile_off = at<int32_t>(d_arena, L.tile_off);
-  sc.work_l = at<int32_t>(d_arena, L.work_l);
-  sc.work_p0 = at<int32_t>(d_arena, L.work_p0);
-  sc.work_n = at<int32_t>(d_arena, L.work_n);
-  sc.max_work = L.max_work;
-  sc.partial = at<unsigned long long>(d_arena, L.partial);
-  sc.train_perm = at<int32_t>(d_arena, L.train_perm);
-  sc.train_members = at<int32_t>(d_arena, L.train_members);
-  sc.train_off = at<int32_t>(d_arena, L.train_off);
-  sc.slab_mark = at<uint32_t>(d_arena, L.slab_mark);
-  sc.tmp64 = at<long long>(d_arena, L.tmp64);
-  sc.gthr = at<uint32_t>(d_arena, L.gthr);
-  sc.tc_rows = L.tc_rows;
-  sc.x_tiles = at<float>(d_arena, L.x_tiles);
-  sc.x_norm = at<float>(d_arena, L.x_norm);
-  sc.c_tiles = at<float>(d_arena, L.c_tiles);
-  sc.c_norm = at<float>(d_arena, L.c_norm);
-  sc.c_csa = at<float>(d_arena, L.c_csa);
-  sc.c_cnb = at<float>(d_arena, L.c_cnb);
-  sc.cand = at<unsigned long long>(d_arena, L.cand);
-  sc.cand_ubv = at<float>(d_arena, L.cand_ubv);
-  sc.cand_cnt = at<int32_t>(d_arena, L.cand_cnt);
-  sc.cand_cap_assign = (int32_t)L.cap_assign;
-  sc.cand_cap_probe = (int32_t)L.cap_probe;
+  st.sctr = at<int32_t>(d_arena, L.sctr);
+  st.conc = 0;
+  carve_scratch(ix->sc, d_arena, L);
 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaMemsetAsync(st.att, 0xff, (size_t)L.cap_local * 8, s);          // ATT <- INVALID
@@ -328,6 +344,81 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   return SIVF_OK;
 }
 
+sivf_rc sivf_view_arena_bytes(const sivf_config* cfg, size_t* bytes) {
+  if (!valid_config(cfg) || !bytes) return SIVF_E_INVALID_ARG;
+  *bytes = make_layout(cfg, true).total;
+  return SIVF_OK;
+}
+
+sivf_rc sivf_create_view(sivf_index owner_h, void* d_arena, size_t arena_bytes, sivf_stream_t stream,
+                         sivf_index* out) {
+  if (!owner_h || !out) return SIVF_E_INVALID_ARG;
+  Index* own = reinterpret_cast<Index*>(owner_h);
+  if (own->view) return SIVF_E_INVALID_ARG;  // views of views are not needed
+  const Layout L = make_layout(&own->cfg, true);
+  if (!d_arena || arena_bytes < L.total || (reinterpret_cast<uintptr_t>(d_arena) % kAlign) != 0)
+    return SIVF_E_ARENA_TOO_SMALL;
+  Index* ix = new (std::nothrow) Index();
+  if (!ix) return SIVF_E_INVALID_ARG;
+  ix->cfg = own->cfg;
+  ix->view = true;
+  ix->owner = own;
+  ix->num_sms = own->num_sms;
+  ix->smem_optin = own->smem_optin;
+  ix->trained = own->trained;
+  ix->st = own->st;  // shared index state
+  ix->st.sctr = at<int32_t>(d_arena, L.sctr);
+  ix->st.conc = 1;
+  carve_scratch(ix->sc, d_arena, L);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(ix->st.sctr, 0, I_NICTR * 4, s);
+  cudaStreamCreateWithFlags(&ix->side, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&ix->cap_stream, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&ix->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ix->ev_join, cudaEventDisableTiming);
+  cudaError_t e = setup_search_kernels(*ix);
+  if (e == cudaSuccess) e = setup_coarse_tc(*ix);
+  if (e == cudaSuccess) e = setup_coarse_exact(*ix);
+  if (e == cudaSuccess && ix->trained) e = refresh_centroid_tiles(*ix, s);  // the view's own centroid tiles
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    delete ix;
+    return SIVF_E_CUDA;
+  }
+  *out = reinterpret_cast<sivf_index>(ix);
+  return SIVF_OK;
+}
+
+sivf_rc sivf_insert_concurrent(sivf_index h, const int64_t* d_ids, const float* d_x, int64_t n, int32_t* d_status,
+                               int32_t* d_list, sivf_stream_t stream) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (n < 0 || n > ix->cfg.max_batch) return SIVF_E_INVALID_ARG;
+  if (n > 0 && (!d_ids || !d_x)) return SIVF_E_INVALID_ARG;
+  if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  Index* own = ix->view ? ix->owner : ix;
+  if (!own->dirs_prepared) return SIVF_E_UNSUPPORTED;
+  own->conc_used = true;
+  return cuda_rc(launch_insert_concurrent(*ix, d_ids, d_x, n, d_status, d_list, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sivf_rc sivf_reserve_directories(sivf_index h, int32_t spare, sivf_stream_t stream) {
+  if (!h || spare < 0 || spare > 256) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (ix->view) return SIVF_E_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int32_t* d_fail = reinterpret_cast<int32_t*>(ix->sc.tmp64 + 8);
+  cudaMemsetAsync(d_fail, 0, 4, s);
+  cudaError_t e = launch_reserve_dirs(*ix, spare, d_fail, s);
+  int32_t fail = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&fail, d_fail, 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return SIVF_E_CUDA;
+  if (fail) return SIVF_E_UNSUPPORTED;
+  ix->dirs_prepared = true;
+  return SIVF_OK;
+}
+
 sivf_rc sivf_destroy(sivf_index h) {
   if (!h) return SIVF_E_INVALID_ARG;
   delete reinterpret_cast<Index*>(h);
@@ -337,6 +428,7 @@ sivf_rc sivf_destroy(sivf_index h) {
 sivf_rc sivf_set_centroids(sivf_index h, const float* d_c, sivf_stream_t stream) {
   if (!h || !d_c) return SIVF_E_INVALID_ARG;
   Index* ix = reinterpret_cast<Index*>(h);
+  if (ix->view) return SIVF_E_INVALID_ARG;  // quiescent, owner only
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int D = ix->st.D, Dp = ix->st.Dp;
   cudaError_t e = cudaMemcpy2DAsync(ix->st.centroids, (size_t)Dp * 4, d_c, (size_t)D * 4, (size_t)D * 4,
@@ -359,6 +451,7 @@ sivf_rc sivf_get_centroids(sivf_index h, float* d_c, sivf_stream_t stream) {
 sivf_rc sivf_train_centroids(sivf_index h, const float* d_x, int64_t n, int32_t niter, sivf_stream_t stream) {
   if (!h || !d_x) return SIVF_E_INVALID_ARG;
   Index* ix = reinterpret_cast<Index*>(h);
+  if (ix->view) return SIVF_E_INVALID_ARG;  // quiescent, owner only
   if (n < ix->st.nlist || n > ix->cfg.max_train || niter < 0) return SIVF_E_INVALID_ARG;
   cudaError_t e = launch_train(*ix, d_x, n, niter, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return SIVF_E_CUDA;
@@ -370,9 +463,11 @@ sivf_rc sivf_insert(sivf_index h, const int64_t* d_ids, const float* d_x, int64_
                     int32_t* d_list, sivf_stream_t stream) {
   if (!h) return SIVF_E_INVALID_ARG;
   Index* ix = reinterpret_cast<Index*>(h);
+  if (ix->view) return SIVF_E_INVALID_ARG;  // quiescent, owner only (views: sivf_insert_concurrent)
   if (n < 0 || n > ix->cfg.max_batch) return SIVF_E_INVALID_ARG;
   if (n > 0 && (!d_ids || !d_x)) return SIVF_E_INVALID_ARG;
   if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  ix->dirs_prepared = false;  // directories may grow without spare entries
   return cuda_rc(launch_insert(*ix, d_ids, d_x, n, d_status, d_list, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -494,6 +589,8 @@ sivf_rc sivf_search(sivf_index h, const float* d_q, int64_t nq, int32_t k, int32
 
 sivf_rc sivf_reclaim(sivf_index h, int64_t* d_nreclaimed, sivf_stream_t stream) {
   if (!h) return SIVF_E_INVALID_ARG;
+  if (reinterpret_cast<Index*>(h)->view) return SIVF_E_INVALID_ARG;  // quiescent, owner only
+  reinterpret_cast<Index*>(h)->dirs_prepared = false;
   return cuda_rc(launch_reclaim(*reinterpret_cast<Index*>(h), d_nreclaimed, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -545,6 +642,8 @@ sivf_rc sivf_sliding_window_step(sivf_index h, const int64_t* d_new_ids, const f
                                  int32_t nprobe, float* d_dist, int64_t* d_ids, int32_t* d_status,
                                  int64_t* d_ndeleted, sivf_stream_t stream) {
   if (!h) return SIVF_E_INVALID_ARG;
+  if (reinterpret_cast<Index*>(h)->view) return SIVF_E_INVALID_ARG;  // quiescent, owner only
+  reinterpret_cast<Index*>(h)->dirs_prepared = false;
   Index* ix = reinterpret_cast<Index*>(h);
   if (n_new < 0 || n_new > ix->cfg.max_batch || n_old < 0 || nq < 0 || nq > ix->cfg.max_queries)
     return SIVF_E_INVALID_ARG;
@@ -581,6 +680,7 @@ sivf_rc sivf_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int32_t G
 sivf_rc sivf_dump_state(sivf_index h, int32_t* d_list_of_id, int64_t* d_live_per_list, int64_t* d_violations,
                         sivf_stream_t stream) {
   if (!h) return SIVF_E_INVALID_ARG;
+  if (reinterpret_cast<Index*>(h)->view) return SIVF_E_INVALID_ARG;  // quiescent, owner only
   return cuda_rc(launch_dump(*reinterpret_cast<Index*>(h), d_list_of_id, d_live_per_list, d_violations,
                              reinterpret_cast<cudaStream_t>(stream)));
 }
@@ -609,6 +709,8 @@ sivf_rc sivf_stats(sivf_index h, sivf_stats_t* out, sivf_stream_t stream) {
   out->pool_exhausted_items = (int64_t)c[C_EXHAUSTED];
   out->reclaimed_slabs = (int64_t)c[C_RECLAIMED];
   out->device_errors = (int64_t)c[C_DEVERR];
+  out->leaked_slabs = (int64_t)c[C_LEAKED];
+  out->leaked_recycled = (int64_t)c[C_LEAKRECL];
   out->dir_compactions = (int64_t)c[C_DIRCOMPACT];
   out->slabs_free = ic[I_FREE_TOP];
   out->slabs_in_use = ix->st.num_slabs - ic[I_FREE_TOP];
@@ -651,6 +753,7 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
     case SIVF_OPT_RANK_SPLIT: ix->rank_split = value < 0 ? 0 : (int)value; return SIVF_OK;
     case 99: ix->dbg = (int)value; return SIVF_OK;  // SIVF_OPT_DEBUG: experiments only
     case 98: ix->tc_max_stages = (int)value; return SIVF_OK;  // experiments only: scan stage-ring cap
+    case SIVF_OPT_CONCURRENT: ix->st.conc = value != 0; return SIVF_OK;
     case SIVF_OPT_SEED_SLABS:
       if (value < 0 || value > (1 << 20)) return SIVF_E_INVALID_ARG;
       ix->seed_slabs = (int)value;

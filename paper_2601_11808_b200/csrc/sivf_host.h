@@ -83,6 +83,11 @@ struct Index {
   sivf_config cfg{};
   DevState st{};
   Scratch sc{};
+  // NEXT-2: a view (sivf_create_view) shares its owner's index state and owns its scratch
+  bool view = false;
+  Index* owner = nullptr;       // a view's owner (nullptr on an owner)
+  bool dirs_prepared = false;   // owner: sivf_reserve_directories ran since the last quiescent mutation
+  bool conc_used = false;       // owner: sivf_insert_concurrent ran (reclaim then also recycles leaked slabs)
   bool trained = false;
   bool use_tc_scan = true;
   bool use_tc_coarse = true;  // tcgen05 coarse quantisation (k_coarse_tc.cu); false = exact SIMT k_dist_exact
@@ -181,6 +186,9 @@ struct PhaseTimer {
 // k_insert.cu
 cudaError_t launch_insert(Index& ix, const int64_t* d_ids, const float* d_x, int64_t n, int32_t* d_status,
                           int32_t* d_list, cudaStream_t s);
+cudaError_t launch_insert_concurrent(Index& ix, const int64_t* d_ids, const float* d_x, int64_t n, int32_t* d_status,
+                                     int32_t* d_list, cudaStream_t s);
+cudaError_t launch_reserve_dirs(Index& ix, int spare, int32_t* d_fail, cudaStream_t s);
 // k_delete.cu
 cudaError_t launch_delete(Index& ix, const int64_t* d_ids, int64_t n, int64_t* d_ndeleted, cudaStream_t s);
 cudaError_t launch_reclaim(Index& ix, int64_t* d_nreclaimed, cudaStream_t s);

@@ -40,13 +40,17 @@ __host__ __device__ __forceinline__ size_t rec16_id_off(int Dh, int n) { return 
 constexpr uint32_t kFlagIntegral = 1u;  // every value an integer with |v| <= 2048 (exact in tf32 and fp16)
 constexpr uint32_t kFlagF16Over = 2u;   // some value has |v| > 65504 (no finite fp16 copy): scan re-ranks all
 constexpr uint64_t kAttInvalid = ~0ull;            // INVALID sentinel (reading C14)
+constexpr uint64_t kAttClaimed = 0xFFFFFFFE00000000ull;  // concurrent insert in flight (slab field >= any num_slabs)
+constexpr int32_t kSlabLeaking = -2;               // slab_list of a slab popped by a concurrent insert, not yet linked
+constexpr int32_t kDirPending = -3;                // directory entry claimed by a concurrent expansion (k_insert_cas)
 constexpr int32_t kClaimEmpty = 0x7f7f7f7f;        // byte-memsettable "no claimant"
 constexpr uint64_t kPadKey = 0x7F800000FFFFFFFFull; // (+inf, id 0xFFFFFFFF): sorts after every real key
 constexpr unsigned kFull = 0xffffffffu;
 using u64 = unsigned long long;
 
 // Counters (u64, arena) — index into DevState::ctr
-enum { C_LIVE = 0, C_INSERTED, C_DELETED, C_EXHAUSTED, C_RECLAIMED, C_DEVERR, C_NDEL_TMP, C_DIRCOMPACT, C_NCTR = 8 };
+enum { C_LIVE = 0, C_INSERTED, C_DELETED, C_EXHAUSTED, C_RECLAIMED, C_DEVERR, C_NDEL_TMP, C_DIRCOMPACT, C_LEAKED,
+       C_LEAKRECL, C_NCTR = 10 };
 // Counters (i32, arena) — index into DevState::ictr
 // I_DIR_BUMP: next free entry of the active directory half; I_DIR_HALF: which half (0/1) is active
 enum { I_FREE_TOP = 0, I_DIR_BUMP, I_WORK, I_NTILES, I_NTILES0, I_WORK2, I_DIR_HALF, I_NICTR = 8 };  // *0/*2: phased scan
@@ -74,7 +78,9 @@ struct DevState {
   int64_t dir_half;      // entries per half (>= 2 num_slabs + 8 nlist: a compaction always fits)
   float* centroids;      // [nlist][Dp] (zero padded)
   unsigned long long* ctr;
-  int32_t* ictr;
+  int32_t* ictr;         // index counters (free-stack top, directory bump/half): shared state
+  int32_t* sctr;         // search work counters (I_WORK, I_NTILES, I_NTILES0, I_WORK2): per-handle scratch
+  int32_t conc;          // concurrent mode (NEXT-2): acquire loads of directories and bitmaps in the scans
 };
 
 __device__ __forceinline__ u64 make_key(float d, uint32_t id) {
@@ -199,6 +205,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Concurrent mode (NEXT-2, DevState::conc): loads of directory lengths / bitmaps
+// with acquire semantics (a set validity bit then guarantees the slot's payload,
+// id and ATT writes, published by the writer's fence + atomicOr), and
+// the generic -> async proxy fence before bulk copies read such slots.
+__device__ __forceinline__ uint32_t ld_acq_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_state_u32(const uint32_t* p, int conc) {
+  return conc ? ld_acq_u32(p) : *p;
+}
+__device__ __forceinline__ int32_t ld_state_s32(const int32_t* p, int conc) {
+  return conc ? (int32_t)ld_acq_u32(reinterpret_cast<const uint32_t*>(p)) : *p;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {

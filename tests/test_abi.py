@@ -58,7 +58,7 @@ def test_arena_bytes_and_validation(L):
     c.flags = S.CFG_NO_SCAN_COPY  # no scan records: exactly 46,024 x (32 x 128 x 2 + 256) bytes less
     assert L.sivf_arena_bytes(ctypes.byref(c), ctypes.byref(n)) == 0
     assert full - n.value == 46_024 * (32 * 128 * 2 + 256)  # fp16 copy + the records' norm and id copies
-    c.flags = 2  # unknown flag bit
+    c.flags = 4  # unknown flag bit
     assert L.sivf_arena_bytes(ctypes.byref(c), ctypes.byref(n)) == -1
     c.flags = 0
     c.max_k = 129
