@@ -118,7 +118,10 @@ __global__ void k_dump_att(DevState st, int32_t* __restrict__ list_of_id, unsign
       const uint64_t id = (uint64_t)u * st.G + st.rank;
       ok = ((st.bitmap[s] >> o) & 1u) && st.slab_ids[(size_t)s * kSlot + o] == (uint32_t)id && l >= 0;
     }
-    if (!ok && viol) atomicAdd(viol, 1ull);
+    if (!ok && viol) {
+      atomicAdd(viol, 1ull);
+      atomicAdd(viol + 2, 1ull);  // by type (sivf_debug_violations): ATT entry -> slot
+    }
   }
   if (list_of_id) list_of_id[u] = l;
 }
@@ -139,15 +142,15 @@ __global__ void k_dump_lists(DevState st, long long* __restrict__ live_per_list,
     if (lane == 0) {
       live += __popc(bm);
       atomicAdd(&mark[s], 1u);
-      if (st.slab_list[s] != l) bad++;
-      if (cur > 32u || (cur < 32u && (bm >> cur) != 0u)) bad++;  // bits only below the cursor
-      if (j + 1 < len && cur != 32u) bad++;                       // only the tail may be partial
+      if (st.slab_list[s] != l) { bad++; atomicAdd(viol + 3, 1ull); }
+      if (cur > 32u || (cur < 32u && (bm >> cur) != 0u)) { bad++; atomicAdd(viol + 4, 1ull); }  // bits below the cursor
+      if (j + 1 < len && cur != 32u) { bad++; atomicAdd(viol + 5, 1ull); }  // only the tail may be partial
     }
     if ((bm >> lane) & 1u) {  // every valid slot maps back through the ATT
       const uint32_t id = st.slab_ids[(size_t)s * kSlot + lane];
       const bool mine = (int64_t)id < st.cap && (int64_t)(id % st.G) == st.rank;
       const uint64_t want = ((uint64_t)(uint32_t)s << 32) | (uint32_t)lane;
-      if (!mine || st.att[id / st.G] != want) bad++;
+      if (!mine || st.att[id / st.G] != want) { bad++; atomicAdd(viol + 6, 1ull); }
     }
   }
   bad = __reduce_add_sync(kFull, bad);
@@ -174,10 +177,16 @@ __global__ void k_dump_free(DevState st, uint32_t* __restrict__ mark, unsigned l
 __global__ void k_dump_marks(DevState st, const uint32_t* __restrict__ mark, unsigned long long* __restrict__ viol,
                              const unsigned long long* __restrict__ live_sum) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s == 0 && *live_sum != st.ctr[C_LIVE]) atomicAdd(viol, 1ull);  // sum popc == live counter
+  if (s == 0 && *live_sum != st.ctr[C_LIVE]) {  // sum popc == live counter
+    atomicAdd(viol, 1ull);
+    atomicAdd(viol + 7, 1ull);
+  }
   if (s >= st.num_slabs) return;
   // each slab: exactly one directory, or the free stack, or leaked by a concurrent insert (awaiting reclaim)
-  if (mark[s] != 1u && !(mark[s] == 0u && st.slab_list[s] == kSlabLeaking)) atomicAdd(viol, 1ull);
+  if (mark[s] != 1u && !(mark[s] == 0u && st.slab_list[s] == kSlabLeaking)) {
+    atomicAdd(viol, 1ull);
+    atomicAdd(viol + 8, 1ull);
+  }
 }
 
 }  // namespace
@@ -208,7 +217,7 @@ cudaError_t launch_dump(Index& ix, int32_t* d_list_of_id, int64_t* d_live_per_li
   DevState& st = ix.st;
   unsigned long long* viol = reinterpret_cast<unsigned long long*>(ix.sc.tmp64);
   unsigned long long* live_sum = viol + 1;
-  cudaMemsetAsync(ix.sc.tmp64, 0, 2 * sizeof(long long), s);
+  cudaMemsetAsync(ix.sc.tmp64, 0, 9 * sizeof(long long), s);
   cudaMemsetAsync(ix.sc.slab_mark, 0, sizeof(uint32_t) * st.num_slabs, s);
   if (st.cap_local > 0) k_dump_att<<<ceil_div(st.cap_local, 256), 256, 0, s>>>(st, d_list_of_id, viol);
   k_dump_lists<<<ceil_div((int64_t)st.nlist * 32, 256), 256, 0, s>>>(

@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(256) k_insert_cas(DevState st, const int64_t* 
           if (len < cap) {
             const int e = ld_acquire_s32(&dir[len]);
             if (e >= 0) {  // an expansion published but not yet counted: help advance the length
+              __threadfence();  // release: the entry (seen by acquire) before the length
               atomicCAS(&st.dir_len[l], len, len + 1);
               continue;
             }
@@ -520,7 +521,10 @@ __global__ void __launch_bounds__(256) k_insert_cas(DevState st, const int64_t* 
               continue;
             }
           }
-          const int h = len > 0 ? dir[len - 1] : -1;
+          // the tail entry: a strong load (the length's acquire orders it after the
+          // entry's publication; a weak load could hit a stale L1 line)
+          const int h = len > 0 ? ld_acquire_s32(&dir[len - 1]) : -1;
+          if (len > 0 && h < 0) continue;  // unreachable: entries below the length are published slabs
           if (h >= 0) {
             const uint32_t c = ld_relaxed_u32(&st.cursor[h]);
             if (c < (uint32_t)kSlot) {
@@ -554,6 +558,7 @@ __global__ void __launch_bounds__(256) k_insert_cas(DevState st, const int64_t* 
           st.slab_list[sn] = l;
           __threadfence();  // slab metadata visible before the publication
           atomicExch(&dir[len], sn);              // publish the slab ...
+          __threadfence();                        // (release: the entry before the length)
           atomicCAS(&st.dir_len[l], len, len + 1);  // ... and the list end
           slab = sn;
           slot = 0;

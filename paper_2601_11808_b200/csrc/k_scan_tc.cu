@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           int sl = 0;
           uint32_t bm = 0u;
           if (j < len) {
-            sl = dir[j];
+            sl = ld_state_s32(&dir[j], st.conc);
             bm = ld_state_u32(&st.bitmap[sl], st.conc);
           }
           const unsigned live = __ballot_sync(kFull, bm != 0u);
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           int sl = 0;
           uint32_t bm = 0u, fl = 0u;
           if (j < rec.len) {
-            sl = dir[j];
+            sl = ld_state_s32(&dir[j], st.conc);
             bm = ld_state_u32(&st.bitmap[sl], st.conc);
             if (bm) fl = st.slab_flag[sl] & 3u;
           }

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) k_scan(ScanArgs a) {
         const int len = ld_state_s32(&st.dir_len[l], st.conc);
         const int32_t* dir = st.dir_arena + st.dir_off[l];
         for (int j = 0; j < len; ++j) {
-          const int s = dir[j];
+          const int s = ld_state_s32(&dir[j], st.conc);
           const uint32_t bm = ld_state_u32(&st.bitmap[s], st.conc);
           if (bm == 0u) continue;  // nothing valid in this slab
           if (st.conc) fence_proxy_async_global();  // the bitmap acquire orders the copies (NEXT-2)

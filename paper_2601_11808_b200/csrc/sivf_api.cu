@@ -407,7 +407,7 @@ sivf_rc sivf_reserve_directories(sivf_index h, int32_t spare, sivf_stream_t stre
   Index* ix = reinterpret_cast<Index*>(h);
   if (ix->view) return SIVF_E_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  int32_t* d_fail = reinterpret_cast<int32_t*>(ix->sc.tmp64 + 8);
+  int32_t* d_fail = reinterpret_cast<int32_t*>(ix->sc.tmp64 + 15);
   cudaMemsetAsync(d_fail, 0, 4, s);
   cudaError_t e = launch_reserve_dirs(*ix, spare, d_fail, s);
   int32_t fail = 0;
@@ -683,6 +683,15 @@ sivf_rc sivf_dump_state(sivf_index h, int32_t* d_list_of_id, int64_t* d_live_per
   if (reinterpret_cast<Index*>(h)->view) return SIVF_E_INVALID_ARG;  // quiescent, owner only
   return cuda_rc(launch_dump(*reinterpret_cast<Index*>(h), d_list_of_id, d_live_per_list, d_violations,
                              reinterpret_cast<cudaStream_t>(stream)));
+}
+
+// debug (not in sivf.h): the last sivf_dump_state's violations by type: [ATT entry ->
+// slot, slab_list, bits above the cursor, partial non-tail slab, slot -> ATT, live sum,
+// slab marks]; synchronises the device
+extern "C" int sivf_debug_violations(sivf_index h, int64_t* host7) {
+  if (!h || !host7) return SIVF_E_INVALID_ARG;
+  return cudaMemcpy(host7, reinterpret_cast<Index*>(h)->sc.tmp64 + 2, 7 * 8, cudaMemcpyDeviceToHost) == cudaSuccess
+             ? SIVF_OK : SIVF_E_CUDA;
 }
 
 sivf_rc sivf_dump_att(sivf_index h, uint64_t* d_att, sivf_stream_t stream) {
