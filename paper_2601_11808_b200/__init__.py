@@ -15,7 +15,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SIVF_LIB_PATH") or os.path.join(_HERE, "lib", "libsivf.so")  # override: experiments
+_DEFAULT_LIB = os.path.join(_HERE, "lib", "libsivf.so")
+LIB_PATH = os.environ.get("SIVF_LIB_PATH") or _DEFAULT_LIB  # override: experiments
 
 ST_OK, ST_POOL_EXHAUSTED, ST_DUPLICATE, ST_ID_OUT_OF_RANGE, ST_WRONG_SHARD = 0, 1, 2, 3, 4
 ST_DIR_FULL, ST_RETRY_LIMIT = 5, 6  # sivf_insert_concurrent only
@@ -114,6 +115,8 @@ def lib():
             raise RuntimeError(f"{LIB_PATH} is missing; build it with `make sivf` (nvcc, sm_100a)")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in EXPORTS.items():
+            if LIB_PATH != _DEFAULT_LIB and not hasattr(L, name):
+                continue  # experiments (SIVF_LIB_PATH): an older build may lack newer entry points
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

@@ -237,7 +237,9 @@ __device__ unsigned long long g_scnt[4];  // slow-path entries, survivors, inser
 //   the other set processes g + 1, then both arrive on acc_free and stage_free
 //   (the stage is refilled only after its group's epilogue, so the producer
 //   can run nst groups ahead of the epilogue, nst up to MAXST).
-template <int KP>
+// CONC: concurrent mode (DevState::conc, NEXT-2): acquire loads of directory entries and
+// bitmaps, the async-proxy fence before record copies, L2-coherent payload loads
+template <int KP, bool CONC>
 __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       ItemRec r{-1, 0, 0, 0, -1, 0, 0, 0};
       if (w < ntiles) {
         const int l = a.work_l[w];
-        const int len = ld_state_s32(&st.dir_len[l], st.conc);
+        const int len = ld_state_s32(&st.dir_len[l], CONC);
         const int32_t* dir = st.dir_arena + st.dir_off[l];
         uint2* rec = irec + slot * MAXS;
         int npre = 0, j0 = 0;
@@ -326,8 +328,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           int sl = 0;
           uint32_t bm = 0u;
           if (j < len) {
-            sl = ld_state_s32(&dir[j], st.conc);
-            bm = ld_state_u32(&st.bitmap[sl], st.conc);
+            sl = ld_state_s32(&dir[j], CONC);
+            bm = ld_state_u32(&st.bitmap[sl], CONC);
           }
           const unsigned live = __ballot_sync(kFull, bm != 0u);
           if (npre + __popc(live) > MAXS) break;  // the producer walks the rest
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&full[stg], (a.dbg & 8) ? 0u : (uint32_t)nvalid * rbytes);
       __syncwarp();
-      if (st.conc) fence_proxy_async_global();  // the bitmap acquire orders the record copies (NEXT-2)
+      if (CONC) fence_proxy_async_global();  // the bitmap acquire orders the record copies (NEXT-2)
       if (lane < nvalid && !(a.dbg & 8))
         bulk_g2s(stage_x(stg) + (size_t)lane * rbytes, reinterpret_cast<const unsigned char*>(st.payload16) +
                                                            (size_t)sl * rbytes, rbytes, &full[stg]);
@@ -403,8 +405,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           int sl = 0;
           uint32_t bm = 0u, fl = 0u;
           if (j < rec.len) {
-            sl = ld_state_s32(&dir[j], st.conc);
-            bm = ld_state_u32(&st.bitmap[sl], st.conc);
+            sl = ld_state_s32(&dir[j], CONC);
+            bm = ld_state_u32(&st.bitmap[sl], CONC);
             if (bm) fl = st.slab_flag[sl] & 3u;
           }
           const unsigned live = __ballot_sync(kFull, bm != 0u);
@@ -704,7 +706,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
                   const float* qr = a.Q + (int64_t)qglob * st.D;
                   float acc = 0.f;
                   for (int i4 = 0; i4 < nq4; ++i4) {
-                    const float4 xv = __ldcg(reinterpret_cast<const float4*>(xs + pay_off(Dp, c, i4)));
+                    const float4* xp = reinterpret_cast<const float4*>(xs + pay_off(Dp, c, i4));
+                    // concurrent mode: L2-coherent loads (a texture-cache line read earlier in
+                    // this launch may predate the slot's publication)
+                    const float4 xv = CONC ? __ldcg(xp) : __ldg(xp);
                     float qv[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) qv[e] = 4 * i4 + e < st.D ? __ldg(qr + 4 * i4 + e) : 0.f;
@@ -887,15 +892,17 @@ bool scan_tc_supported(const Index& ix, int k) {
 cudaError_t setup_scan_tc(Index& ix) {
   if (ix.st.Dh == 0 || ix.st.Dh > 128) return cudaSuccess;
   cudaError_t e = cudaSuccess;
-  if (tc_stages(ix, 10) >= 2)
-    e = cudaFuncSetAttribute(k_scan_tc<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc_plan(ix.st.Dh, tc_stages(ix, 10), 10).total);
-  if (e == cudaSuccess && tc_stages(ix, 16) >= 2)
-    e = cudaFuncSetAttribute(k_scan_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc_plan(ix.st.Dh, tc_stages(ix, 16), 16).total);
-  if (e == cudaSuccess && tc_stages(ix, 32) >= 2)
-    e = cudaFuncSetAttribute(k_scan_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc_plan(ix.st.Dh, tc_stages(ix, 32), 32).total);
+#define SIVF_TC_ATTR(KPV)                                                                                   \
+  if (e == cudaSuccess && tc_stages(ix, KPV) >= 2) {                                                        \
+    const int sm = (int)tc_plan(ix.st.Dh, tc_stages(ix, KPV), KPV).total;                                   \
+    e = cudaFuncSetAttribute(k_scan_tc<KPV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);       \
+    if (e == cudaSuccess)                                                                                   \
+      e = cudaFuncSetAttribute(k_scan_tc<KPV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);      \
+  }
+  SIVF_TC_ATTR(10)
+  SIVF_TC_ATTR(16)
+  SIVF_TC_ATTR(32)
+#undef SIVF_TC_ATTR
   return e;
 }
 
@@ -905,9 +912,17 @@ cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaS
   const int nst = tc_stages(ix, KP);
   TcArgs a{ix.st, d_q, nprobe, k, nst, sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n, sc.partial, sc.gthr, phase, ix.dbg};
   const size_t smem = tc_plan(ix.st.Dh, nst, KP).total;
-  if (KP == 10) k_scan_tc<10><<<ix.num_sms, TTHREADS, smem, s>>>(a);
-  else if (KP == 16) k_scan_tc<16><<<ix.num_sms, TTHREADS, smem, s>>>(a);
-  else k_scan_tc<32><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+  const bool conc = ix.st.conc != 0;
+  if (KP == 10) {
+    if (conc) k_scan_tc<10, true><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+    else k_scan_tc<10, false><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+  } else if (KP == 16) {
+    if (conc) k_scan_tc<16, true><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+    else k_scan_tc<16, false><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+  } else {
+    if (conc) k_scan_tc<32, true><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+    else k_scan_tc<32, false><<<ix.num_sms, TTHREADS, smem, s>>>(a);
+  }
   ix.launches += 1;
   return cudaGetLastError();
 }

@@ -322,6 +322,43 @@ __global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs
   pairs[atomicAdd(&cursor[b * nlist + probes[i]], 1)] = (int32_t)i;
 }
 
+// Block-aggregated scatter (nb * nlist <= kScatterEnt): a block of 1024 threads x 4
+// pairs ranks its pairs per entry with shared-memory atomics, reserves each entry's
+// range with ONE global atomicAdd per (block, entry) and writes the pairs: ~50x fewer
+// contended global atomics than one per pair (every list receives ~nq nprobe / nlist).
+constexpr int kScatterEnt = 12288, kScatterPPT = 4;  // 48 KB of static shared memory
+__global__ void __launch_bounds__(1024) k_inv_scatter_blk(const int32_t* __restrict__ probes, int64_t npairs,
+                                                         int nprobe, int nb, int r0, int nlist,
+                                                         int32_t* __restrict__ cursor, int32_t* __restrict__ pairs) {
+  __shared__ int32_t hist[kScatterEnt];
+  const int nent = nb * nlist;
+  for (int e = threadIdx.x; e < nent; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * blockDim.x * kScatterPPT;
+  int ent[kScatterPPT], loc[kScatterPPT];
+#pragma unroll
+  for (int u = 0; u < kScatterPPT; ++u) {
+    const int64_t i = base + (int64_t)u * blockDim.x + threadIdx.x;
+    ent[u] = -1;
+    if (i < npairs) {
+      const int p = (int)(i % nprobe);
+      ent[u] = ((nb == 2 && p >= r0) ? nlist : 0) + probes[i];
+      loc[u] = atomicAdd(&hist[ent[u]], 1);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+    const int c = hist[e];
+    if (c) hist[e] = atomicAdd(&cursor[e], c);  // the entry's range for this block
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kScatterPPT; ++u) {
+    const int64_t i = base + (int64_t)u * blockDim.x + threadIdx.x;
+    if (ent[u] >= 0) pairs[hist[ent[u]] + loc[u]] = (int32_t)i;
+  }
+}
+
 // Warp per query, nprobe <= 32, k <= KM: lane p holds probe p's sorted partial list in
 // registers; k rounds of a warp-wide minimum over the list heads, the winning lane
 // shifts its list (static register moves, no local memory).  Same result as k_merge.
@@ -497,6 +534,10 @@ cudaError_t launch_search_front(Index& ix, const SearchPlan& p, const float* d_q
   }
   k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, p.QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.sctr, nlist,
                                 sc.work_l, sc.work_p0, sc.work_n);
+  if (nent <= kScatterEnt && !(ix.dbg & 4096)) {  // dbg 4096 (experiments): the per-pair scatter
+    k_inv_scatter_blk<<<ceil_div(npairs, 1024 * kScatterPPT), 1024, 0, s>>>(sc.probes, npairs, nprobe, p.nb, p.r0,
+                                                                            nlist, sc.inv_cursor, sc.inv_pairs);
+  } else
   k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, p.nb, p.r0, nlist, sc.inv_cursor,
                                                        sc.inv_pairs);
   ix.launches += 2;
