@@ -37,8 +37,8 @@ N_BASE, DIM, NLIST, BATCH, NQ, K, NPROBE = 1_000_000, 128, 1024, 10_000, 10_000,
 N_TRAIN, N_ITER, SEED = 262_144, 20, 0x51F7
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_scan_tc launch, from the committed ncu
 # --set full capture of this bench step (per launch; compare with roofline.hbm_view).
-SCAN_TRAFFIC_NCU = 571.754496e6 + 25.640192e6
-SCAN_TRAFFIC_SRC = "profiles/r01s10_scan_full.txt (ncu --set full, bench.py --steps 1 --warmup 1 --no-sweep --no-cpu --no-extra)"
+SCAN_TRAFFIC_NCU = 576.274944e6 + 25.813248e6
+SCAN_TRAFFIC_SRC = "profiles/r02zd_scan_full.txt (ncu --set full, bench.py --steps 1 --warmup 1 --no-sweep --no-cpu --no-extra)"
 WORKLOAD = ("SIFT1M-shaped sliding step: 1M x 128 fp32 live window, nlist=1024; per step insert 10k new + "
             "delete 10k oldest + search 10k queries (k=10, nprobe=32) + reclaim")
 
@@ -570,11 +570,11 @@ def run_sivf(args):
         fl = latency_floors(S, dev, log)
         hop_us = fl["dram_dependent_load_ns"] / 1e3
         k_step = launches / Kst if Kst else 0
-        # the phase timers bracket ops inside a busy stream: the floor of one kernel there is
-        # empty_launch_busy_stream_us (events included)
-        floor_del = fl["empty_launch_busy_stream_us"] + 2 * hop_us  # ATT read -> atomicAnd on the bitmap word
+        # the phase timers bracket ops inside a stream of work: the floor of one kernel there is
+        # launch_in_stream_us (back-to-back launches)
+        floor_del = fl["launch_in_stream_us"] + 2 * hop_us  # ATT read -> atomicAnd on the bitmap word
         n_ins = 9  # claim, rows_tiles, gemm, select, chunk_rank, chunk_prefix, reserve, dir_update, append
-        floor_ins = fl["empty_launch_busy_stream_us"] + (n_ins - 1) * fl["launch_in_stream_us"] + n_ins * hop_us
+        floor_ins = n_ins * (fl["launch_in_stream_us"] + hop_us)
         floor_step = fl["graph_replay_1_kernel_us"] + (k_step - 1) * fl["graph_node_us"] + k_step * hop_us
         meas_ins = (ph_ms["assign"] + ph_ms["append"]) * 1e3
         lat = {"floors": fl,
@@ -677,11 +677,11 @@ def _ev():
 def latency_floors(S, dev, log):
     """SURVEY §8(d) "Latency roofline for small batches": the floors a small-batch op cannot
     beat, measured on this GPU with CUDA events: one empty kernel bracketed by events on an
-    idle stream, and on a busy stream (between two runs of 50 back-to-back launches: how the
-    phase timers see one kernel inside a step), the per-launch time of 200 back-to-back empty
-    kernels, one CUDA-graph replay of one empty kernel and the per-node time of a replayed
-    20-kernel chain, and the dependent-load latency (one thread chasing a random single-cycle
-    permutation: 1 GB, far beyond the 126 MB L2 = DRAM; 4 MB = L2)."""
+    idle stream (host-visible launch latency), the per-launch time of 200 back-to-back empty
+    kernels on one stream (the floor of one kernel inside a stream of work), one CUDA-graph
+    replay of one empty kernel and the per-node time of a replayed 20-kernel chain, and the
+    dependent-load latency (one thread chasing a random single-cycle permutation: 1 GB, far
+    beyond the 126 MB L2 = DRAM; 4 MB = L2)."""
     import torch
 
     def med_ms(fn, reps=30):
@@ -699,17 +699,6 @@ def latency_floors(S, dev, log):
     torch.cuda.synchronize()
     one = med_ms(lambda: S.probe_launch(1))
     many = med_ms(lambda: S.probe_launch(200), reps=10) / 200
-    busy = []
-    for _ in range(30):
-        a, b = _ev(), _ev()
-        S.probe_launch(50)
-        a.record()
-        S.probe_launch(1)
-        b.record()
-        S.probe_launch(50)
-        torch.cuda.synchronize()
-        busy.append(a.elapsed_time(b))
-    busy = statistics.median(busy)
     g1, g20 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     side = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(side):
@@ -736,8 +725,7 @@ def latency_floors(S, dev, log):
         hops[name] = t * 1e6 / 4000  # ns per dependent load
         del nxt
     torch.cuda.empty_cache()
-    res = {"empty_launch_us": one * 1e3, "empty_launch_busy_stream_us": busy * 1e3,
-           "launch_in_stream_us": many * 1e3, "graph_replay_1_kernel_us": rep1 * 1e3,
+    res = {"empty_launch_us": one * 1e3, "launch_in_stream_us": many * 1e3, "graph_replay_1_kernel_us": rep1 * 1e3,
            "graph_node_us": (rep20 - rep1) / 19 * 1e3, "dram_dependent_load_ns": hops["dram"],
            "l2_dependent_load_ns": hops["l2"]}
     log("latency floors: " + ", ".join(f"{k} {v:.2f}" for k, v in res.items()))
