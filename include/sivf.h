@@ -102,7 +102,7 @@ typedef struct {
   int64_t device_errors;        /* sticky internal errors (unreachable directory-arena overflow); must stay 0 */
   double overhead_paper;        /* 128/(32*(4d+8)): the paper's per-slab header accounting (reading C17) */
   double overhead_actual;       /* this build: (16 B metadata/slab * slabs_in_use + 8 B * id slots) / (live payload+id bytes) */
-  double overhead_scan_copy;    /* the scan records (fp16 copy 2 Dh B + norm and id copies 8 B per slot of slabs_in_use) / (live payload+id bytes); 0 without */
+  double overhead_scan_copy;    /* the scan copy of slabs_in_use / (live payload+id bytes): D <= 128 the fp16 records (2 Dh B + norm and id 8 B per slot), D > 128 the split-fp16 copy (4 Dg B + scale 4 B per slot); 0 without */
   int64_t dir_compactions;      /* times the list directories were repacked into the idle arena half (k_reserve) */
   int64_t leaked_slabs;         /* slabs leaked by lost publication CASes of sivf_insert_concurrent */
   int64_t leaked_recycled;      /* of those, returned to the pool by sivf_reclaim */

@@ -24,6 +24,40 @@ namespace sivf {
 
 namespace {
 
+// The split-fp16 scan copy of one vector (D > 128; warp per vector, recg_off()):
+// e = 15 - exponent(max |x|) puts every scaled value below 2^15 (finite in fp16),
+// x 2^e = hi + lo with hi = fp16_rn(x 2^e) and lo = fp16_rn(x 2^e - hi) (the
+// difference is exact in fp32); slab_xs = 2^-e undoes the scale.
+__device__ __forceinline__ void append_split_copy(const DevState& st, int slab, int o, const float* xr, int lane) {
+  float mx = 0.f;
+  for (int d = lane; d < st.D; d += 32) mx = fmaxf(mx, fabsf(xr[d]));
+  mx = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(mx)));  // non-negative: uint order
+  int e = 0;
+  if (mx > 0.f && mx <= 3.4e38f) {
+    int ex;
+    frexpf(mx, &ex);  // mx in [2^(ex-1), 2^ex)
+    e = 15 - ex;
+    e = e < -120 ? -120 : e > 120 ? 120 : e;
+  }
+  unsigned char* base = reinterpret_cast<unsigned char*>(st.payload_g) + (size_t)slab * recg_bytes(st.Dg);
+  for (int c8 = lane; c8 < (st.Dg >> 3); c8 += 32) {
+    uint32_t hw[4], lw[4];
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      const int d = 8 * c8 + 2 * e2;
+      const float s0 = ldexpf(d < st.D ? xr[d] : 0.f, e), s1 = ldexpf(d + 1 < st.D ? xr[d + 1] : 0.f, e);
+      const __half h0 = __float2half_rn(s0), h1 = __float2half_rn(s1);
+      const __half l0 = __float2half_rn(s0 - __half2float(h0)), l1 = __float2half_rn(s1 - __half2float(h1));
+      const __half2 hh = __halves2half2(h0, h1), ll = __halves2half2(l0, l1);
+      hw[e2] = *reinterpret_cast<const uint32_t*>(&hh);
+      lw[e2] = *reinterpret_cast<const uint32_t*>(&ll);
+    }
+    *reinterpret_cast<uint4*>(base + recg_off(st.Dg, o, 8 * c8, 0)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(base + recg_off(st.Dg, o, 8 * c8, 1)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+  }
+  if (lane == 0) st.slab_xs[(size_t)slab * kSlot + o] = ldexpf(1.f, -e);
+}
+
 __global__ void k_claim(DevState st, const int64_t* __restrict__ ids, int64_t n, int32_t* __restrict__ status,
                         int64_t* __restrict__ lid_out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -382,6 +416,7 @@ __global__ void __launch_bounds__(256) k_append(DevState st, const int64_t* __re
         if (dst16)  // zero dims [Dp, Dh) of the fp16 copy
           for (int c4 = nc4 + lane; c4 < (st.Dh >> 2); c4 += 32)
             *reinterpret_cast<uint2*>(dst16 + pay16_off(st.Dh, o, c4 >> 1) + 4 * (c4 & 1)) = make_uint2(0u, 0u);
+        if (st.payload_g) append_split_copy(st, slab, o, xr, lane);
 #pragma unroll
         for (int off = 16; off; off >>= 1) nrm += __shfl_xor_sync(kFull, nrm, off);
         integral = __all_sync(kFull, integral);
@@ -599,6 +634,7 @@ __global__ void __launch_bounds__(256) k_insert_cas(DevState st, const int64_t* 
       if (dst16)
         for (int c4 = nc4 + lane; c4 < (st.Dh >> 2); c4 += 32)
           *reinterpret_cast<uint2*>(dst16 + pay16_off(st.Dh, slot, c4 >> 1) + 4 * (c4 & 1)) = make_uint2(0u, 0u);
+      if (st.payload_g) append_split_copy(st, slab, slot, xr, lane);
 #pragma unroll
       for (int off = 16; off; off >>= 1) nrm += __shfl_xor_sync(kFull, nrm, off);
       integral = __all_sync(kFull, integral);

@@ -238,7 +238,8 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
                                                    int32_t* __restrict__ off, int32_t* __restrict__ cursor,
                                                    int32_t* __restrict__ tile_off, int32_t* __restrict__ ictr,
                                                    int nlist, int32_t* __restrict__ work_l,
-                                                   int32_t* __restrict__ work_p0, int32_t* __restrict__ work_n) {
+                                                   int32_t* __restrict__ work_p0, int32_t* __restrict__ work_n,
+                                                   int32_t* __restrict__ item_of) {
   __shared__ int32_t ws[2][32];
   __shared__ int32_t carry[2];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -309,17 +310,22 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
       work_l[tt] = e % nlist;
       work_p0[tt] = off[e] + j * QT;
       work_n[tt] = min(QT, c - j * QT);
+      if (item_of)  // inverse-map position -> work item (k_gs_select)
+        for (int u = 0; u < work_n[tt]; ++u) item_of[off[e] + j * QT + u] = tt;
     }
   }
 }
 
 __global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs, int nprobe, int nb, int r0,
-                              int nlist, int32_t* __restrict__ cursor, int32_t* __restrict__ pairs) {
+                              int nlist, int32_t* __restrict__ cursor, int32_t* __restrict__ pairs,
+                              int32_t* __restrict__ pair_pos) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npairs) return;
   const int p = (int)(i % nprobe);
   const int b = (nb == 2 && p >= r0) ? 1 : 0;
-  pairs[atomicAdd(&cursor[b * nlist + probes[i]], 1)] = (int32_t)i;
+  const int pos = atomicAdd(&cursor[b * nlist + probes[i]], 1);
+  pairs[pos] = (int32_t)i;
+  if (pair_pos) pair_pos[i] = pos;
 }
 
 // Block-aggregated scatter (nb * nlist <= kScatterEnt): a block of 1024 threads x 4
@@ -329,7 +335,8 @@ __global__ void k_inv_scatter(const int32_t* __restrict__ probes, int64_t npairs
 constexpr int kScatterEnt = 12288, kScatterPPT = 4;  // 48 KB of static shared memory
 __global__ void __launch_bounds__(1024) k_inv_scatter_blk(const int32_t* __restrict__ probes, int64_t npairs,
                                                          int nprobe, int nb, int r0, int nlist,
-                                                         int32_t* __restrict__ cursor, int32_t* __restrict__ pairs) {
+                                                         int32_t* __restrict__ cursor, int32_t* __restrict__ pairs,
+                                                         int32_t* __restrict__ pair_pos) {
   __shared__ int32_t hist[kScatterEnt];
   const int nent = nb * nlist;
   for (int e = threadIdx.x; e < nent; e += blockDim.x) hist[e] = 0;
@@ -355,7 +362,10 @@ __global__ void __launch_bounds__(1024) k_inv_scatter_blk(const int32_t* __restr
 #pragma unroll
   for (int u = 0; u < kScatterPPT; ++u) {
     const int64_t i = base + (int64_t)u * blockDim.x + threadIdx.x;
-    if (ent[u] >= 0) pairs[hist[ent[u]] + loc[u]] = (int32_t)i;
+    if (ent[u] >= 0) {
+      pairs[hist[ent[u]] + loc[u]] = (int32_t)i;
+      if (pair_pos) pair_pos[i] = hist[ent[u]] + loc[u];
+    }
   }
 }
 
@@ -463,9 +473,15 @@ bool scan_tc_supported(const Index& ix, int k);
 cudaError_t setup_scan_tc(Index& ix);
 cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s, int phase);
 int scan_tc_tile();
+bool scan_gs_supported(const Index& ix);
+cudaError_t setup_scan_gs(Index& ix);
+cudaError_t launch_scan_gs(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s);
+cudaError_t launch_select_gs(Index& ix, const float* d_q, int64_t nq, int k, int nprobe, float* d_dist,
+                             int64_t* d_ids, cudaStream_t s);
 
 cudaError_t setup_search_kernels(Index& ix) {
   cudaError_t e = setup_scan_tc(ix);
+  if (e == cudaSuccess) e = setup_scan_gs(ix);
   if (e != cudaSuccess) return e;
   for (int nw : {8, 4, 2}) {
     size_t need = scan_smem_bytes(nw, ix.st.Dp, ix.cfg.max_k);
@@ -482,9 +498,10 @@ SearchPlan plan_search(const Index& ix, int64_t nq, int32_t k, int32_t nprobe) {
   SearchPlan p{};
   const int nlist = ix.st.nlist;
   p.tc = ix.use_tc_scan && scan_tc_supported(ix, k);
-  p.smem = p.tc ? 0 : scan_smem_for(ix, k, &p.nw);
-  p.ok = p.tc || p.nw != 0;
-  p.QT = p.tc ? scan_tc_tile() : kQPW * p.nw;
+  p.gs = !p.tc && ix.use_tc_scan && scan_gs_supported(ix);
+  p.smem = p.tc || p.gs ? 0 : scan_smem_for(ix, k, &p.nw);
+  p.ok = p.tc || p.gs || p.nw != 0;
+  p.QT = p.tc ? scan_tc_tile() : p.gs ? 128 : kQPW * p.nw;
   // Tensor-core path: probe-rank buckets, one scan launch.  Work items are laid
   // out bucket-major, so with nb = 2 every query's r0 nearest lists are scanned
   // first and its k-th distance bound is tight before the other lists are
@@ -533,13 +550,14 @@ cudaError_t launch_search_front(Index& ix, const SearchPlan& p, const float* d_q
     ix.launches += 1;
   }
   k_inv_scan<<<1, 1024, 0, s>>>(sc.inv_cnt, nent, p.QT, sc.inv_off, sc.inv_cursor, sc.tile_off, ix.st.sctr, nlist,
-                                sc.work_l, sc.work_p0, sc.work_n);
+                                sc.work_l, sc.work_p0, sc.work_n, p.gs ? sc.item_of : nullptr);
+  int32_t* pair_pos = p.gs ? sc.pair_pos : nullptr;
   if (nent <= kScatterEnt && !(ix.dbg & 4096)) {  // dbg 4096 (experiments): the per-pair scatter
     k_inv_scatter_blk<<<ceil_div(npairs, 1024 * kScatterPPT), 1024, 0, s>>>(sc.probes, npairs, nprobe, p.nb, p.r0,
-                                                                            nlist, sc.inv_cursor, sc.inv_pairs);
+                                                                            nlist, sc.inv_cursor, sc.inv_pairs, pair_pos);
   } else
   k_inv_scatter<<<ceil_div(npairs, 256), 256, 0, s>>>(sc.probes, npairs, nprobe, p.nb, p.r0, nlist, sc.inv_cursor,
-                                                       sc.inv_pairs);
+                                                       sc.inv_pairs, pair_pos);
   ix.launches += 2;
   return cudaGetLastError();
 }
@@ -553,7 +571,9 @@ cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q,
   const int grid = ix.num_sms;  // persistent: one CTA per SM
   {
     PhaseTimer pt(ix, SIVF_PH_SCAN, s);
-    if (p.tc) {
+    if (p.gs) {
+      e = launch_scan_gs(ix, d_q, k, nprobe, s);
+    } else if (p.tc) {
       e = launch_seed_bound(ix, d_q, nq, k, nprobe, s);  // after the front reset gthr to +inf
       if (e == cudaSuccess && p.nb == 2 && ix.tc_two_phase) {
         // two launches: every query's r0 nearest lists complete (and its k-th
@@ -570,12 +590,13 @@ cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q,
     } else {
       k_scan<2><<<grid, 32 * 3, p.smem, s>>>(a);
     }
-    if (!p.tc) ix.launches += 1;
+    if (!p.tc && !p.gs) ix.launches += 1;
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return e;  // a failed scan launch must not be masked by the merge below
   }
   if (after_scan) cudaEventRecord(after_scan, s);  // the index is no longer read by this search
   PhaseTimer pt(ix, SIVF_PH_MERGE, s);
+  if (p.gs) return launch_select_gs(ix, d_q, nq, k, nprobe, d_dist, d_ids, s);
   const int wpb = 4;
   if (nprobe <= 32 && k <= 16) {
     if (k <= 10) k_merge_regs<10><<<ceil_div(nq, 4), 128, 0, s>>>(sc.partial, nq, nprobe, k, d_dist, d_ids);

@@ -15,7 +15,7 @@ constexpr size_t kAlign = 256;
 
 struct Layout {
   size_t total = 0;
-  size_t payload, payload16, slab_ids, slab_norm, slab_flag, bitmap, cursor, slab_list, free_stack, slab_mark, att, claim,
+  size_t payload, payload16, payload_g, slab_xs, slab_ids, slab_norm, slab_flag, bitmap, cursor, slab_list, free_stack, slab_mark, att, claim,
       dir_off, dir_len, dir_cap, dir_arena, centroids, ctr, ictr, sctr, tmp64, gthr;
   size_t row_list, row_rank, row_status, row_lid, row_best, chunk_hist, list_cnt, list_tail_free, list_tail_slab,
       list_granted, list_newbase, list_newoff;
@@ -25,7 +25,9 @@ struct Layout {
   int64_t q_rows;
   size_t x_tiles, x_norm, c_tiles, c_norm, c_csa, c_cnb, cand, cand_ubv, cand_cnt;
   int64_t tc_rows, cap_assign, cap_probe;
-  int64_t Dp, Dh, cap_local, dir_half, max_rows, max_chunks, coarse_rows, max_work;
+  size_t gs_a, gs_qn, gs_qs, item_doff, item_dlen, item_nlive, item_of, pair_pos, dense;
+  int64_t gs_items, dense_cap;
+  int64_t Dp, Dh, Dg, cap_local, dir_half, max_rows, max_chunks, coarse_rows, max_work;
 };
 
 size_t take(Layout& L, size_t bytes) {
@@ -57,6 +59,8 @@ Layout make_layout(const sivf_config* c, bool view = false) {
   L.Dp = (D + 7) / 8 * 8;  // tf32 MMA K-step = 8 dims
   // fp16 scan copy (kind::f16 K-step = 16 dims); none for D > 128 or SIVF_CFG_NO_SCAN_COPY
   L.Dh = (D <= 128 && !(c->flags & SIVF_CFG_NO_SCAN_COPY)) ? (D + 15) / 16 * 16 : 0;
+  // split-fp16 scan copy for D > 128 (k_scan_gs.cu, 64-dim K chunks)
+  L.Dg = (D > 128 && !(c->flags & SIVF_CFG_NO_SCAN_COPY)) ? (D + 63) / 64 * 64 : 0;
   const int64_t cap = c->id_capacity, G = c->shard_count, r = c->shard_rank;
   L.cap_local = cap > r ? (cap - r + G - 1) / G : 0;
   // directory arena: two halves; a compaction into the idle half needs at most
@@ -82,6 +86,8 @@ Layout make_layout(const sivf_config* c, bool view = false) {
   const size_t sv = view ? 0 : 1;  // state arrays: the owner's in a view
   L.payload = take(L, sv * (size_t)S * kSlot * L.Dp * 4);
   L.payload16 = take(L, L.Dh ? sv * (size_t)S * rec16_bytes((int)L.Dh) : 0);
+  L.payload_g = take(L, L.Dg ? sv * (size_t)S * recg_bytes((int)L.Dg) : 0);
+  L.slab_xs = take(L, L.Dg ? sv * (size_t)S * kSlot * 4 : 0);
   L.slab_ids = take(L, sv * (size_t)S * kSlot * 4);
   L.slab_norm = take(L, sv * (size_t)S * kSlot * 4);
   L.slab_flag = take(L, sv * (size_t)S * 4);
@@ -152,6 +158,26 @@ Layout make_layout(const sivf_config* c, bool view = false) {
   L.qx_tiles = take(L, (size_t)2 * L.q_rows * L.Dp * 4);
   L.qx_norm = take(L, (size_t)L.q_rows * 4);
   L.qcoarse = take(L, (size_t)L.q_rows * nl * 4);
+  // GEMM scan (D > 128, k_scan_gs.cu): per work item of <= 128 queries its split-fp16
+  // query tile, per pair its row of list distances in the dense buffer, sized for lists
+  // up to twice the average length (items beyond it take the SIMT fallback)
+  L.gs_items = L.Dg ? npairs / 128 + nl + 1 : 0;
+  L.gs_a = take(L, (size_t)L.gs_items * L.Dg * 512);
+  L.gs_qn = take(L, (size_t)L.gs_items * 128 * 4);
+  L.gs_qs = take(L, (size_t)L.gs_items * 128 * 4);
+  L.item_doff = take(L, L.Dg ? (size_t)(L.max_work + 1) * 8 : 0);
+  L.item_dlen = take(L, L.Dg ? (size_t)L.max_work * 4 : 0);
+  L.item_nlive = take(L, L.Dg ? (size_t)L.max_work * 4 : 0);
+  L.item_of = take(L, L.Dg ? (size_t)npairs * 4 + 4 : 0);
+  L.pair_pos = take(L, L.Dg ? (size_t)npairs * 4 + 4 : 0);
+  {
+    int64_t lavg = (2 * S + nl - 1) / nl;
+    if (lavg < 8) lavg = 8;
+    int64_t cap = L.Dg ? npairs * 33 * lavg + 4 * L.max_work : 0;
+    if (cap > ((int64_t)3 << 29)) cap = (int64_t)3 << 29;  // 6 GB
+    L.dense_cap = cap;
+    L.dense = take(L, (size_t)cap * 4);
+  }
   return L;
 }
 
@@ -235,6 +261,17 @@ void carve_scratch(Scratch& sc, void* d_arena, const Layout& L) {
   sc.cand_cnt = at<int32_t>(d_arena, L.cand_cnt);
   sc.cand_cap_assign = (int32_t)L.cap_assign;
   sc.cand_cap_probe = (int32_t)L.cap_probe;
+  sc.gs_items = L.gs_items;
+  sc.gs_a = at<uint16_t>(d_arena, L.gs_a);
+  sc.gs_qn = at<float>(d_arena, L.gs_qn);
+  sc.gs_qs = at<float>(d_arena, L.gs_qs);
+  sc.item_doff = at<int64_t>(d_arena, L.item_doff);
+  sc.item_dlen = at<int32_t>(d_arena, L.item_dlen);
+  sc.item_nlive = at<int32_t>(d_arena, L.item_nlive);
+  sc.item_of = at<int32_t>(d_arena, L.item_of);
+  sc.pair_pos = at<int32_t>(d_arena, L.pair_pos);
+  sc.dense = at<float>(d_arena, L.dense);
+  sc.dense_cap = L.dense_cap;
 }
 
 }  // namespace
@@ -299,6 +336,9 @@ sivf_rc sivf_create(const sivf_config* cfg, void* d_arena, size_t arena_bytes, s
   st.num_slabs = cfg->num_slabs;
   st.payload = at<float>(d_arena, L.payload);
   st.payload16 = L.Dh ? at<uint16_t>(d_arena, L.payload16) : nullptr;
+  st.Dg = (int32_t)L.Dg;
+  st.payload_g = L.Dg ? at<uint16_t>(d_arena, L.payload_g) : nullptr;
+  st.slab_xs = L.Dg ? at<float>(d_arena, L.slab_xs) : nullptr;
   st.slab_ids = at<uint32_t>(d_arena, L.slab_ids);
   st.slab_norm = at<float>(d_arena, L.slab_norm);
   st.slab_flag = at<uint32_t>(d_arena, L.slab_flag);
@@ -728,8 +768,10 @@ sivf_rc sivf_stats(sivf_index h, sivf_stats_t* out, sivf_stream_t stream) {
   const double live_bytes = (double)out->live * (4.0 * d + 4.0);
   out->overhead_actual =
       live_bytes > 0 ? (16.0 * out->slabs_in_use + 8.0 * (double)ix->st.cap_local) / live_bytes : 0.0;
-  out->overhead_scan_copy =
-      live_bytes > 0 && ix->st.Dh ? (double)rec16_bytes(ix->st.Dh) * (double)out->slabs_in_use / live_bytes : 0.0;
+  const double copy_bytes = ix->st.Dh ? (double)rec16_bytes(ix->st.Dh)
+                          : ix->st.Dg ? (double)recg_bytes(ix->st.Dg) + 4.0 * kSlot  // + the slots' scales
+                                      : 0.0;
+  out->overhead_scan_copy = live_bytes > 0 ? copy_bytes * (double)out->slabs_in_use / live_bytes : 0.0;
   return SIVF_OK;
 }
 

@@ -54,6 +54,18 @@ struct Scratch {
   // validation
   uint32_t* slab_mark = nullptr;    // [num_slabs]
   uint32_t* gthr = nullptr;         // [max_queries] per-query global k-th distance bound (fp32 bits)
+  // GEMM scan (D > 128, k_scan_gs.cu)
+  int64_t gs_items = 0;             // work items of <= 128 queries the query tiles are sized for
+  uint16_t* gs_a = nullptr;         // [gs_items][Dg/64][hi 16 KB | lo 16 KB] split-fp16 query tiles
+  float* gs_qn = nullptr;           // [gs_items][128] ||q||^2
+  float* gs_qs = nullptr;           // [gs_items][128] 2^-e_q
+  int64_t* item_doff = nullptr;     // [max_work + 1] item's region in dense (-1: SIMT fallback)
+  int32_t* item_dlen = nullptr;     // [max_work] directory length at planning (row stride = 32 dlen)
+  int32_t* item_nlive = nullptr;    // [max_work] live slabs scanned
+  int32_t* item_of = nullptr;       // [npairs] inverse-map position -> work item
+  int32_t* pair_pos = nullptr;      // [npairs] pair -> inverse-map position
+  float* dense = nullptr;           // [dense_cap] per item: slab ids (pad 4) + [rows][32 dlen] distances
+  int64_t dense_cap = 0;
   long long* tmp64 = nullptr;       // [16] small device scalars
   // tensor-core coarse quantisation (k_coarse_tc.cu)
   int64_t tc_rows = 0;              // rows per k_coarse_gemm pass
@@ -209,6 +221,7 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
 // k_search.cu
 struct SearchPlan {
   bool tc, ok;
+  bool gs;  // D > 128: the split-fp16 GEMM scan + per-query selection (k_scan_gs.cu)
   int nw, QT, nb, r0;
   size_t smem;
 };

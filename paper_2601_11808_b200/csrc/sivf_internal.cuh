@@ -36,6 +36,18 @@ __host__ __device__ __forceinline__ size_t rec16_norm_off(int Dh, int n) {
   return (size_t)(n >> 3) * rec16_sbo(Dh) + (size_t)16 * Dh + (n & 7) * 4;
 }
 __host__ __device__ __forceinline__ size_t rec16_id_off(int Dh, int n) { return rec16_norm_off(Dh, n) + 32; }
+// The split-fp16 scan copy of a slab for D > 128 (k_scan_gs.cu; Dg = D rounded
+// up to 64): x * 2^e_x (e_x per vector, slab_xs = 2^-e_x) = hi + lo, hi =
+// fp16_rn(x 2^e), lo = fp16_rn(x 2^e - hi).  Per slab 4 row groups x Dg/64
+// dim chunks, each chunk [hi: 8 K-cores x 8 slots x 8 halves = 1 KB][lo: 1 KB]:
+// one 2-KB piece per (row group, chunk) holds both halves of an UMMA B
+// operand slice (K-major SWIZZLE_NONE, LBO = 128 B, SBO = 2 KB in the stage).
+__host__ __device__ __forceinline__ size_t recg_bytes(int Dg) { return (size_t)128 * Dg; }
+// byte offset of (slot n, dim d, part: 0 hi / 1 lo) inside a slab's copy
+__host__ __device__ __forceinline__ size_t recg_off(int Dg, int n, int d, int part) {
+  return ((size_t)(n >> 3) * (Dg >> 6) + (d >> 6)) * 2048 + part * 1024 + ((d >> 3) & 7) * 128 + (n & 7) * 16 +
+         (d & 7) * 2;
+}
 // slab_flag bits
 constexpr uint32_t kFlagIntegral = 1u;  // every value an integer with |v| <= 2048 (exact in tf32 and fp16)
 constexpr uint32_t kFlagF16Over = 2u;   // some value has |v| > 65504 (no finite fp16 copy): scan re-ranks all
@@ -62,6 +74,9 @@ struct DevState {
   int64_t cap, cap_local, num_slabs;
   float* payload;        // [num_slabs][4][Dp/4][8][4]  see pay_off(): a slab is one UMMA B core-matrix block
   uint16_t* payload16;   // [num_slabs] scan records of rec16_bytes(Dh): fp16 (RN) copy + norms + ids, pay16_off()
+  int32_t Dg;            // split-fp16 scan copy dims for D > 128 (D rounded up to 64; 0 = no copy)
+  uint16_t* payload_g;   // [num_slabs] split-fp16 copies of recg_bytes(Dg), recg_off()
+  float* slab_xs;        // [num_slabs][32] 2^-e_x: the scale of each slot's split-fp16 copy
   uint32_t* slab_ids;    // [num_slabs][32] user ids (u32)
   float* slab_norm;      // [num_slabs][32] ||x||^2 (fp32), for the tensor-core distance expansion
   uint32_t* slab_flag;   // [num_slabs] bit0: every payload value is an integer with |x| <= 2048 (tf32-exact)
@@ -276,6 +291,15 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (fp16 A and B, fp32 accumulate).
+__device__ __forceinline__ void umma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32.
