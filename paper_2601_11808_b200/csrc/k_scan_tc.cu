@@ -518,9 +518,12 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       const ItemRec rec = items[slot];
       if (rec.l < 0) break;
       const uint32_t ab = i & 1u;
-      const bool rv = row < rec.nqt;
-      const bool wv = 32 * qw < rec.nqt && !(a.dbg & 16);  // warp-uniform: the warp has a real row
-      const int pair = rv ? a.inv_pairs[rec.p0 + row] : -1;
+      // TMEM lane 32 qw + lane holds the item's row 4 lane + qw: a partial tile's rows
+      // spread over the four lane quarters (the epilogue warps share its work evenly)
+      const int trow = 4 * lane + qw;
+      const bool rv = trow < rec.nqt;
+      const bool wv = qw < rec.nqt && !(a.dbg & 16);  // warp-uniform: the warp has a real row
+      const int pair = rv ? a.inv_pairs[rec.p0 + trow] : -1;
       const float* qr = a.Q + (int64_t)(rv ? pair / a.nprobe : 0) * st.D;
       const uint32_t ta = tbase + ((uint32_t)(32 * qw) << 16) + ab * 64u;
       float nrm = 0.f;
@@ -602,8 +605,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       const QInfo qi = qinfo[(i % NQI) * TM + row];
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_read[i % NQI]);
-      const bool rv = row < rec.nqt;
-      const bool wact = 32 * qw < rec.nqt;
+      const bool rv = 4 * lane + qw < rec.nqt;  // the item's row 4 lane + qw (see the loaders)
+      const bool wact = qw < rec.nqt;
       const int qglob = rv ? qi.pair / a.nprobe : 0;
       const float qn = qi.qn, sqn = sqrtf(qn);
       float thr = rv ? __uint_as_float(__ldcg(a.gthr + qglob)) : -INFINITY;
