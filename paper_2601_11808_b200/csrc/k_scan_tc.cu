@@ -129,7 +129,7 @@ struct QInfo {
 };
 
 struct TcPlan {
-  size_t stage_bytes, off_meta, off_q, off_items, off_thr, off_mrg, off_ring, off_bar, total;
+  size_t stage_bytes, off_meta, off_q, off_items, off_thr, off_mrg, off_vst, off_ring, off_bar, total;
 };
 __host__ __device__ inline TcPlan tc_plan(int Dh, int nst, int KP) {
   TcPlan p;
@@ -139,7 +139,8 @@ __host__ __device__ inline TcPlan tc_plan(int Dh, int nst, int KP) {
   p.off_items = p.off_q + NQI * TM * sizeof(QInfo);
   p.off_thr = p.off_items + NITEM * (sizeof(ItemRec) + MAXS * sizeof(uint2));
   p.off_mrg = p.off_thr + 2 * TM * 8;
-  p.off_ring = p.off_mrg + (size_t)TM * KP * 8;
+  p.off_vst = p.off_mrg + (size_t)TM * KP * 8;
+  p.off_ring = p.off_vst + (size_t)2 * TM * kSlot * 4;  // slow-path chunk rows [2 sets][TM][32]
   p.off_bar = p.off_ring + 128 * sizeof(uint2);
   p.total = p.off_bar + (3 * MAXST + 2 * NB + 4 + 2 * NQI + 2 * NITEM + 2) * 8 + 1024;  // + alignment slack
   return p;
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
   uint2* irec = reinterpret_cast<uint2*>(items + NITEM);  // [NITEM][MAXS] (slab | flags << 30, bitmap)
   u64* thr_sh = reinterpret_cast<u64*>(smem + p.off_thr);    // [2][TM] (item << 32 | k-th bound bits)
   u64* mrg = reinterpret_cast<u64*>(smem + p.off_mrg);       // [TM][KP] half-list hand-over
+  uint32_t* vst = reinterpret_cast<uint32_t*>(smem + p.off_vst);  // [2][TM][32] a slow chunk's raw q.x
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);  // [MAXST] producer -> MMA, meta (tx bytes)
   uint64_t* meta_ready = full + MAXST;                             // [MAXST] meta warp -> epilogue
   uint64_t* stage_free = meta_ready + MAXST;                       // [MAXST] epilogue -> producer
@@ -679,6 +681,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
               SCNT_ADD(&g_scnt[0], 1ull);
               const bool cold = !(thr < INFINITY);
 #endif
+              // the chunk's 32 raw products to this thread's shared row (16-B quads
+              // XOR-swizzled by the row: conflict-free), read back per survivor
+              uint32_t* vrow = vst + (size_t)(h * TM + row) * kSlot;
+#pragma unroll
+              for (int c4 = 0; c4 < 8; ++c4)
+                *reinterpret_cast<uint4*>(vrow + 4 * (c4 ^ (row & 7))) =
+                    make_uint4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
               uint32_t pm = 0u;
               if (unsafe) {
                 pm = m.bm[j];  // every valid slot
@@ -699,7 +708,11 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
               while (pm) {
                 const int c = __ffs(pm) - 1;
                 pm &= pm - 1;
-                const float t = fmaf(-2.f, __uint_as_float(pick32(v, c)), m.xnm[kSlot * j + c]);
+                // independent shared loads first: product, norm, id
+                const uint32_t pv = vrow[4 * ((c >> 2) ^ (row & 7)) + (c & 3)];
+                const float xn = m.xnm[kSlot * j + c];
+                const uint32_t cid = *reinterpret_cast<const uint32_t*>(rb + rec16_id_off(Dh, c));
+                const float t = fmaf(-2.f, __uint_as_float(pv), xn);
                 if (!unsafe && !(t <= tadj)) continue;  // the threshold may have tightened
                 float d;
                 if (ex) {
@@ -726,7 +739,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
                 }
                 d = fmaxf(d, 0.f);
                 if (!(d <= thr)) continue;
-                const u64 key = make_key(d, *reinterpret_cast<const uint32_t*>(rb + rec16_id_off(Dh, c)));
+                const u64 key = make_key(d, cid);
                 if (key >= kth) continue;
                 topk_reg_insert<KP>(keys, key);
                 kth = keys[KP - 1];
