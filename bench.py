@@ -981,11 +981,9 @@ def leg_h(S, dev, log, G, rank, pg, n_total):
     osamp = h_oracle_sample(ix, dev, gen, local_n, G, rank, Qg, log)
 
     def search(npb):
-        d, i = ix.search(Qg, K, npb)
-        if pg is not None:
-            gd, gi = shard.allgather_topk(pg, d, i)
-            d, i = S.merge_topk(gd, gi)
-        return d, i
+        if pg is not None:  # coarse step sharded over queries, probe sets all-gathered (NEXT-3)
+            return shard.sharded_search(pg, ix, Qg, K, npb)
+        return ix.search(Qg, K, npb)
 
     sweep, qps_at_09, np_at_09 = {}, None, None
     for npb in (8, 16, 32, 64):
@@ -1076,6 +1074,7 @@ def h_projection(S, dev, log, gen, C, Qg, n_total, base, base_ms, nvlink_gbs=400
     import torch
 
     from datagen import TRAIN_BASE  # noqa: F401  (same generator family as the H leg)
+    from paper_2601_11808_b200 import shard
 
     NLH = C.shape[0]
     out = {"method": "PROJECTION from measured single-shard runs on one B200 (no multi-GPU measurement): "
@@ -1117,6 +1116,28 @@ def h_projection(S, dev, log, gen, C, Qg, n_total, base, base_ms, nvlink_gbs=400
             times.append(a.elapsed_time(b))
         shard_ms = statistics.median(times)
         ph = h_phase_ms(ix, Qg)
+        # NEXT-3 query-sharded coarse step: rank 0's slice of the probe sets (sivf_probe on
+        # nq/G queries), then the scan + merge with the all-gathered full probe sets
+        # (sivf_search_probed); results bit-identical to the replicated search
+        nq = Qg.shape[0]
+        lo, hi = shard.query_slice(nq, Gp, 0)
+        probes = ix.probe(Qg, NPROBE)
+        pt, st_ = [], []
+        for rep in range(5):
+            a, b = _ev(), _ev()
+            a.record()
+            ix.probe(Qg[lo:hi], NPROBE)
+            b.record()
+            c_, d_ = _ev(), _ev()
+            c_.record()
+            dq, iq = ix.search_probed(Qg, probes, K)
+            d_.record()
+            torch.cuda.synchronize()
+            if rep >= 2:
+                pt.append(a.elapsed_time(b))
+                st_.append(c_.elapsed_time(d_))
+        qs_equal = bool(torch.equal(iq, i) and torch.equal(dq, d))
+        coarse_slice_ms, scan_probed_ms = statistics.median(pt), statistics.median(st_)
         del ix
         torch.cuda.empty_cache()
         nq = Qg.shape[0]
@@ -1136,7 +1157,16 @@ def h_projection(S, dev, log, gen, C, Qg, n_total, base, base_ms, nvlink_gbs=400
         ag_bytes = Gp * nq * K * (4 + 8)  # gathered per rank: dist f32 + id i64 of every shard
         ag_ms = (ag_bytes * (Gp - 1) / Gp) / (nvlink_gbs * 1e9) * 1e3 + 2 * coll_us / 1e3
         t_ms = shard_ms + ag_ms + merge_ms
+        agp_bytes = nq * NPROBE * 4  # gathered probe sets (int32), one collective
+        agp_ms = (agp_bytes * (Gp - 1) / Gp) / (nvlink_gbs * 1e9) * 1e3 + coll_us / 1e3
+        tq_ms = coarse_slice_ms + agp_ms + scan_probed_ms + ag_ms + merge_ms
         out[f"G{Gp}"] = {"local_n": local_n, "build_inserts_per_s_shard": local_n / (ins_ms / 1e3),
+                         "query_sharded_coarse": {
+                             "coarse_slice_ms": coarse_slice_ms, "queries_per_rank": hi - lo,
+                             "scan_merge_probed_ms": scan_probed_ms, "probe_allgather_bytes": agp_bytes,
+                             "probe_allgather_ms_model": agp_ms, "projected_search_ms": tq_ms,
+                             "projected_qps": nq / (tq_ms / 1e3), "projected_speedup_vs_G1": base_ms / tq_ms,
+                             "results_equal_replicated": qs_equal},
                          "search_ms_shard": shard_ms, "phases_ms_shard": ph, "merge_ms": merge_ms,
                          "allgather_bytes_per_rank": ag_bytes, "allgather_ms_model": ag_ms,
                          "projected_search_ms": t_ms, "projected_qps": nq / (t_ms / 1e3),
@@ -1145,6 +1175,9 @@ def h_projection(S, dev, log, gen, C, Qg, n_total, base, base_ms, nvlink_gbs=400
         log(f"H projection G={Gp}: shard search {shard_ms:.3f} ms (coarse {ph.get('coarse', 0):.3f}, scan "
             f"{ph.get('scan', 0):.3f}), merge {merge_ms:.3f}, all-gather model {ag_ms:.3f} -> projected "
             f"{nq / (t_ms / 1e3) / 1e6:.2f}M QPS, x{base_ms / t_ms:.2f} vs G=1")
+        log(f"H projection G={Gp} query-sharded coarse: slice coarse {coarse_slice_ms:.3f} ms + probe all-gather "
+            f"{agp_ms:.3f} + probed scan/merge {scan_probed_ms:.3f} + top-k all-gather/merge -> "
+            f"{nq / (tq_ms / 1e3) / 1e6:.2f}M QPS, x{base_ms / tq_ms:.2f} vs G=1 (equal: {qs_equal})")
     return out
 
 

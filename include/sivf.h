@@ -72,7 +72,15 @@ enum {
   /* Room for concurrent phases (NEXT-2): the directory arena gets 256 extra
    * entries per list so that sivf_reserve_directories can give every list up to
    * 256 spare entries (1 MB per 1024 lists). */
-  SIVF_CFG_CONCURRENT = 2
+  SIVF_CFG_CONCURRENT = 2,
+  /* Float-valued data at dim <= 128: keep the split-fp16 (hi + lo, per-vector
+   * power-of-2 scale) scan copy instead of the single fp16 copy, and search with
+   * the K-chunked GEMM scan (three kind::f16 MMAs per K step, distances within
+   * ~2^-20 relative: no exact re-rank of filter survivors).  The fp16 filter of
+   * the default copy is exact on small-integer data (SIFT-shaped) but re-ranks
+   * every survivor from the fp32 payload on float data.  +100 % of the payload
+   * bytes; dim > 128 always uses this copy.  Ignored with SIVF_CFG_NO_SCAN_COPY. */
+  SIVF_CFG_SPLIT_COPY = 4
 };
 
 typedef struct {
@@ -157,6 +165,22 @@ sivf_rc sivf_delete(sivf_index ix, const int64_t* d_ids, int64_t n, int64_t* d_n
  * kernel supports (e.g. shared memory for dim) returns SIVF_E_UNSUPPORTED. */
 sivf_rc sivf_search(sivf_index ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
                     int64_t* d_ids, int32_t* d_probes, sivf_stream_t stream);
+
+/* NEXT-3 (query-sharded coarse step): the coarse step alone
+ * and the scan + merge given the probe sets.
+ * sivf_probe: d_probes[nq][nprobe] (device, caller-owned) receives the exact probe
+ * SET of each query row (reading C3), as sivf_search's d_probes.
+ * Reads only the centroids: a rank may compute it for its slice of a batch.
+ * sivf_search_probed: as sivf_search, with the probe sets taken from
+ * d_probes_in[nq][nprobe] (device, read only; every entry in [0, nlist),
+ * nearest-first order preferred: it steers the scan's work order, not its
+ * results).  Given the probe sets sivf_probe returns (on any shard of the same
+ * centroids), its output equals sivf_search's bit for bit.  Entries outside
+ * [0, nlist) are undefined behaviour (not validated on the device). */
+sivf_rc sivf_probe(sivf_index ix, const float* d_q, int64_t nq, int32_t nprobe, int32_t* d_probes,
+                   sivf_stream_t stream);
+sivf_rc sivf_search_probed(sivf_index ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe,
+                           const int32_t* d_probes_in, float* d_dist, int64_t* d_ids, sivf_stream_t stream);
 
 /* One sliding-window step (reading C22): insert(new) -> delete(old) ->
  * search(queries) -> reclaim of full, fully-dead slabs.  Arguments as in the

@@ -71,6 +71,8 @@ EXPORTS = {
     "sivf_insert": (_i32, [_P, _P, _P, _i64, _P, _P, _P]),
     "sivf_delete": (_i32, [_P, _P, _i64, _P, _P]),
     "sivf_search": (_i32, [_P, _P, _i64, _i32, _i32, _P, _P, _P, _P]),
+    "sivf_probe": (_i32, [_P, _P, _i64, _i32, _P, _P]),
+    "sivf_search_probed": (_i32, [_P, _P, _i64, _i32, _i32, _P, _P, _P, _P]),
     "sivf_sliding_window_step": (_i32, [_P, _P, _P, _i64, _P, _i64, _P, _i64, _i32, _i32, _P, _P, _P, _P, _P]),
     "sivf_merge_topk": (_i32, [_P, _P, _i32, _i64, _i32, _P, _P, _P]),
     "sivf_reclaim": (_i32, [_P, _P, _P]),
@@ -93,6 +95,7 @@ EXPORTS = {
 
 CFG_NO_SCAN_COPY = 1  # sivf_config.flags: no fp16 scan copy (paper footprint, CUDA-core scan)
 CFG_CONCURRENT = 2  # sivf_config.flags: directory room for sivf_reserve_directories (NEXT-2)
+CFG_SPLIT_COPY = 4  # sivf_config.flags: split-fp16 copy + GEMM scan at dim <= 128 (float-valued data)
 OPT_TC_SCAN = 1
 OPT_TC_TWO_PHASE = 2
 OPT_TC_COARSE = 3
@@ -278,6 +281,28 @@ class Index:
         _check(lib().sivf_search(self._h, _ptr(Q), nq, k, nprobe, _ptr(dist), _ptr(ids), _ptr(probes),
                                  _stream(stream)), "sivf_search")
         return (dist, ids, probes) if return_probes else (dist, ids)
+
+    def probe(self, Q: torch.Tensor, nprobe: int, out=None, stream=None) -> torch.Tensor:
+        """Coarse step only (sivf_probe): the exact probe set [nq][nprobe] of each query."""
+        Q = _dev(Q, torch.float32, "queries")
+        nq = Q.shape[0]
+        probes = torch.empty(nq, nprobe, dtype=torch.int32, device=self.device) if out is None else out
+        _check(lib().sivf_probe(self._h, _ptr(Q), nq, nprobe, _ptr(probes), _stream(stream)), "sivf_probe")
+        return probes
+
+    def search_probed(self, Q: torch.Tensor, probes: torch.Tensor, k: int, out=None, stream=None):
+        """Scan + merge with given probe sets (sivf_search_probed); probes [nq][nprobe] int32."""
+        Q = _dev(Q, torch.float32, "queries")
+        probes = _dev(probes, torch.int32, "probes")
+        nq, nprobe = probes.shape
+        if out is None:
+            dist = torch.empty(nq, k, dtype=torch.float32, device=self.device)
+            ids = torch.empty(nq, k, dtype=torch.int64, device=self.device)
+        else:
+            dist, ids = out
+        _check(lib().sivf_search_probed(self._h, _ptr(Q), nq, k, nprobe, _ptr(probes), _ptr(dist), _ptr(ids),
+                                        _stream(stream)), "sivf_search_probed")
+        return dist, ids
 
     def sliding_window_step(self, new_ids, new_x, old_ids, Q, k: int, nprobe: int, out=None, stream=None):
         new_ids = _dev(new_ids, torch.int64, "new_ids")

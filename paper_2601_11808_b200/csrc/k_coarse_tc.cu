@@ -371,7 +371,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(const __grid_consta
                   Uo = ub;
                   T = fminf(T, Uo);
                 }
-                const int slot = atomicAdd(&cnt_sm[r], 1);
+                // N-split grid (gridDim.y > 1): the row's CTAs share one global counter
+                const int slot = gridDim.y > 1 ? atomicAdd(&a.cand_cnt[row], 1) : atomicAdd(&cnt_sm[r], 1);
                 if (slot < a.cap) {
                   crow[slot] = ((unsigned long long)__float_as_uint(fmaxf(lb, 0.f)) << 32) |
                                (uint32_t)(j * TN + cb + 4 * e4 + e);
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_coarse_gemm(const __grid_consta
       if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
     asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI));
-    if (KP != 0 && h == 0 && rv) a.cand_cnt[row] = cnt_sm[r];
+    if (KP != 0 && gridDim.y == 1 && h == 0 && rv) a.cand_cnt[row] = cnt_sm[r];
   }
   if (KP == 0 && warp >= W_EPI0 && lane == 0) bulk_wait0();  // stores complete before exit
   tc_fence_before();
@@ -1259,12 +1260,30 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
     const float* xr = d_x + r0 * D;
     const int64_t ntile = ceil_div(nr, TM);
     k_rows_tiles<<<ntile, 4 * TM, 0, s>>>(xr, nr, D, Dp, sc.x_tiles, sc.x_norm);
+    // Fewer row tiles than SMs (a search batch, a query slice, a small insert batch):
+    // split the N-tiles over ncg CTAs per row tile (the wave count times the N-tiles
+    // per CTA is minimised).  Each CTA bounds with its own range's m-th smallest upper
+    // bound U_R >= the row's U_(m), so every list with lower bound <= U_(m) is still
+    // appended (a superset; >= m per range) and k_coarse_rerank's exact U* over the
+    // candidates is unchanged.  ncg * m stays within half the candidate capacity.
+    int ncg = 1;
+    if (ntile < ix.num_sms) {
+      int64_t best = -1;
+      for (int c = 1; c <= ntn && c * 2 * m <= cap && c <= 16; c *= 2) {
+        const int64_t t = ceil_div((int64_t)ntile * c, (int64_t)ix.num_sms) * ceil_div((int64_t)ntn, (int64_t)c);
+        if (best < 0 || t < best) best = t, ncg = c;
+      }
+    }
+    const int ntpc = (int)ceil_div((int64_t)ntn, (int64_t)ncg);
+    ncg = (int)ceil_div((int64_t)ntn, (int64_t)ntpc);
+    if (ncg > 1) cudaMemsetAsync(sc.cand_cnt, 0, sizeof(int32_t) * nr, s);
     CoarseArgs a{sc.x_tiles, sc.x_norm, sc.c_tiles, sc.c_norm, sc.c_csa, sc.c_cnb, nr, Dp, st.nlist, m, cap,
-                 bd.kb, sc.cand, sc.cand_ubv, sc.cand_cnt, nullptr, ntn};
+                 bd.kb, sc.cand, sc.cand_ubv, sc.cand_cnt, nullptr, ntpc};
+    const dim3 grid((unsigned)ntile, (unsigned)ncg);
     if (m == 1)
-      k_coarse_gemm<1><<<ntile, CTHREADS, coarse_smem_bytes(), s>>>(*reinterpret_cast<const CUtensorMap*>(ix.coarse_tmap), a);
+      k_coarse_gemm<1><<<grid, CTHREADS, coarse_smem_bytes(), s>>>(*reinterpret_cast<const CUtensorMap*>(ix.coarse_tmap), a);
     else
-      k_coarse_gemm<32><<<ntile, CTHREADS, coarse_smem_bytes(), s>>>(*reinterpret_cast<const CUtensorMap*>(ix.coarse_tmap), a);
+      k_coarse_gemm<32><<<grid, CTHREADS, coarse_smem_bytes(), s>>>(*reinterpret_cast<const CUtensorMap*>(ix.coarse_tmap), a);
     if (probes == nullptr)
       k_coarse_rerank<0><<<ceil_div(nr, 4), 128, rsm, s>>>(xr, nr, D, st.centroids, Dp, st.nlist, m, sc.cand,
                                                           sc.cand_ubv, sc.cand_cnt, cap, best + r0, nullptr, 0);

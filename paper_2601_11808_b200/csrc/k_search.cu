@@ -526,21 +526,28 @@ SearchPlan plan_search(const Index& ix, int64_t nq, int32_t k, int32_t nprobe) {
 // Coarse quantisation + inverse probe map: reads only the centroids and the
 // queries (never the index state), so it may run concurrently with mutations.
 cudaError_t launch_search_front(Index& ix, const SearchPlan& p, const float* d_q, int64_t nq, int32_t nprobe,
-                                int32_t* d_probes, cudaStream_t s) {
+                                int32_t* d_probes, cudaStream_t s, const int32_t* probes_in) {
   Scratch& sc = ix.sc;
   const int nlist = ix.st.nlist;
   const int64_t npairs = nq * nprobe;
   // the coarse selection may count the inverse map on the fly (k_inv_count fused)
   cudaMemsetAsync(sc.inv_cnt, 0, sizeof(int32_t) * p.nb * nlist, s);
-  ix.fuse_inv_cnt = sc.inv_cnt;
-  ix.fuse_nb = p.nb;
-  ix.fuse_r0 = p.r0;
-  ix.fuse_inv_done = false;
-  cudaError_t e = launch_probe_exact(ix, d_q, nq, nprobe, s);
-  const bool counted = ix.fuse_inv_done;
-  ix.fuse_inv_cnt = nullptr;
-  ix.fuse_inv_done = false;
-  if (e != cudaSuccess) return e;
+  bool counted = false;
+  if (probes_in) {
+    // probe sets computed elsewhere (the query-sharded coarse step, NEXT-3): only the
+    // inverse map is built here
+    cudaMemcpyAsync(sc.probes, probes_in, sizeof(int32_t) * npairs, cudaMemcpyDeviceToDevice, s);
+  } else {
+    ix.fuse_inv_cnt = sc.inv_cnt;
+    ix.fuse_nb = p.nb;
+    ix.fuse_r0 = p.r0;
+    ix.fuse_inv_done = false;
+    cudaError_t e = launch_probe_exact(ix, d_q, nq, nprobe, s);
+    counted = ix.fuse_inv_done;
+    ix.fuse_inv_cnt = nullptr;
+    ix.fuse_inv_done = false;
+    if (e != cudaSuccess) return e;
+  }
   if (d_probes) cudaMemcpyAsync(d_probes, sc.probes, sizeof(int32_t) * npairs, cudaMemcpyDeviceToDevice, s);
   const int nent = p.nb * nlist;
   PhaseTimer pt(ix, SIVF_PH_INVMAP, s);
@@ -610,11 +617,11 @@ cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q,
 }
 
 cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
-                          int64_t* d_ids, int32_t* d_probes, cudaStream_t s) {
+                          int64_t* d_ids, int32_t* d_probes, cudaStream_t s, const int32_t* probes_in) {
   if (nq <= 0) return cudaSuccess;
   const SearchPlan p = plan_search(ix, nq, k, nprobe);
   if (!p.ok) return cudaErrorInvalidConfiguration;
-  cudaError_t e = launch_search_front(ix, p, d_q, nq, nprobe, d_probes, s);
+  cudaError_t e = launch_search_front(ix, p, d_q, nq, nprobe, d_probes, s, probes_in);
   if (e != cudaSuccess) return e;
   return launch_search_back(ix, p, d_q, nq, k, nprobe, d_dist, d_ids, s);
 }

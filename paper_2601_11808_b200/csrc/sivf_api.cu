@@ -47,7 +47,8 @@ bool valid_config(const sivf_config* c) {
   if (c->shard_count < 1 || c->shard_rank < 0 || c->shard_rank >= c->shard_count) return false;
   if (c->max_train > 0 && c->max_train < c->nlist) return false;
   if ((int64_t)c->max_queries * c->max_nprobe > 0x7FFFFFFFll) return false;
-  if (c->flags & ~(int32_t)(SIVF_CFG_NO_SCAN_COPY | SIVF_CFG_CONCURRENT)) return false;  // unknown flag bits
+  if (c->flags & ~(int32_t)(SIVF_CFG_NO_SCAN_COPY | SIVF_CFG_CONCURRENT | SIVF_CFG_SPLIT_COPY))
+    return false;  // unknown flag bits
   return true;
 }
 
@@ -58,9 +59,11 @@ Layout make_layout(const sivf_config* c, bool view = false) {
   const int64_t D = c->dim, nl = c->nlist, S = c->num_slabs;
   L.Dp = (D + 7) / 8 * 8;  // tf32 MMA K-step = 8 dims
   // fp16 scan copy (kind::f16 K-step = 16 dims); none for D > 128 or SIVF_CFG_NO_SCAN_COPY
-  L.Dh = (D <= 128 && !(c->flags & SIVF_CFG_NO_SCAN_COPY)) ? (D + 15) / 16 * 16 : 0;
-  // split-fp16 scan copy for D > 128 (k_scan_gs.cu, 64-dim K chunks)
-  L.Dg = (D > 128 && !(c->flags & SIVF_CFG_NO_SCAN_COPY)) ? (D + 63) / 64 * 64 : 0;
+  const bool nocopy = (c->flags & SIVF_CFG_NO_SCAN_COPY) != 0;
+  const bool split = D > 128 || (c->flags & SIVF_CFG_SPLIT_COPY) != 0;
+  L.Dh = (!split && !nocopy) ? (D + 15) / 16 * 16 : 0;
+  // split-fp16 scan copy for D > 128 or SIVF_CFG_SPLIT_COPY (k_scan_gs.cu, 64-dim K chunks)
+  L.Dg = (split && !nocopy) ? (D + 63) / 64 * 64 : 0;
   const int64_t cap = c->id_capacity, G = c->shard_count, r = c->shard_rank;
   L.cap_local = cap > r ? (cap - r + G - 1) / G : 0;
   // directory arena: two halves; a compaction into the idle half needs at most
@@ -624,6 +627,53 @@ sivf_rc sivf_search(sivf_index h, const float* d_q, int64_t nq, int32_t k, int32
   key.n[2] = nq, key.k = k, key.nprobe = nprobe, key.kind = 1;
   return graph_cached(ix, key, s, [&](cudaStream_t cs) {
     return cuda_rc(launch_search(*ix, d_q, nq, k, nprobe, d_dist, d_ids, d_probes, cs));
+  });
+}
+
+// Coarse step alone (a7): the exact probe set of each query row (NEXT-3: ranks
+// compute the probe sets of their slice of the queries, then all-gather them).
+sivf_rc sivf_probe(sivf_index h, const float* d_q, int64_t nq, int32_t nprobe, int32_t* d_probes,
+                   sivf_stream_t stream) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (nq < 0 || nq > ix->cfg.max_queries) return SIVF_E_INVALID_ARG;
+  if (nprobe < 1 || nprobe > ix->cfg.max_nprobe || nprobe > ix->st.nlist) return SIVF_E_INVALID_ARG;
+  if (nq > 0 && (!d_q || !d_probes)) return SIVF_E_INVALID_ARG;
+  if (!ix->trained) return SIVF_E_NOT_TRAINED;
+  if (nq == 0) return SIVF_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Index::StepGraph key;
+  const void* p[8] = {d_q, d_probes, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  for (int i = 0; i < 8; ++i) key.p[i] = p[i];
+  key.n[2] = nq, key.nprobe = nprobe, key.kind = 2;
+  return graph_cached(ix, key, s, [&](cudaStream_t cs) {
+    cudaError_t e = launch_probe_exact(*ix, d_q, nq, nprobe, cs);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(d_probes, ix->sc.probes, sizeof(int32_t) * nq * nprobe, cudaMemcpyDeviceToDevice, cs);
+    return cuda_rc(e);
+  });
+}
+
+// Scan + merge with caller-supplied probe sets (d_probes_in[nq][nprobe], e.g. the
+// all-gathered output of sivf_probe): the same results as sivf_search when they
+// are the probe sets sivf_search would compute.
+sivf_rc sivf_search_probed(sivf_index h, const float* d_q, int64_t nq, int32_t k, int32_t nprobe,
+                           const int32_t* d_probes_in, float* d_dist, int64_t* d_ids, sivf_stream_t stream) {
+  if (!h) return SIVF_E_INVALID_ARG;
+  Index* ix = reinterpret_cast<Index*>(h);
+  if (nq < 0 || nq > ix->cfg.max_queries) return SIVF_E_INVALID_ARG;
+  if (k < 1 || k > ix->cfg.max_k) return SIVF_E_INVALID_ARG;
+  if (nprobe < 1 || nprobe > ix->cfg.max_nprobe || nprobe > ix->st.nlist) return SIVF_E_INVALID_ARG;
+  if (nq > 0 && (!d_q || !d_probes_in || !d_dist || !d_ids)) return SIVF_E_INVALID_ARG;
+  if (nq > 0 && !plan_search(*ix, nq, k, nprobe).ok) return SIVF_E_UNSUPPORTED;
+  if (nq == 0) return SIVF_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Index::StepGraph key;
+  const void* p[8] = {d_q, d_dist, d_ids, d_probes_in, nullptr, nullptr, nullptr, nullptr};
+  for (int i = 0; i < 8; ++i) key.p[i] = p[i];
+  key.n[2] = nq, key.k = k, key.nprobe = nprobe, key.kind = 3;
+  return graph_cached(ix, key, s, [&](cudaStream_t cs) {
+    return cuda_rc(launch_search(*ix, d_q, nq, k, nprobe, d_dist, d_ids, nullptr, cs, d_probes_in));
   });
 }
 

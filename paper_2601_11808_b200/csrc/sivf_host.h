@@ -227,13 +227,13 @@ struct SearchPlan {
 };
 SearchPlan plan_search(const Index& ix, int64_t nq, int32_t k, int32_t nprobe);
 cudaError_t launch_search_front(Index& ix, const SearchPlan& p, const float* d_q, int64_t nq, int32_t nprobe,
-                                int32_t* d_probes, cudaStream_t s);
+                                int32_t* d_probes, cudaStream_t s, const int32_t* probes_in = nullptr);
 cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q, int64_t nq, int32_t k,
                                int32_t nprobe, float* d_dist, int64_t* d_ids, cudaStream_t s,
                                cudaEvent_t after_scan = nullptr);
 bool coarse_front_concurrent_ok(const Index& ix, int32_t nprobe);
 cudaError_t launch_search(Index& ix, const float* d_q, int64_t nq, int32_t k, int32_t nprobe, float* d_dist,
-                          int64_t* d_ids, int32_t* d_probes, cudaStream_t s);
+                          int64_t* d_ids, int32_t* d_probes, cudaStream_t s, const int32_t* probes_in = nullptr);
 cudaError_t launch_seed_bound(Index& ix, const float* d_q, int64_t nq, int k, int nprobe, cudaStream_t s);
 cudaError_t launch_merge_topk(const float* d_dist_g, const int64_t* d_ids_g, int32_t G, int64_t nq, int32_t k,
                               float* d_dist, int64_t* d_ids, cudaStream_t s, int64_t* launches);

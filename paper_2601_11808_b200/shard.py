@@ -47,5 +47,55 @@ def allgather_topk(pg, d, i):
     return gd, gi
 
 
-__all__ = ["owner", "route", "local_count", "allgather_topk"]
+def query_slice(nq: int, G: int, rank: int):
+    """The rank's contiguous slice [lo, hi) of a batch of nq queries (query-sharded coarse
+    step, NEXT-3): sizes differ by at most one."""
+    lo = rank * nq // G
+    return lo, (rank + 1) * nq // G
+
+
+def allgather_probes(pg, probes_local, nq: int):
+    """All-gather the per-rank probe sets [hi - lo][nprobe] (int32) of the query slices
+    into the full [nq][nprobe] on every rank (one all_gather_into_tensor of equal-size
+    padded blocks under NCCL; the list form otherwise)."""
+    import torch
+
+    G = pg.get_world_size()
+    if G == 1:
+        return probes_local
+    nprobe = probes_local.shape[1]
+    blk = -(-nq // G)  # ceil: every rank contributes a padded block of blk rows
+    pad = torch.zeros((blk, nprobe), dtype=probes_local.dtype, device=probes_local.device)
+    pad[: probes_local.shape[0]] = probes_local
+    g = torch.empty((G, blk, nprobe), dtype=probes_local.dtype, device=probes_local.device)
+    if pg.get_backend() == "nccl":
+        pg.all_gather_into_tensor(g.view(-1), pad.view(-1))
+    else:
+        pg.all_gather(list(g.unbind(0)), pad)
+    parts = []
+    for r in range(G):
+        lo, hi = query_slice(nq, G, r)
+        parts.append(g[r, : hi - lo])
+    return torch.cat(parts, 0)
+
+
+def sharded_search(pg, ix, Q, k: int, nprobe: int):
+    """Id-sharded search with the coarse step sharded over queries (§8(e), NEXT-3):
+    rank r computes the probe sets of its query slice (sivf_probe), the slices are
+    all-gathered, every rank scans its shard with the full probe sets
+    (sivf_search_probed), and the per-shard top-k lists are all-gathered and merged
+    (sivf_merge_topk).  Bit-identical to the replicated-coarse search: the probe
+    sets do not depend on the shard."""
+    from . import merge_topk
+
+    G, rank = pg.get_world_size(), pg.get_rank()
+    nq = Q.shape[0]
+    lo, hi = query_slice(nq, G, rank)
+    probes = allgather_probes(pg, ix.probe(Q[lo:hi], nprobe), nq)
+    d, i = ix.search_probed(Q, probes, k)
+    gd, gi = allgather_topk(pg, d, i)
+    return merge_topk(gd, gi)
+
+
+__all__ = ["owner", "route", "local_count", "allgather_topk", "query_slice", "allgather_probes", "sharded_search"]
 _ = np  # numpy arrays and torch tensors both route (ids % G works on either)

@@ -58,7 +58,10 @@ def test_arena_bytes_and_validation(L):
     c.flags = S.CFG_NO_SCAN_COPY  # no scan records: exactly 46,024 x (32 x 128 x 2 + 256) bytes less
     assert L.sivf_arena_bytes(ctypes.byref(c), ctypes.byref(n)) == 0
     assert full - n.value == 46_024 * (32 * 128 * 2 + 256)  # fp16 copy + the records' norm and id copies
-    c.flags = 4  # unknown flag bit
+    c.flags = S.CFG_SPLIT_COPY  # split-fp16 copy at dim 128: 2 x 2 B per value + a scale per slot, no fp16 records
+    assert L.sivf_arena_bytes(ctypes.byref(c), ctypes.byref(n)) == 0
+    assert n.value > full
+    c.flags = 8  # unknown flag bit
     assert L.sivf_arena_bytes(ctypes.byref(c), ctypes.byref(n)) == -1
     c.flags = 0
     c.max_k = 129

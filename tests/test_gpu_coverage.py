@@ -12,6 +12,7 @@ import torch
 
 import oracle as O
 import paper_2601_11808_b200 as S
+from paper_2601_11808_b200 import shard
 from datagen import Generator, sift_shape
 from tests.checkers import check_state
 from tests.test_gpu_parity import T, dele, ins, make_pair, srch
@@ -31,10 +32,12 @@ def test_coarse_large_nlist_sift_shaped(NL):
     rng = np.random.default_rng(NL)
     C = (gen.range(1 << 41, NL) + rng.integers(-2, 3, (NL, 128))).astype(np.float32)
     N = 20000
-    g, o = make_pair(128, NL, N, C, max_batch=10000, max_queries=1000, max_k=32, max_nprobe=64)
+    g, o = make_pair(128, NL, N, C, max_batch=19000, max_queries=1000, max_k=32, max_nprobe=64)
     X = gen.range(0, N)
-    ins(g, o, np.arange(10000), X[:10000])  # ins() asserts statuses and assigned lists equal
-    ins(g, o, np.arange(10000, N), X[10000:])
+    # 149 row tiles: one CTA per row tile; then 8 row tiles: the N-tiles split over CTAs
+    # (per-range bounds, shared candidate counters), as for the queries below
+    ins(g, o, np.arange(19000), X[:19000])  # ins() asserts statuses and assigned lists equal
+    ins(g, o, np.arange(19000, N), X[19000:])
     check_state(g, o, f"nlist {NL}")
     Q = gen.queries(0, 1000)
     for npb in (1, 8, 32, 64):
@@ -100,8 +103,24 @@ def test_sharded_index_on_one_gpu(G):
         dg = torch.stack([d for d, _ in outs])
         ig = torch.stack([i for _, i in outs])
         md, mi = S.merge_topk(dg, ig)
-        od, oi, _ = ref.search(Q, k, npb)
+        od, oi, op = ref.search(Q, k, npb)
         assert np.array_equal(mi.cpu().numpy(), oi) and np.array_equal(md.cpu().numpy(), od)
+        # NEXT-3 query-sharded coarse step: rank r computes the probe sets of its query
+        # slice (sivf_probe), the slices are concatenated (the all-gather), and every
+        # shard scans with the full probe sets (sivf_search_probed): the merged result is
+        # the unsharded oracle's, bitwise, and each shard's equals its own sivf_search
+        Qt = T(Q)
+        parts = []
+        for r, (g, _) in enumerate(shards):
+            lo, hi = shard.query_slice(len(Q), G, r)
+            parts.append(g.probe(Qt[lo:hi], npb))
+        probes = torch.cat(parts, 0)
+        assert np.array_equal(np.sort(probes.cpu().numpy(), 1), np.sort(np.asarray(op), 1))
+        outs2 = [g.search_probed(Qt, probes, k) for g, _ in shards]
+        for (d1, i1), (d2, i2) in zip(outs, outs2):
+            assert torch.equal(i1, i2) and torch.equal(d1, d2)
+        md2, mi2 = S.merge_topk(torch.stack([d for d, _ in outs2]), torch.stack([i for _, i in outs2]))
+        assert torch.equal(md2, md) and torch.equal(mi2, mi)
 
 
 # ------------------------------------------------------------------ sivf_search graph cache

@@ -32,6 +32,27 @@ def test_gs_scan_float_data(dim):
         assert srch(g, o, Q, k, npb, exact=False) <= 3
 
 
+@pytest.mark.parametrize("dim", [16, 100, 128])
+def test_split_copy_flag_dim_le_128_float(dim):
+    # SIVF_CFG_SPLIT_COPY: the split-fp16 copy and the GEMM scan at dim <= 128 (float
+    # data: uniform [0, 1) as the paper's grids); the default fp16 copy is absent
+    # (its tensor-core scan is not used)
+    rng = np.random.default_rng(dim)
+    X = rng.random((6000, dim), dtype=np.float32)
+    C = O.kmeans(X[:3000], 32, 5, 4)
+    g, o = make_pair(dim, 32, 6000, C, max_queries=300, max_nprobe=32, max_batch=6000, flags=S.CFG_SPLIT_COPY)
+    ins(g, o, np.arange(6000), X)
+    dele(g, o, np.arange(0, 6000, 5))
+    Q = rng.random((300, dim), dtype=np.float32)
+    for k, npb in ((1, 1), (10, 8), (32, 32), (100, 4)):
+        assert srch(g, o, Q, k, npb, exact=False) <= 3
+    d1, i1 = g.search(T(Q), 10, 8)
+    g.set_option(S.OPT_TC_SCAN, 0)  # the CUDA-core scan of the same index
+    d2, i2 = g.search(T(Q), 10, 8)
+    assert np.allclose(d1.cpu().numpy(), d2.cpu().numpy(), rtol=1e-4, atol=1e-6)
+    assert (i1 == i2).float().mean().item() > 0.99
+
+
 def test_gs_scan_matches_simt_scan():
     # the same index searched by the GEMM scan and by the CUDA-core scan (OPT_TC_SCAN 0):
     # ids equal up to near-ties, distances within 1e-4 relative

@@ -50,7 +50,11 @@ def _worker(rank, G, port, out):
     # a delete batch routed by id: every rank receives only its own ids
     dels, = shard.route(np.arange(0, N, 7, dtype=np.int64), G, rank)
     ix.delete(dels)
-    d, i, _ = ix.search(Q, K, NPROBE)
+    d, i, P = ix.search(Q, K, NPROBE)
+    # query-sharded coarse step (NEXT-3): this rank's slice of the probe sets, all-gathered
+    lo, hi = shard.query_slice(NQ, G, rank)
+    Pg = shard.allgather_probes(dist, torch.from_numpy(np.ascontiguousarray(np.asarray(P, np.int32)[lo:hi])), NQ)
+    assert np.array_equal(Pg.numpy(), np.asarray(P, np.int32))
     gd, gi = shard.allgather_topk(dist, torch.from_numpy(np.ascontiguousarray(d)),
                                   torch.from_numpy(np.ascontiguousarray(i)))
     if rank == 0:
@@ -60,6 +64,14 @@ def _worker(rank, G, port, out):
         np.save(out + ".n.npy", np.array([gd.shape[0]]))
     dist.barrier()
     dist.destroy_process_group()
+
+
+def test_query_slices_partition_batch():
+    for nq, G in ((10, 3), (2, 4), (10000, 8), (0, 2)):
+        sl = [shard.query_slice(nq, G, r) for r in range(G)]
+        assert sl[0][0] == 0 and sl[-1][1] == nq
+        assert all(sl[r][1] == sl[r + 1][0] for r in range(G - 1))
+        assert max(h - l for l, h in sl) - min(h - l for l, h in sl) <= 1
 
 
 def test_route_partitions_ids():

@@ -37,10 +37,10 @@ def timed(fn, s):
     return e0.elapsed_time(e1)
 
 
-def build(n, nlist, mf=1.2, sf=1.2, max_queries=10_000):
+def build(n, nlist, mf=1.2, sf=1.2, max_queries=10_000, flags=0):
     gen = DeviceGenerator(uniform_shape(0x0E1F, D))
     ix = S.Index(D, nlist, n, S.num_slabs_for(n, nlist, mf, sf), max_batch=BATCH, max_queries=max_queries, max_k=10,
-                 max_nprobe=min(64, nlist))
+                 max_nprobe=min(64, nlist), flags=flags)
     cent = torch.empty(nlist, D, device="cuda")
     gen.range_into(cent, 1 << 41)
     ix.set_centroids(cent)
@@ -75,18 +75,20 @@ def ingestion(ns, nls):
     return out
 
 
-def search(ns, nls):
+def search(ns, nls, flags=0):
+    # flags = S.CFG_SPLIT_COPY: the split-fp16 copy + GEMM scan for this float data
     out = []
     for n in ns:
         for nl in nls:
-            ix, gen, _ = build(n, nl)
+            ix, gen, _ = build(n, nl, flags=flags)
             Q = torch.empty(10_000, D, device="cuda")
             gen.range_into(Q, 1 << 40)
             s = torch.cuda.current_stream()
             npb = min(32, nl)
             ix.search(Q, 10, npb)
             ms = min(timed(lambda: ix.search(Q, 10, npb), s) for _ in range(5))
-            out.append({"n": n, "nlist": nl, "nprobe": npb, "k": 10, "qps": 10_000 / (ms / 1e3), "ms_10k": ms})
+            out.append({"n": n, "nlist": nl, "nprobe": npb, "k": 10, "qps": 10_000 / (ms / 1e3), "ms_10k": ms,
+                        "scan_copy": "split-fp16 (SIVF_CFG_SPLIT_COPY)" if flags else "fp16"})
             print(json.dumps(out[-1]), flush=True)
             del ix
             torch.cuda.empty_cache()
@@ -120,8 +122,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/grids.json")
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--search-only", action="store_true")
     a = ap.parse_args()
     q = a.quick
+    if a.search_only:
+        ns = [100_000] if q else [100_000, 300_000, 500_000]
+        res = {"search": search(ns, [1024, 4096, 16384]),
+               "search_split_copy": search(ns, [1024, 4096, 16384], S.CFG_SPLIT_COPY)}
+        os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+        json.dump(res, open(a.out, "w"), indent=1)
+        return
     res = {"data": "uniform d=128 (P:485; dimension unstated, reading C27), centroids = sampled points",
            "ingestion": ingestion([1_000_000] if q else [1_000_000, 2_000_000, 4_000_000], [1024, 4096, 16384]),
            "search": search([100_000] if q else [100_000, 300_000, 500_000], [1024, 4096, 16384]),
