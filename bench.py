@@ -215,35 +215,78 @@ def _oracle_steps(ref, gen, si, sd, sq, warmup, budget_steps):
     return times
 
 
+def sivf_config(G):
+    """The workload config dict, shared by both arms (same_config)."""
+    return {"workload": WORKLOAD, "n_base": N_BASE, "dim": DIM, "nlist": NLIST, "batch": BATCH, "nq": NQ,
+            "k": K, "nprobe": NPROBE, "parallelism": f"id-shard{G}",
+            "l2": "no flush: the 0.75 GB index scanned every step exceeds the 126 MB L2",
+            "generator": "datagen SIFT-shaped (M=50, r=24, a=60, b=50, sigma=15), seed 0x51F7"}
+
+
 def run_reference(args):
+    """The CPU oracle as it stands (oracle/, test infrastructure) on the box's host
+    cores: WHOLE sliding steps of the same workload (10k inserts + 10k deletes + 10k
+    queries + reclaim on the 1M-vector window, the quantizer = the oracle k-means on
+    the same training sample and iterations, which the GPU k-means equals bit for
+    bit), exactly `--warmup` untimed and `--steps` timed steps, no extrapolation.  All
+    host threads (the oracle's per-item parallel loops); rank 0 only."""
+    import oracle as O
+    from datagen import Generator, sift_shape
+
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    n_cores = 1
     log = lambda m: print(f"[bench:reference] {m}", file=sys.stderr, flush=True)
-    steps = max(1, min(args.steps, 5))
-    times = oracle_sample(n_cores, steps, min(args.warmup, 1), log)
-    full = [t["full_step_s"] for t in times]
-    mean = statistics.mean(full)
+    n_cores = os.cpu_count() or 1
+    O.set_threads(n_cores)
+    gen = Generator(sift_shape(seed=SEED))
+    t0 = time.time()
+    C = O.kmeans(gen.train(N_TRAIN), NLIST, N_ITER, SEED)
+    steps, warm = args.steps, args.warmup
+    ref = O.Index(DIM, NLIST, N_BASE + (steps + warm + 1) * BATCH)
+    ref.set_centroids(C)
+    for b0 in range(0, N_BASE, 100_000):
+        ref.insert(np.arange(b0, b0 + 100_000), gen.range(b0, 100_000))
+    log(f"setup (k-means {N_ITER} iters on {N_TRAIN} samples + 1M build) {time.time() - t0:.1f}s on {n_cores} threads")
+    times, parts = [], []
+    t_wall = time.time()
+    for t in range(warm + steps):
+        new = np.arange(N_BASE + t * BATCH, N_BASE + (t + 1) * BATCH)
+        old = np.arange(t * BATCH, (t + 1) * BATCH)
+        Xn = gen.range(int(new[0]), BATCH)
+        Q = gen.queries(t * NQ, NQ)
+        a = time.perf_counter()
+        ref.insert(new, Xn)
+        b = time.perf_counter()
+        ref.delete(old)
+        c = time.perf_counter()
+        ref.search(Q, K, NPROBE)
+        d = time.perf_counter()
+        ref.reclaim()
+        e = time.perf_counter()
+        if t >= warm:
+            times.append(e - a)
+            parts.append({"insert_10k": b - a, "delete_10k": c - b, "search_10k": d - c, "reclaim": e - d})
+        log(f"step {t} {'(warm-up) ' if t < warm else ''}{(e - a) * 1e3:.0f} ms")
+    wall = time.time() - t_wall
+    mean = statistics.mean(times)
     value = 1.0 / mean
-    sample = ("per timed step: 1k inserts + 1k deletes + 100 queries (k=10, nprobe=32) + reclaim on a 1M-vector "
-              "oracle index (one thread pinned to one core); value and ms_per_step are EXTRAPOLATED x10/x10/x100 "
-              "to the full 10k/10k/10k step (sample_ms_per_step is the measured time of the sampled step)")
+    sample = (f"{steps} whole sliding steps (after {warm} untimed): 10k inserts + 10k deletes + 10k queries (k=10, "
+              f"nprobe=32) + reclaim on the 1M-vector oracle window, {n_cores} host threads; not extrapolated")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus,
-        "steps": len(full), "warmup": min(args.warmup, 1), "ms_per_step": mean * 1e3, "higher_is_better": True,
+        "steps": steps, "warmup": warm, "ms_per_step": mean * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "oracle": "oracle/ (plain C++17, -O2 -ffp-contract=off)"},
+        "config": sivf_config(args.gpus),
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": n_cores, "kind": "oracle", "sample": sample,
-                         "cpu_model": cpu_model(), "extrapolated": True},
-        "sample_ms_per_step": statistics.mean(t["sample_step_s"] for t in times) * 1e3,
-        "extrapolated": True,
+                         "cpu_model": cpu_model(), "extrapolated": False},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "breakdown_s": {k: statistics.mean(t[k] for t in times) for k in times[0]},
-        "metrics": {"inserts_per_s": BATCH / statistics.mean(t["insert_1k"] * BATCH / (BATCH // 10) for t in times),
-                    "deletes_per_s": BATCH / statistics.mean(t["delete_1k"] * 10 for t in times),
-                    "qps_nprobe32": NQ / statistics.mean(t["search_100q"] * 100 for t in times),
-                    "step_ms_p50": pct(full, 50) * 1e3, "step_ms_p99": pct(full, 99) * 1e3},
+        "timed_wall_s": wall,
+        "breakdown_s": {k: statistics.mean(p[k] for p in parts) for k in parts[0]},
+        "metrics": {"inserts_per_s": BATCH / statistics.mean(p["insert_10k"] for p in parts),
+                    "deletes_per_s": BATCH / statistics.mean(p["delete_10k"] for p in parts),
+                    "qps_nprobe32": NQ / statistics.mean(p["search_10k"] for p in parts),
+                    "step_ms_p50": pct(times, 50) * 1e3, "step_ms_p99": pct(times, 99) * 1e3},
     }
     print(json.dumps(line), flush=True)
 
@@ -621,13 +664,10 @@ def run_sivf(args):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_base": N_BASE, "dim": DIM, "nlist": NLIST, "batch": BATCH, "nq": NQ,
-                   "k": K, "nprobe": NPROBE, "parallelism": f"id-shard{G}",
-                   "l2": "no flush: the 0.75 GB index scanned every step exceeds the 126 MB L2",
-                   "generator": "datagen SIFT-shaped (M=50, r=24, a=60, b=50, sigma=15), seed 0x51F7",
-                   "timing": ("value: one CUDA-graph replay per step (inputs copied into the graph's static buffers "
+        "config": sivf_config(G),
+        "timing": ("value: one CUDA-graph replay per step (inputs copied into the graph's static buffers "
                               "inside the timed region); phases/roofline: the same steps launched directly with "
-                              "per-phase CUDA events") if graph else "direct launches with per-phase CUDA events"},
+                              "per-phase CUDA events") if graph else "direct launches with per-phase CUDA events",
         "metrics": {
             "ms_per_step_direct": direct_ms,
             "step_ms_p50": pct(step_ms, 50), "step_ms_p99": pct(step_ms, 99),

@@ -1266,8 +1266,13 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
     // bound U_R >= the row's U_(m), so every list with lower bound <= U_(m) is still
     // appended (a superset; >= m per range) and k_coarse_rerank's exact U* over the
     // candidates is unchanged.  ncg * m stays within half the candidate capacity.
+    // Only for probe selection (m > 1) on a few row tiles (a query slice of the
+    // query-sharded coarse step): with m = 1 every range's running minimum starts
+    // loose and the appended candidates overflow the small assignment buffers, and at
+    // >= a quarter of the SMs in row tiles the extra per-CTA pipeline fills cost more
+    // than the split gains (measured, tools/coarse_cmp.py).
     int ncg = 1;
-    if (ntile < ix.num_sms) {
+    if (m > 1 && ntile * 4 <= ix.num_sms) {
       int64_t best = -1;
       for (int c = 1; c <= ntn && c * 2 * m <= cap && c <= 16; c *= 2) {
         const int64_t t = ceil_div((int64_t)ntile * c, (int64_t)ix.num_sms) * ceil_div((int64_t)ntn, (int64_t)c);

@@ -34,8 +34,8 @@ def test_coarse_large_nlist_sift_shaped(NL):
     N = 20000
     g, o = make_pair(128, NL, N, C, max_batch=19000, max_queries=1000, max_k=32, max_nprobe=64)
     X = gen.range(0, N)
-    # 149 row tiles: one CTA per row tile; then 8 row tiles: the N-tiles split over CTAs
-    # (per-range bounds, shared candidate counters), as for the queries below
+    # 149 row tiles, then 8 (one CTA per row tile for the assignment); the 8-tile query
+    # batches below split their N-tiles over CTAs (per-range bounds, shared counters)
     ins(g, o, np.arange(19000), X[:19000])  # ins() asserts statuses and assigned lists equal
     ins(g, o, np.arange(19000, N), X[19000:])
     check_state(g, o, f"nlist {NL}")
