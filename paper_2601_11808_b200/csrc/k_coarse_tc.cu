@@ -1269,10 +1269,10 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
     // Only for probe selection (m > 1) on a few row tiles (a query slice of the
     // query-sharded coarse step): with m = 1 every range's running minimum starts
     // loose and the appended candidates overflow the small assignment buffers, and at
-    // >= a quarter of the SMs in row tiles the extra per-CTA pipeline fills cost more
+    // >= half of the SMs in row tiles the extra per-CTA pipeline fills cost more
     // than the split gains (measured, tools/coarse_cmp.py).
     int ncg = 1;
-    if (m > 1 && ntile * 4 <= ix.num_sms) {
+    if (m > 1 && ntile * 2 <= ix.num_sms) {
       int64_t best = -1;
       for (int c = 1; c <= ntn && c * 2 * m <= cap && c <= 16; c *= 2) {
         const int64_t t = ceil_div((int64_t)ntile * c, (int64_t)ix.num_sms) * ceil_div((int64_t)ntn, (int64_t)c);
