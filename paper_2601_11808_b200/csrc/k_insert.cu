@@ -155,16 +155,28 @@ __global__ void __launch_bounds__(1024) k_chunk_rank(const unsigned long long* _
   }
 }
 
-__global__ void k_chunk_prefix(int32_t* __restrict__ hist, int64_t nchunks, int nlist, int32_t* __restrict__ cnt) {
-  int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= nlist) return;
+// Warp per list: 32 chunks per step (independent loads), a warp scan, the running
+// carry (was one thread per list walking the chunks one dependent load at a time:
+// 47 us per 64k batch, 0.5 ms per 1M batch).
+__global__ void __launch_bounds__(256) k_chunk_prefix(int32_t* __restrict__ hist, int64_t nchunks, int nlist,
+                                                      int32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int l = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (l >= nlist) return;  // warp-uniform
   int run = 0;
-  for (int64_t c = 0; c < nchunks; ++c) {
-    int h = hist[c * nlist + l];
-    hist[c * nlist + l] = run;
-    run += h;
+  for (int64_t c0 = 0; c0 < nchunks; c0 += 32) {
+    const int64_t c = c0 + lane;
+    const int h = c < nchunks ? hist[c * nlist + l] : 0;
+    int x = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (c < nchunks) hist[c * nlist + l] = run + x - h;
+    run += __shfl_sync(kFull, x, 31);
   }
-  cnt[l] = run;
+  if (lane == 0) cnt[l] = run;
 }
 
 // Block-wide exclusive scan of one value per thread (1024 threads); returns the
@@ -466,7 +478,7 @@ cudaError_t launch_stable_ranks(Index& ix, int64_t n, int check_claim, cudaStrea
   cudaMemsetAsync(sc.chunk_hist, 0, sizeof(int32_t) * nchunks * nlist, s);
   k_chunk_rank<<<nchunks, 1024, 0, s>>>(sc.row_best, n, sc.row_status, sc.row_lid, ix.st.claim, check_claim,
                                          sc.row_list, sc.row_rank, sc.chunk_hist, nlist);
-  k_chunk_prefix<<<ceil_div(nlist, 256), 256, 0, s>>>(sc.chunk_hist, nchunks, nlist, sc.list_cnt);
+  k_chunk_prefix<<<ceil_div((int64_t)nlist * 32, 256), 256, 0, s>>>(sc.chunk_hist, nchunks, nlist, sc.list_cnt);
   ix.launches += 2;
   return cudaGetLastError();
 }

@@ -126,6 +126,8 @@ struct QInfo {
   int32_t pair;
   uint32_t qint;  // every value an integer with |v| <= 2048 (exact in fp16)
   uint32_t qover; // some |v| > 65504: no finite fp16 copy, every candidate is re-ranked
+  float thr0;     // the query's k-th distance bound (gthr) read by the loader: the epilogue
+                  // starts the item without a global load on its path (re-read every group)
 };
 
 struct TcPlan {
@@ -526,6 +528,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       const bool rv = trow < rec.nqt;
       const bool wv = qw < rec.nqt && !(a.dbg & 16);  // warp-uniform: the warp has a real row
       const int pair = rv ? a.inv_pairs[rec.p0 + trow] : -1;
+      const uint32_t thr0 = rv ? __ldcg(a.gthr + pair / a.nprobe) : 0xFF800000u;  // consumed at the QInfo write
       const float* qr = a.Q + (int64_t)(rv ? pair / a.nprobe : 0) * st.D;
       const uint32_t ta = tbase + ((uint32_t)(32 * qw) << 16) + ab * 64u;
       float nrm = 0.f;
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       tmem_st_wait();
       const int qb = (int)(i % NQI);
       PW(5, MBW(&q_read[qb], ((i / NQI) & 1u) ^ 1u, 12));  // item i - NQI's QInfo has been read
-      qinfo[qb * TM + row] = QInfo{nrm, pair, integ, over};
+      qinfo[qb * TM + row] = QInfo{nrm, pair, integ, over, __uint_as_float(thr0)};
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -611,8 +614,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       const bool wact = qw < rec.nqt;
       const int qglob = rv ? qi.pair / a.nprobe : 0;
       const float qn = qi.qn, sqn = sqrtf(qn);
-      float thr = rv ? __uint_as_float(__ldcg(a.gthr + qglob)) : -INFINITY;
-      float gnext = thr, tpub = thr;
+      float thr = rv ? qi.thr0 : -INFINITY;
+      // the current bound, read now: consumed at the first group (after its barrier
+      // waits), fresher than the loader's copy
+      float gnext = rv ? __uint_as_float(__ldcg(a.gthr + qglob)) : thr, tpub = thr;
       u64 keys[KP];
 #pragma unroll
       for (int t = 0; t < KP; ++t) keys[t] = t < KP - k ? 0ull : kPadKey;  // k-th = keys[KP-1]

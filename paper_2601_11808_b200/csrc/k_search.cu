@@ -245,8 +245,11 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (t == 0) carry[0] = carry[1] = 0;
   __syncthreads();
+  // prefix order: bucket 0 by list, then bucket 1 by list in REVERSE, so the lists the
+  // first bucket scanned last (still in L2) are the first the second bucket reads
+  auto ent = [&](int r) { return r < nlist ? r : nlist + (nent - 1 - r); };
   for (int l0 = 0; l0 < nent; l0 += 1024) {
-    const int l = l0 + t;
+    const int l = l0 + t < nent ? ent(l0 + t) : nent;  // entry at prefix rank l0 + t
     const int c = l < nent ? cnt[l] : 0;
     const int tl = (c + QT - 1) / QT;
     int v0 = c, v1 = tl;
@@ -296,17 +299,18 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int32_t* __restrict__ c
     tile_off[nent] = carry[1];
     ictr[I_NTILES] = carry[1];
     ictr[I_WORK] = 0;
-    // bucket 0 (each query's r0 nearest lists) = tiles [0, tile_off[nlist]): the
-    // phased tensor-core scan runs it to completion before bucket 1
-    const int t0 = nent > nlist ? tile_off[nlist] : carry[1];
+    // bucket 0 (each query's r0 nearest lists) = tiles [0, t0), t0 = the offset of the
+    // first entry of bucket 1 in prefix order (its last list): the phased
+    // tensor-core scan runs bucket 0 to completion before bucket 1
+    const int t0 = nent > nlist ? tile_off[nent - 1] : carry[1];
     ictr[I_NTILES0] = t0;
     ictr[I_WORK2] = t0;
   }
   __syncthreads();  // the block's offsets are visible to all of its threads
   // work items (list, first pair, number of pairs), bucket-major (k_work_fill fused)
   for (int e = t; e < nent; e += blockDim.x) {
-    const int c = off[e + 1] - off[e];
-    for (int tt = tile_off[e], j = 0; tt < tile_off[e + 1]; ++tt, ++j) {
+    const int c = cnt[e];  // (entries are not contiguous in prefix order: no off[e + 1] - off[e])
+    for (int tt = tile_off[e], j = 0; j * QT < c; ++tt, ++j) {
       work_l[tt] = e % nlist;
       work_p0[tt] = off[e] + j * QT;
       work_n[tt] = min(QT, c - j * QT);
