@@ -445,45 +445,104 @@ __global__ void __launch_bounds__(256) k_gs_fallback(GsArgs a, unsigned long lon
 }
 
 // Warp per query: top-k of its nprobe rows (dense) or partial lists (fallback
-// items), by (dist, id) (C4), padded (+inf, -1) (C5).
+// items), by (dist, id) (C4), padded (+inf, -1) (C5).  k <= 32 (RK): the running
+// top-k lives in registers, key j in lane j; a candidate vector with few
+// survivors of the k-th-key filter is inserted one key at a time (a ballot for
+// the position and one shuffle shift), a crowded one by a warp sort and a
+// bitonic merge.  k > 32: the shared-memory list (warp_topk_insert).
+template <bool RK>
 __global__ void __launch_bounds__(128) k_gs_select(GsArgs a, const int32_t* __restrict__ pair_pos,
                                                    const int32_t* __restrict__ item_of,
                                                    const unsigned long long* __restrict__ partial, int64_t nq,
                                                    float* __restrict__ dist, int64_t* __restrict__ ids) {
-  __shared__ u64 sm[4][256];
+  __shared__ u64 sm[4][RK ? 1 : 256];
   const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31, k = a.k;
   const int64_t q = (int64_t)blockIdx.x * 4 + wp;
   if (q >= nq) return;  // warp-uniform
   const DevState& st = a.st;
   u64* top = sm[wp];
   u64* tmp = top + k;
-  warp_topk_init(top, k);
+  u64 tk = kPadKey;    // RK: lane j < k holds the j-th smallest key so far
+  u64 kth = kPadKey;   // RK: the k-th smallest key (warp-uniform)
+  if (!RK) warp_topk_init(top, k);
+  // offer one candidate per lane (kPadKey: none)
+  auto offer = [&](u64 cand) {
+    if (!RK) {
+      warp_topk_insert(top, tmp, k, cand);
+      return;
+    }
+    unsigned m = __ballot_sync(kFull, cand < kth);
+    if (!m) return;
+    if (__popc(m) > 4) {
+      const u64 v = warp_sort32(cand < kth ? cand : kPadKey);  // ascending
+      u64 w = umin64(tk, __shfl_sync(kFull, v, 31 - lane));     // the 32 smallest, bitonic
+#pragma unroll
+      for (int j = 16; j > 0; j >>= 1) {
+        const u64 o = __shfl_xor_sync(kFull, w, j);
+        w = (lane & j) ? umax64(w, o) : umin64(w, o);
+      }
+      tk = lane < k ? w : kPadKey;
+    } else {
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const u64 c = __shfl_sync(kFull, cand, src);
+        if (!(c < kth)) continue;  // warp-uniform (kth tightened)
+        const int pos = __popc(__ballot_sync(kFull, tk < c));
+        const u64 up = __shfl_up_sync(kFull, tk, 1);
+        tk = lane == pos ? c : (lane > pos ? up : tk);
+        if (lane >= k) tk = kPadKey;
+        kth = __shfl_sync(kFull, tk, k - 1);
+      }
+    }
+    kth = __shfl_sync(kFull, tk, k - 1);
+  };
+  // per-probe metadata for 32 probes at once (lane r: probe r0 + r): one round of
+  // dependent loads per 32 probes instead of one per probe
+  int m_pos = 0, m_w = 0, m_dl = 0, m_nl = 0, m_p0 = 0;
+  long long m_doff = -1;
   for (int r = 0; r < a.nprobe; ++r) {
     const int pair = (int)(q * a.nprobe + r);
-    const int pos = pair_pos[pair];
-    const int w = item_of[pos];
-    const int64_t doff = a.doff[w];
+    if ((r & 31) == 0) {
+      if (r + lane < a.nprobe) {
+        m_pos = pair_pos[pair + lane];
+        m_w = item_of[m_pos];
+        m_doff = a.doff[m_w];
+        m_dl = a.dlen[m_w];
+        m_nl = a.nlive[m_w];
+        m_p0 = a.work_p0[m_w];
+      }
+    }
+    const int src = r & 31;
+    const int pos = __shfl_sync(kFull, m_pos, src);
+    const int64_t doff = (int64_t)__shfl_sync(kFull, m_doff, src);
     if (doff < 0) {
-      for (int j0 = 0; j0 < k; j0 += 32)
-        warp_topk_insert(top, tmp, k, j0 + lane < k ? partial[(size_t)pair * k + j0 + lane] : kPadKey);
+      for (int j0 = 0; j0 < k; j0 += 32) offer(j0 + lane < k ? partial[(size_t)pair * k + j0 + lane] : kPadKey);
       continue;
     }
-    const int dl = a.dlen[w], nl = a.nlive[w];
+    const int dl = __shfl_sync(kFull, m_dl, src), nl = __shfl_sync(kFull, m_nl, src);
     const int32_t* hdr = reinterpret_cast<const int32_t*>(a.dense + doff);
-    const float* rowp = a.dense + doff + gs_hdr(dl) + (int64_t)(pos - a.work_p0[w]) * kSlot * dl;
+    const float* rowp = a.dense + doff + gs_hdr(dl) + (int64_t)(pos - __shfl_sync(kFull, m_p0, src)) * kSlot * dl;
     for (int j0 = 0; j0 < nl; j0 += 4) {
       float d4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) d4[u] = j0 + u < nl ? __ldcs(rowp + (int64_t)(j0 + u) * kSlot + lane) : INFINITY;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t kth_hi = (uint32_t)(top[k - 1] >> 32);
+        const uint32_t kth_hi = (uint32_t)((RK ? kth : top[k - 1]) >> 32);
         const bool pass = d4[u] < INFINITY && __float_as_uint(d4[u]) <= kth_hi;
         if (!__ballot_sync(kFull, pass)) continue;
-        const u64 cand = pass ? make_key(d4[u], st.slab_ids[(size_t)hdr[j0 + u] * kSlot + lane]) : kPadKey;
-        warp_topk_insert(top, tmp, k, cand);
+        offer(pass ? make_key(d4[u], st.slab_ids[(size_t)hdr[j0 + u] * kSlot + lane]) : kPadKey);
       }
     }
+  }
+  if (RK) {
+    if (lane < k) {
+      const bool pad = tk == kPadKey;
+      dist[q * k + lane] = pad ? __int_as_float(0x7f800000) : key_dist(tk);
+      ids[q * k + lane] = pad ? -1 : (int64_t)key_id(tk);
+    }
+    return;
   }
   for (int j = lane; j < k; j += 32) {
     const u64 key = top[j];
@@ -522,7 +581,10 @@ cudaError_t launch_select_gs(Index& ix, const float* d_q, int64_t nq, int k, int
   Scratch& sc = ix.sc;
   GsArgs a{ix.st,      d_q,       nprobe,    k,         sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n,
            sc.gs_a,    sc.gs_qn,  sc.gs_qs,  sc.item_doff, sc.item_dlen, sc.item_nlive, sc.dense};
-  k_gs_select<<<ceil_div(nq, 4), 128, 0, s>>>(a, sc.pair_pos, sc.item_of, sc.partial, nq, d_dist, d_ids);
+  if (k <= 32)
+    k_gs_select<true><<<ceil_div(nq, 4), 128, 0, s>>>(a, sc.pair_pos, sc.item_of, sc.partial, nq, d_dist, d_ids);
+  else
+    k_gs_select<false><<<ceil_div(nq, 4), 128, 0, s>>>(a, sc.pair_pos, sc.item_of, sc.partial, nq, d_dist, d_ids);
   ix.launches += 1;
   return cudaGetLastError();
 }
