@@ -1222,7 +1222,10 @@ cudaError_t launch_coarse_tc(Index& ix, const float* d_x, int64_t n, int m, unsi
       const int64_t ntile = ceil_div(nr, TM);
       k_rows_tiles<<<ntile, 4 * TM, 0, s>>>(xr, nr, D, Dp, xt, xn);
       // split the N-tiles over CTAs until every SM has a CTA
-      int ncg = ntile >= ix.num_sms ? 1 : (int)ceil_div(ix.num_sms, ntile);
+      // (from half the SMs in row tiles on, one CTA per row tile: the extra waves and
+      // per-CTA fills of a split cost more than it gains, tools/ncg_sweep.py)
+      int ncg = 2 * ntile >= ix.num_sms ? 1 : (int)ceil_div(ix.num_sms, ntile);
+      if ((ix.dbg >> 16) & 7) ncg = (ix.dbg >> 16) & 7;  // experiments (SIVF_OPT_DEBUG bits 16-18)
       if (ncg > ntn) ncg = ntn;
       const int ntpc = (int)ceil_div(ntn, ncg);
       CoarseArgs a{xt, xn, sc.c_tiles, sc.c_norm, sc.c_csa, sc.c_cnb, nr, Dp, st.nlist, m, 0,

@@ -14,6 +14,7 @@ for rep in range(2):
     ix = S.Index(D, NL, N, S.num_slabs_for(N, NL), max_batch=max(B, 65536), max_queries=16, max_k=16,
                  max_train=262144, seed=1)
     ix.train(torch.from_numpy(gen.train(262144)).cuda(), niter=4)
+    ix.set_option(S.OPT_COARSE_SELECT, int(os.environ.get("COARSE_SELECT", "1")))
     torch.cuda.synchronize()
     ix.profile(rep == 1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
