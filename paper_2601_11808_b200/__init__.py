@@ -104,6 +104,7 @@ OPT_RANK_SPLIT = 5
 OPT_COARSE_SELECT = 6
 OPT_STEP_GRAPH = 7
 OPT_CONCURRENT = 8
+OPT_SEED_LIST = 9
 
 PHASES = ("assign", "append", "delete", "coarse", "invmap", "scan", "merge", "reclaim")
 

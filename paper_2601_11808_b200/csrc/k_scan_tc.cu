@@ -840,6 +840,113 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
 }
 
 
+// Per-list seed of the per-query bound (SIVF_OPT_SEED_LIST): block per list l;
+// the first live slab of l holding >= k valid slots is staged once in shared
+// memory, and every query whose NEAREST probed list is l (its rank-0 pair, found in
+// the inverse map's entry l) gets the k-th smallest of its exact distances to
+// those slots.  Any k real candidates bound the final k-th distance from above,
+// so this prunes work only, never results.  The distances are the scan's exact
+// re-rank form (fp32 differences, fmaf squares; on integer data it and
+// ||q||^2 + t are exact) summed in four interleaved partial sums: two orders of a
+// sum of D non-negative terms differ by at most D 2^-23 relative, so the k-th value
+// is inflated by (1 + (Dp+2) 2^-23), rounded up, and bounds the scan's own values
+// of those k candidates.  One slab per list (~10 queries
+// each at SIFT1M / nprobe 32) instead of one per query: ~100x fewer payload bytes
+// than k_seed_bound.
+__global__ void __launch_bounds__(256) k_seed_list(DevState st, const float* __restrict__ Q, int nprobe, int k,
+                                                   const int32_t* __restrict__ inv_off,
+                                                   const int32_t* __restrict__ inv_cnt,
+                                                   const int32_t* __restrict__ inv_pairs, uint32_t* __restrict__ gthr) {
+  __shared__ float xs[kSlot][129];  // Dp <= 128 (+1: conflict-free rows)
+  __shared__ float qs[8][128];
+  __shared__ int32_t q0[256];
+  __shared__ int s_slab, s_n0;
+  __shared__ uint32_t s_bm;
+  const int l = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cnt = inv_cnt[l];
+  if (cnt == 0) return;  // block-uniform
+  const int Dp = st.Dp;
+  if (threadIdx.x == 0) s_n0 = 0;
+  __syncthreads();
+  if (w == 0) {  // the list's first live slab with >= k valid slots (beside the pair scan)
+    const int len = st.dir_len[l];
+    const int32_t* dir = st.dir_arena + st.dir_off[l];
+    int slab = -1;
+    uint32_t bmf = 0u;
+    for (int j0 = 0; j0 < len && slab < 0; j0 += 32) {
+      const int j = j0 + lane;
+      int sl = 0;
+      uint32_t bm = 0u;
+      if (j < len) {
+        sl = dir[j];
+        bm = st.bitmap[sl];
+      }
+      const unsigned ok = __ballot_sync(kFull, __popc(bm) >= k);
+      if (ok) {
+        const int src = __ffs(ok) - 1;
+        slab = __shfl_sync(kFull, sl, src);
+        bmf = __shfl_sync(kFull, bm, src);
+      }
+    }
+    if (lane == 0) {
+      s_slab = slab;
+      s_bm = bmf;
+    }
+  } else {  // the queries whose nearest probed list is l (rank-0 pairs of entry l)
+    const int off = inv_off[l];
+    for (int i = threadIdx.x - 32; i < cnt; i += blockDim.x - 32) {
+      const int p = inv_pairs[off + i];
+      if (p % nprobe == 0) {
+        const int pos = atomicAdd(&s_n0, 1);
+        if (pos < 256) q0[pos] = p / nprobe;
+      }
+    }
+  }
+  __syncthreads();
+  const int slab = s_slab;
+  if (s_n0 == 0 || slab < 0) return;  // block-uniform (e.g. no query starts here at nlist 16384)
+  const float* xsrc = st.payload + (size_t)slab * kSlot * Dp;
+  for (int i = threadIdx.x; i < kSlot * (Dp >> 2); i += blockDim.x) {
+    const int n = i & 31, c4 = i >> 5;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(xsrc + pay_off(Dp, n, c4)));
+    xs[n][4 * c4] = v.x, xs[n][4 * c4 + 1] = v.y, xs[n][4 * c4 + 2] = v.z, xs[n][4 * c4 + 3] = v.w;
+  }
+  __syncthreads();
+  const int n0 = min(s_n0, 256);
+  const uint32_t bm = s_bm;
+  const float infl = 1.f + (float)(Dp + 2) * 0x1p-23f;
+  for (int t = w; t < n0; t += 8) {
+    const int q = q0[t];
+    for (int d = lane; d < Dp; d += 32) qs[w][d] = d < st.D ? __ldg(Q + (int64_t)q * st.D + d) : 0.f;
+    __syncwarp();
+    // four independent partial sums (any order: the inflation below covers the
+    // reordering against the scan's sequential sum, (Dp+2) 2^-23 relative)
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int d = 0; d < Dp; d += 4) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float tt = qs[w][d + e] - xs[lane][d + e];
+        a4[e] = fmaf(tt, tt, a4[e]);
+      }
+    }
+    const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    const uint32_t key = ((bm >> lane) & 1u) ? __float_as_uint(acc) : 0x7f800000u;  // >= 0: bit order
+    // the k-th smallest over the 32 slots: bitonic sort of the keys across the warp
+    uint32_t v = key;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const uint32_t o = __shfl_xor_sync(kFull, v, stride);
+        const bool up = (lane & size) == 0 || size == 32, lower = (lane & stride) == 0;
+        v = (lower == up) ? min(v, o) : max(v, o);
+      }
+    const uint32_t kth = __shfl_sync(kFull, v, k - 1);
+    if (lane == 0 && kth < 0x7f800000u) atomicMin(gthr + q, __float_as_uint(__fmul_ru(__uint_as_float(kth), infl)));
+    __syncwarp();
+  }
+}
+
 // Seed of the per-query bound gthr[q] on its final k-th distance: exact
 // distances from q to the live slots of the first `nseed` live slabs of its
 // nearest probed list (probes are sorted, rank 0 first).  Any k real
@@ -951,7 +1058,14 @@ cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaS
 int scan_tc_tile() { return TM; }
 
 cudaError_t launch_seed_bound(Index& ix, const float* d_q, int64_t nq, int k, int nprobe, cudaStream_t s) {
-  if (ix.seed_slabs <= 0 || nq <= 0 || ix.st.Dp > 128 || k > 32) return cudaSuccess;
+  // (only with >= 4 queries per list on average: a block per list must amortise its
+  // directory walk and slab load; the sliding step's 1k queries or nlist 16384 do not)
+  if (ix.seed_list && nq >= 4 * (int64_t)ix.st.nlist && ix.st.Dp <= 128 && k <= 32 && !ix.st.conc) {
+    k_seed_list<<<ix.st.nlist, 256, 0, s>>>(ix.st, d_q, nprobe, k, ix.sc.inv_off, ix.sc.inv_cnt, ix.sc.inv_pairs,
+                                            ix.sc.gthr);
+    ix.launches += 1;
+  }
+  if (ix.seed_slabs <= 0 || nq <= 0 || ix.st.Dp > 128 || k > 32) return cudaGetLastError();
   k_seed_bound<<<ceil_div(nq, 4), 128, 0, s>>>(ix.st, d_q, nq, nprobe, ix.sc.probes, ix.seed_slabs, k, ix.sc.gthr);
   ix.launches += 1;
   return cudaGetLastError();

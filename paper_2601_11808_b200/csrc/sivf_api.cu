@@ -855,6 +855,7 @@ sivf_rc sivf_set_option(sivf_index h, int32_t option, int64_t value) {
     case 99: ix->dbg = (int)value; return SIVF_OK;  // SIVF_OPT_DEBUG: experiments only
     case 98: ix->tc_max_stages = (int)value; return SIVF_OK;  // experiments only: scan stage-ring cap
     case SIVF_OPT_CONCURRENT: ix->st.conc = value != 0; return SIVF_OK;
+    case SIVF_OPT_SEED_LIST: ix->seed_list = value != 0; return SIVF_OK;
     case SIVF_OPT_SEED_SLABS:
       if (value < 0 || value > (1 << 20)) return SIVF_E_INVALID_ARG;
       ix->seed_slabs = (int)value;
