@@ -89,7 +89,7 @@ def sift_shape(seed: int = 0x51F7, dim: int = 128) -> Shape:
 
 
 def gist_shape(seed: int = 0x6157, dim: int = 960) -> Shape:
-    return Shape(seed=seed, dim=dim, kind=GIST, M=50, r=48, a=0.12, b=0.06, sigma=0.015)
+    return Shape(seed=seed, dim=dim, kind=GIST, M=50, r=48, a=0.12, b=0.15, sigma=0.015)
 
 
 def uniform_shape(seed: int, dim: int) -> Shape:
