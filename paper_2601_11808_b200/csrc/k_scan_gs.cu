@@ -445,57 +445,87 @@ __global__ void __launch_bounds__(256) k_gs_fallback(GsArgs a, unsigned long lon
 }
 
 // Warp per query: top-k of its nprobe rows (dense) or partial lists (fallback
-// items), by (dist, id) (C4), padded (+inf, -1) (C5).  k <= 32 (RK): the running
-// top-k lives in registers, key j in lane j; a candidate vector with few
-// survivors of the k-th-key filter is inserted one key at a time (a ballot for
-// the position and one shuffle shift), a crowded one by a warp sort and a
-// bitonic merge.  k > 32: the shared-memory list (warp_topk_insert).
-template <bool RK>
+// items), by (dist, id) (C4), padded (+inf, -1) (C5).  The running top-k lives in
+// registers, key 32 r + lane in tk[r] (R registers per lane, k <= 32 R); a
+// candidate vector with few survivors of the k-th-key filter is inserted one key at
+// a time (ballots for the position, one shuffle shift per register), a crowded one
+// by a warp sort and a bitonic merge (R = 1) or through the shared-memory list
+// (warp_topk_insert, R > 1).
+template <int R>
 __global__ void __launch_bounds__(128) k_gs_select(GsArgs a, const int32_t* __restrict__ pair_pos,
                                                    const int32_t* __restrict__ item_of,
                                                    const unsigned long long* __restrict__ partial, int64_t nq,
                                                    float* __restrict__ dist, int64_t* __restrict__ ids) {
-  __shared__ u64 sm[4][RK ? 1 : 256];
+  __shared__ u64 sm[4][R == 1 ? 1 : 64 * R];
   const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31, k = a.k;
   const int64_t q = (int64_t)blockIdx.x * 4 + wp;
   if (q >= nq) return;  // warp-uniform
   const DevState& st = a.st;
   u64* top = sm[wp];
   u64* tmp = top + k;
-  u64 tk = kPadKey;    // RK: lane j < k holds the j-th smallest key so far
-  u64 kth = kPadKey;   // RK: the k-th smallest key (warp-uniform)
-  if (!RK) warp_topk_init(top, k);
+  u64 tk[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) tk[r] = kPadKey;
+  u64 kth = kPadKey;  // the k-th smallest key (warp-uniform)
+  const int rk = (k - 1) >> 5, lk = (k - 1) & 31;
+  auto kth_of = [&]() {
+    u64 v = tk[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) v = r == rk ? tk[r] : v;
+    return __shfl_sync(kFull, v, lk);
+  };
   // offer one candidate per lane (kPadKey: none)
   auto offer = [&](u64 cand) {
-    if (!RK) {
-      warp_topk_insert(top, tmp, k, cand);
-      return;
-    }
     unsigned m = __ballot_sync(kFull, cand < kth);
     if (!m) return;
     if (__popc(m) > 4) {
-      const u64 v = warp_sort32(cand < kth ? cand : kPadKey);  // ascending
-      u64 w = umin64(tk, __shfl_sync(kFull, v, 31 - lane));     // the 32 smallest, bitonic
+      if (R == 1) {
+        const u64 v = warp_sort32(cand < kth ? cand : kPadKey);  // ascending
+        u64 w = umin64(tk[0], __shfl_sync(kFull, v, 31 - lane));  // the 32 smallest, bitonic
 #pragma unroll
-      for (int j = 16; j > 0; j >>= 1) {
-        const u64 o = __shfl_xor_sync(kFull, w, j);
-        w = (lane & j) ? umax64(w, o) : umin64(w, o);
+        for (int j = 16; j > 0; j >>= 1) {
+          const u64 o = __shfl_xor_sync(kFull, w, j);
+          w = (lane & j) ? umax64(w, o) : umin64(w, o);
+        }
+        tk[0] = lane < k ? w : kPadKey;
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (32 * r + lane < k) top[32 * r + lane] = tk[r];
+        __syncwarp();
+        warp_topk_insert(top, tmp, k, cand);
+#pragma unroll
+        for (int r = 0; r < R; ++r) tk[r] = 32 * r + lane < k ? top[32 * r + lane] : kPadKey;
+        __syncwarp();
       }
-      tk = lane < k ? w : kPadKey;
     } else {
       while (m) {
         const int src = __ffs(m) - 1;
         m &= m - 1;
         const u64 c = __shfl_sync(kFull, cand, src);
         if (!(c < kth)) continue;  // warp-uniform (kth tightened)
-        const int pos = __popc(__ballot_sync(kFull, tk < c));
-        const u64 up = __shfl_up_sync(kFull, tk, 1);
-        tk = lane == pos ? c : (lane > pos ? up : tk);
-        if (lane >= k) tk = kPadKey;
-        kth = __shfl_sync(kFull, tk, k - 1);
+        int pos = 0;
+        u64 up[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          pos += __popc(__ballot_sync(kFull, tk[r] < c));
+          up[r] = __shfl_up_sync(kFull, tk[r], 1);  // key 32 r + lane - 1 (lane > 0)
+        }
+#pragma unroll
+        for (int r = R - 1; r > 0; --r) {
+          const u64 carry = __shfl_sync(kFull, tk[r - 1], 31);
+          if (lane == 0) up[r] = carry;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int p = 32 * r + lane;
+          tk[r] = p == pos ? c : (p > pos ? up[r] : tk[r]);
+          if (p >= k) tk[r] = kPadKey;
+        }
+        kth = kth_of();
       }
     }
-    kth = __shfl_sync(kFull, tk, k - 1);
+    kth = kth_of();
   };
   // per-probe metadata for 32 probes at once (lane r: probe r0 + r): one round of
   // dependent loads per 32 probes instead of one per probe
@@ -529,26 +559,21 @@ __global__ void __launch_bounds__(128) k_gs_select(GsArgs a, const int32_t* __re
       for (int u = 0; u < 4; ++u) d4[u] = j0 + u < nl ? __ldcs(rowp + (int64_t)(j0 + u) * kSlot + lane) : INFINITY;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t kth_hi = (uint32_t)((RK ? kth : top[k - 1]) >> 32);
+        const uint32_t kth_hi = (uint32_t)(kth >> 32);
         const bool pass = d4[u] < INFINITY && __float_as_uint(d4[u]) <= kth_hi;
         if (!__ballot_sync(kFull, pass)) continue;
         offer(pass ? make_key(d4[u], st.slab_ids[(size_t)hdr[j0 + u] * kSlot + lane]) : kPadKey);
       }
     }
   }
-  if (RK) {
-    if (lane < k) {
-      const bool pad = tk == kPadKey;
-      dist[q * k + lane] = pad ? __int_as_float(0x7f800000) : key_dist(tk);
-      ids[q * k + lane] = pad ? -1 : (int64_t)key_id(tk);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j = 32 * r + lane;
+    if (j < k) {
+      const bool pad = tk[r] == kPadKey;
+      dist[q * k + j] = pad ? __int_as_float(0x7f800000) : key_dist(tk[r]);
+      ids[q * k + j] = pad ? -1 : (int64_t)key_id(tk[r]);
     }
-    return;
-  }
-  for (int j = lane; j < k; j += 32) {
-    const u64 key = top[j];
-    const bool pad = key == kPadKey;
-    dist[q * k + j] = pad ? __int_as_float(0x7f800000) : key_dist(key);
-    ids[q * k + j] = pad ? -1 : (int64_t)key_id(key);
   }
 }
 
@@ -582,9 +607,9 @@ cudaError_t launch_select_gs(Index& ix, const float* d_q, int64_t nq, int k, int
   GsArgs a{ix.st,      d_q,       nprobe,    k,         sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n,
            sc.gs_a,    sc.gs_qn,  sc.gs_qs,  sc.item_doff, sc.item_dlen, sc.item_nlive, sc.dense};
   if (k <= 32)
-    k_gs_select<true><<<ceil_div(nq, 4), 128, 0, s>>>(a, sc.pair_pos, sc.item_of, sc.partial, nq, d_dist, d_ids);
+    k_gs_select<1><<<ceil_div(nq, 4), 128, 0, s>>>(a, sc.pair_pos, sc.item_of, sc.partial, nq, d_dist, d_ids);
   else
-    k_gs_select<false><<<ceil_div(nq, 4), 128, 0, s>>>(a, sc.pair_pos, sc.item_of, sc.partial, nq, d_dist, d_ids);
+    k_gs_select<4><<<ceil_div(nq, 4), 128, 0, s>>>(a, sc.pair_pos, sc.item_of, sc.partial, nq, d_dist, d_ids);
   ix.launches += 1;
   return cudaGetLastError();
 }
