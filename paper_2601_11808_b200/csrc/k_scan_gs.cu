@@ -45,12 +45,13 @@ namespace sivf {
 namespace {
 
 constexpr int GQ = 128;          // queries per work item (UMMA M)
-constexpr int GG = 4;            // slabs per group (UMMA N = 128)
-constexpr int NSTG = 3;          // stage ring depth
-constexpr int NBG = 2;           // TMEM accumulators (128 columns each)
+constexpr int GG = 8;            // slabs per group (UMMA N = 256: each streamed A chunk serves 8 slabs)
+constexpr int NSTG = 2;          // stage ring depth
+constexpr int NBG = 2;           // TMEM accumulators (GN = 256 columns each)
+constexpr int GN = GG * 32;      // columns per group
 constexpr int NGM = 4;           // group metadata ring
 constexpr int ACH = 32768;       // A chunk bytes: 128 rows x 64 dims x 2 B x (hi, lo)
-constexpr int STG = 65536;       // stage: A chunk + B chunk (4 slabs x 4 row groups x 2 KB)
+constexpr int STG = ACH + GG * 4 * 2048;  // stage: A chunk + B chunk (8 slabs x 4 row groups x 2 KB)
 constexpr int GS_THREADS = 6 * 32;
 
 struct GsMeta {
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) k_scan_gs(GsArgs a) {
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_holder, NBG * 128);
+  if (warp == 1) tmem_alloc(tmem_holder, NBG * GN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -257,8 +258,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) k_scan_gs(GsArgs a) {
           bulk_g2s(m.xn + kSlot * lane, st.slab_norm + (size_t)r.x * kSlot, kSlot * 4, &gm_full[gi]);
           bulk_g2s(m.xs + kSlot * lane, st.slab_xs + (size_t)r.x * kSlot, kSlot * 4, &gm_full[gi]);
         }
-        const int jb = ((lane - 1) >> 2) & 3, rg = (lane - 1) & 3;
-        const uint32_t sj = __shfl_sync(kFull, r.x, jb);
+        const uint32_t sr = r.x;  // lane < nv: slab of the group's position `lane`
         for (int c = 0; c < nch; ++c, ++cseq) {
           const int stg = (int)(cseq % NSTG);
           if (lane == 0) mbar_wait(&empty[stg], ((cseq / NSTG) & 1u) ^ 1u);
@@ -269,11 +269,11 @@ __global__ void __launch_bounds__(GS_THREADS, 1) k_scan_gs(GsArgs a) {
             bulk_g2s(sb, reinterpret_cast<const unsigned char*>(a.gs_a) + ((size_t)w * nch + c) * ACH, ACH, &full[stg]);
           }
           __syncwarp();
-          if (lane >= 1 && lane <= 4 * nv)
-            bulk_g2s(sb + ACH + (jb * 4 + rg) * 2048,
-                     reinterpret_cast<const unsigned char*>(st.payload_g) + (size_t)sj * recg_bytes(st.Dg) +
-                         ((size_t)rg * nch + c) * 2048,
-                     2048, &full[stg]);
+          if (lane < nv)  // slab `lane`'s chunk c: its 4 row-group pieces, one 8-KB copy (chunk-major record)
+            bulk_g2s(sb + ACH + lane * 8192,
+                     reinterpret_cast<const unsigned char*>(st.payload_g) + (size_t)sr * recg_bytes(st.Dg) +
+                         (size_t)c * 8192,
+                     8192, &full[stg]);
         }
         ++gseq;
       };
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) k_scan_gs(GsArgs a) {
       const uint32_t b = gseq % NBG;
       mbar_wait(&acc_free[b], ((gseq / NBG) & 1u) ^ 1u);
       tc_fence_after();
-      const uint32_t dt = tbase + b * 128u;
+      const uint32_t dt = tbase + b * (uint32_t)GN;
       for (int c = 0; c < nch; ++c, ++cseq) {
         const int stg = (int)(cseq % NSTG);
         mbar_wait(&full[stg], (cseq / NSTG) & 1u);
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) k_scan_gs(GsArgs a) {
       float* rowp = a.dense + a.doff[item] + gs_hdr(dl) + (int64_t)row * kSlot * dl;
       for (int j = 0; j < m.nv; ++j) {
         uint32_t v[32];
-        tmem_ld32(tbase + ((uint32_t)(32 * qw) << 16) + b * 128u + 32u * (uint32_t)j, v);
+        tmem_ld32(tbase + ((uint32_t)(32 * qw) << 16) + b * (uint32_t)GN + 32u * (uint32_t)j, v);
         tmem_ld_wait();
         if (rv) {
           const uint32_t bm = m.bm[j];
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) k_scan_gs(GsArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tbase, NBG * 128);
+  if (warp == 1) tmem_dealloc(tbase, NBG * GN);
 }
 
 // Items without a dense region: per-pair top-k on CUDA cores (warp per pair,
