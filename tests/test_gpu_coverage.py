@@ -149,6 +149,37 @@ def test_search_graph_cache_replay():
     assert len(set(launches)) == 1 and launches[0] > 0
 
 
+# ------------------------------------------------------------------ per-list seed of the bounds
+@pytest.mark.parametrize("kind", ["sift", "float"])
+def test_seed_list_changes_nothing(kind):
+    # SIVF_OPT_SEED_LIST (default on with >= 4 queries per list): the k-th distance bounds
+    # seeded from each query's nearest list prune work only.  The same index and queries
+    # with and without it: identical results, and equal to the oracle (integer data) or
+    # within the float tolerance (float data)
+    gen = Generator(sift_shape(seed=0x5EED))
+    if kind == "sift":
+        X, Q = gen.range(0, 30000), gen.queries(0, 2000)
+    else:
+        rng = np.random.default_rng(5)
+        X = rng.random((30000, 128), dtype=np.float32)
+        Q = rng.random((2000, 128), dtype=np.float32)
+    C = O.kmeans(X[:8000], 64, 6, 12)
+    g, o = make_pair(128, 64, 30000, C, max_batch=30000, max_queries=2000)
+    ins(g, o, np.arange(30000), X)
+    dele(g, o, np.arange(0, 30000, 9))
+    for k, npb in ((10, 16), (32, 8), (1, 4)):
+        g.set_option(S.OPT_SEED_LIST, 1)
+        d1, i1 = g.search(T(Q), k, npb)
+        g.set_option(S.OPT_SEED_LIST, 0)
+        d2, i2 = g.search(T(Q), k, npb)
+        assert torch.equal(i1, i2) and torch.equal(d1, d2), (kind, k, npb)
+        if kind == "sift":
+            od, oi, _ = o.search(Q, k, npb)
+            assert np.array_equal(i1.cpu().numpy(), oi) and np.array_equal(d1.cpu().numpy(), od)
+        else:
+            assert srch(g, o, Q, k, npb, exact=False) <= 3
+
+
 # ------------------------------------------------------------------ nprobe = max_nprobe = 1024
 def test_nprobe_1024_full_probe():
     # k_select_probes needs 64 nprobe B of shared memory (64 KB at 1024);
