@@ -201,6 +201,9 @@ __device__ __forceinline__ uint32_t pick32(const uint32_t (&v)[32], int c) {
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 #ifdef SIVF_TC_PROF
 #ifdef SIVF_TC_NOCOUNT  // timing builds: no contended counters on the slow path
@@ -601,6 +604,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
     const float esub = 0x1p-23f * 1.001f * sqrtf((float)Dh);
     const int dbg = a.dbg;
     uint32_t gseq = 0;
+    // item-end hand-over of a row's list between the sets: barrier 1 + qw (h = 1's list
+    // is in mrg) and 5 + qw (h = 0 has consumed mrg); each side only waits for the
+    // other's arrival, so h = 1 goes on to its next item while h = 0 merges
+    if (h == 0) named_bar_arrive(5 + qw, 64);  // mrg starts free
     for (uint32_t i = 0;; ++i) {
       const int slot = (int)(i % NITEM);
       PW(4, MBW(&item_full[slot], (i / NITEM) & 1u, 13));
@@ -802,11 +809,16 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       long long _te = clock64();
 #endif
       // merge the two sets' lists of each row: h = 1 hands its list over in smem
-      if (h == 1 && rv) {
+      if (h == 1) {
+        named_bar_sync(5 + qw, 64);  // the previous item's list has been merged
+        if (rv) {
 #pragma unroll
-        for (int t = 0; t < KP; ++t) mrg[row * KP + t] = keys[t];
+          for (int t = 0; t < KP; ++t) mrg[row * KP + t] = keys[t];
+        }
+        named_bar_arrive(1 + qw, 64);
+      } else {
+        PW(3, named_bar_sync(1 + qw, 64));
       }
-      PW(3, named_bar_sync(1 + qw, 64));
       if (h == 0 && rv) {
         for (int t = KP - k; t < KP; ++t) {
           const u64 key = mrg[row * KP + t];
@@ -819,7 +831,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
           if (t >= KP - k) a.partial[(size_t)qi.pair * k + (t - (KP - k))] = keys[t];
         if (kth != kPadKey) atomicMin(&a.gthr[qglob], __float_as_uint(key_dist(kth)));
       }
-      named_bar_sync(1 + qw, 64);
+      if (h == 0) named_bar_arrive(5 + qw, 64);  // mrg consumed
       if (lane == 0) {
         mbar_arrive(&item_empty[slot]);
       }
@@ -827,6 +839,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_scan_tc(TcArgs a) {
       pw[9] += clock64() - _te;
 #endif
     }
+    if (h == 1) named_bar_sync(5 + qw, 64);  // h = 0's last "mrg consumed" arrival
   }
 #ifdef SIVF_TC_PROF
   if (blockIdx.x < 2 && lane == 0)
