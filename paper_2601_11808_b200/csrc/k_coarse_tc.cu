@@ -810,7 +810,8 @@ __global__ void __launch_bounds__(32 * SELW, 3) k_coarse_select(const float* __r
   for (int k = lane; k < Dp; k += 32) xs[k] = k < D ? __ldg(xr + k) : 0.f;
   const unsigned lt = (1u << lane) - 1u;
   SELCLK(0);
-  // 1. U' = the m-th smallest A of the row (m = 1: the minimum)
+  // 1. U' >= the m-th smallest A of the row, within 8 values above it (m = 1: the
+  //    minimum); any such U' makes step 2's S a superset of every candidate
   float Up;
   {
     float mn = INFINITY;
@@ -848,8 +849,15 @@ __global__ void __launch_bounds__(32 * SELW, 3) k_coarse_select(const float* __r
             int c = 0;
 #pragma unroll
             for (int t = 0; t < CCAP / 32; ++t) c += u[t] <= mid ? 1 : 0;
-            if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) h2 = mid;
-            else lo = mid + 1;
+            const int tot = (int)__reduce_add_sync(kFull, (unsigned)c);
+            if (tot >= m) {
+              h2 = mid;
+              // any key with m..m+8 values at or below it bounds the m-th smallest from
+              // above: the superset S below only grows by those few columns
+              if (tot <= m + 8) break;
+            } else {
+              lo = mid + 1;
+            }
           }
         } else {
           while (lo < h2) {
@@ -857,8 +865,13 @@ __global__ void __launch_bounds__(32 * SELW, 3) k_coarse_select(const float* __r
             int c = 0;
 #pragma unroll
             for (int i = 0; i < NPL; ++i) c += fkey(A[i]) <= mid ? 1 : 0;
-            if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) h2 = mid;
-            else lo = mid + 1;
+            const int tot = (int)__reduce_add_sync(kFull, (unsigned)c);
+            if (tot >= m) {
+              h2 = mid;
+              if (tot <= m + 8) break;  // as above
+            } else {
+              lo = mid + 1;
+            }
           }
         }
         Up = fkey_inv(h2);
