@@ -807,7 +807,12 @@ __global__ void __launch_bounds__(32 * SELW, 3) k_coarse_select(const float* __r
   auto Ecol = [&](int c) { return fmaf(sq, csa_s[c], qnb + cnb_s[c]); };  // the per-column form
   const float Emax = __fmaf_ru(sq, __uint_as_float(cmax[0]), __fadd_ru(qnb, __uint_as_float(cmax[1])));
   const float* xr = X + row * (int64_t)D;
-  for (int k = lane; k < Dp; k += 32) xs[k] = k < D ? __ldg(xr + k) : 0.f;
+  // the row itself is staged only for an exact re-rank (most assignment rows have a
+  // single certain candidate and never read it)
+  auto load_xs = [&]() {
+    for (int k = lane; k < Dp; k += 32) xs[k] = k < D ? __ldg(xr + k) : 0.f;
+    __syncwarp();
+  };
   const unsigned lt = (1u << lane) - 1u;
   SELCLK(0);
   // 1. U' >= the m-th smallest A of the row, within 8 values above it (m = 1: the
@@ -923,8 +928,15 @@ __global__ void __launch_bounds__(32 * SELW, 3) k_coarse_select(const float* __r
         const uint32_t mid = lo + ((hi - lo) >> 1);
         int c = 0;
         each([&](uint32_t u) { c += u <= mid ? 1 : 0; });
-        if ((int)__reduce_add_sync(kFull, (unsigned)c) >= m) hi = mid;
-        else lo = mid + 1;
+        const int tot = (int)__reduce_add_sync(kFull, (unsigned)c);
+        if (tot >= m) {
+          hi = mid;
+          // U >= the m-th smallest upper bound: the candidates below stay a superset of
+          // the exact top-m (a few more may need the exact re-rank)
+          if (tot <= m + 2) break;
+        } else {
+          lo = mid + 1;
+        }
       }
       Ub = hi;
     }
@@ -1024,10 +1036,12 @@ __global__ void __launch_bounds__(32 * SELW, 3) k_coarse_select(const float* __r
       q_w[e] = (uint8_t)w;
       q_l[e] = cand[lane + 32];
     }
+    load_xs();  // read by the block's re-rank queue after the barrier
     path = 1;
     SELCLK(5);
     break;
   }
+  load_xs();
   if (MODE == 1) warp_topk_init(top, m);
   for (int i0 = 0; i0 < total; i0 += 32) {
     const int i = i0 + lane;
