@@ -338,12 +338,13 @@ sivf_rc sivf_profile_enable(sivf_index ix, int32_t on);
  *                      the approximate distance matrix and selects per row (exact
  *                      m-th upper bound by bisection, candidates, exact dist32
  *                      re-rank); 0 = the fused two-pass epilogue.  Same results.
- *   SIVF_OPT_SEED_LIST (default 1): before the tensor-core scan, every query's bound
+ *   SIVF_OPT_SEED_LIST (default 0): before the tensor-core scan, every query's bound
  *                      on its k-th distance is seeded with the k-th smallest exact
  *                      distance to the first live slab (>= k valid slots) of its
  *                      nearest probed list, one staged slab per list (batches of
  *                      >= 4 queries per list on average; not in concurrent mode).
- *                      Changes speed only, never results. */
+ *                      Changes speed only, never results (measured neutral on the
+ *                      SIFT1M-shaped step: the kernel costs about what it saves). */
 enum { SIVF_OPT_TC_SCAN = 1, SIVF_OPT_TC_TWO_PHASE = 2, SIVF_OPT_TC_COARSE = 3, SIVF_OPT_SEED_SLABS = 4,
        SIVF_OPT_RANK_SPLIT = 5, SIVF_OPT_COARSE_SELECT = 6, SIVF_OPT_STEP_GRAPH = 7, SIVF_OPT_CONCURRENT = 8,
        SIVF_OPT_SEED_LIST = 9 };

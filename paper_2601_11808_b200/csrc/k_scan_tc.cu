@@ -918,6 +918,11 @@ __global__ void __launch_bounds__(256) k_seed_list(DevState st, const float* __r
   __syncthreads();
   const int slab = s_slab;
   if (s_n0 == 0 || slab < 0) return;  // block-uniform (e.g. no query starts here at nlist 16384)
+  const int n0 = min(s_n0, 256);
+  // each warp's first query row is fetched together with the slab (two DRAM round
+  // trips overlapped instead of chained)
+  if (w < n0)
+    for (int d = lane; d < Dp; d += 32) qs[w][d] = d < st.D ? __ldg(Q + (int64_t)q0[w] * st.D + d) : 0.f;
   const float* xsrc = st.payload + (size_t)slab * kSlot * Dp;
   for (int i = threadIdx.x; i < kSlot * (Dp >> 2); i += blockDim.x) {
     const int n = i & 31, c4 = i >> 5;
@@ -925,12 +930,12 @@ __global__ void __launch_bounds__(256) k_seed_list(DevState st, const float* __r
     xs[n][4 * c4] = v.x, xs[n][4 * c4 + 1] = v.y, xs[n][4 * c4 + 2] = v.z, xs[n][4 * c4 + 3] = v.w;
   }
   __syncthreads();
-  const int n0 = min(s_n0, 256);
   const uint32_t bm = s_bm;
   const float infl = 1.f + (float)(Dp + 2) * 0x1p-23f;
   for (int t = w; t < n0; t += 8) {
     const int q = q0[t];
-    for (int d = lane; d < Dp; d += 32) qs[w][d] = d < st.D ? __ldg(Q + (int64_t)q * st.D + d) : 0.f;
+    if (t != w)  // (the first one is already staged)
+      for (int d = lane; d < Dp; d += 32) qs[w][d] = d < st.D ? __ldg(Q + (int64_t)q * st.D + d) : 0.f;
     __syncwarp();
     // four independent partial sums (any order: the inflation below covers the
     // reordering against the scan's sequential sum, (Dp+2) 2^-23 relative)

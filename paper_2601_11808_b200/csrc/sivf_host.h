@@ -114,7 +114,7 @@ struct Index {
   int rank_split = 1;         // nearest-probes-first work order (SIVF_OPT_RANK_SPLIT; > 1: r0)
   int dbg = 0;                // experiment switches (SIVF_OPT_DEBUG)
   int tc_max_stages = 0;      // experiments: cap on the tensor-core scan's stage ring (option 98; 0 = as many as fit)
-  int seed_list = 1;          // per-list seed of the k-th distance bounds before the tensor-core scan (SIVF_OPT_SEED_LIST)
+  int seed_list = 0;          // per-list seed of the k-th distance bounds before the tensor-core scan (SIVF_OPT_SEED_LIST; off: measured neutral)
   int seed_slabs = 0;         // k-th distance seeding before the tensor-core scan (SIVF_OPT_SEED_SLABS; off: it costs more than it saves)
   int64_t launches = 0;
   alignas(64) unsigned char coarse_tmap[128] = {};  // TMA store descriptor of sc.coarse (k_coarse_tc.cu)
