@@ -312,7 +312,8 @@ def run_sivf(args):
     G = ws
     stream = torch.cuda.current_stream()
     W, Kst = args.warmup, args.steps
-    n_steps_total = W + 3 * Kst + 2  # direct (profiled) + CUDA-graph + e2e passes
+    E2W = 4  # untimed e2e warm-up steps: the API caches its step graphs for both staging sets
+    n_steps_total = W + 3 * Kst + 2 + E2W  # direct (profiled) + CUDA-graph + e2e warm-up + e2e passes
     gen = Generator(sift_shape(seed=SEED))
 
     # ---------------- setup (untimed): quantizer, index, 1M build
@@ -455,10 +456,10 @@ def run_sivf(args):
     # are copied back (D2H) while step t+1 computes: two staging sets, events between
     # the streams.  The timed region spans the first H2D to the last D2H.
     host_inputs = []
-    for t in range(n_dev_steps, n_dev_steps + Kst):  # steps after the graph pass
+    for t in range(n_dev_steps, n_dev_steps + E2W + Kst):  # steps after the graph pass
         host_inputs.append(tuple(torch.from_numpy(a).pin_memory() for a in step_host(t)))
-    h_d = [torch.empty(NQ, K, dtype=torch.float32).pin_memory() for _ in range(Kst)]
-    h_i = [torch.empty(NQ, K, dtype=torch.int64).pin_memory() for _ in range(Kst)]
+    h_d = [torch.empty(NQ, K, dtype=torch.float32).pin_memory() for _ in range(E2W + Kst)]
+    h_i = [torch.empty(NQ, K, dtype=torch.int64).pin_memory() for _ in range(E2W + Kst)]
     stage = [[torch.empty_like(x, device=dev) for x in host_inputs[0]] for _ in range(2)]
     res_d = [torch.empty(NQ, K, dtype=torch.float32, device=dev) for _ in range(2)]
     res_i = [torch.empty(NQ, K, dtype=torch.int64, device=dev) for _ in range(2)]
@@ -470,43 +471,52 @@ def run_sivf(args):
     ev_done = [torch.cuda.Event() for _ in range(2)]
     ev_out = [torch.cuda.Event() for _ in range(2)]
 
-    def h2d_copy(t):
+    def h2d_copy(t, u):  # step u's inputs into staging set t % 2
         b = t % 2
         with torch.cuda.stream(cs):
             if t >= 2:
                 cs.wait_event(ev_done[b])  # step t-2 no longer reads this staging set
-            for dst, src in zip(stage[b], host_inputs[t]):
+            for dst, src in zip(stage[b], host_inputs[u]):
                 if dst.shape != src.shape:
                     dst.resize_(src.shape)
                 dst.copy_(src, non_blocking=True)
             ev_in[b].record(cs)
 
+    def e2e_pass(u0, n, e0=None):  # host steps u0 .. u0+n-1; the first H2D after e0
+        if e0 is not None:
+            e0.record(main)
+            cs.wait_event(e0)
+        else:
+            cs.wait_stream(main)
+        h2d_copy(0, u0)
+        for t in range(n):
+            b = t % 2
+            if t + 1 < n:
+                h2d_copy(t + 1, u0 + t + 1)
+            main.wait_event(ev_in[b])
+            if t >= 2:
+                main.wait_event(ev_out[b])  # results of step t-2 copied out of this buffer set
+            if G == 1:  # results straight into this step's output buffers
+                one_step(tuple(stage[b]), res_d[b], res_i[b])
+            else:
+                dd, ii = one_step(tuple(stage[b]))
+                res_d[b].copy_(dd, non_blocking=True)
+                res_i[b].copy_(ii, non_blocking=True)
+            ev_done[b].record(main)
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev_done[b])
+                h_d[u0 + t].copy_(res_d[b], non_blocking=True)
+                h_i[u0 + t].copy_(res_i[b], non_blocking=True)
+                ev_out[b].record(cs)
+        main.wait_stream(cs)
+
+    # untimed warm-up: the library captures each staging set's step signature as a CUDA
+    # graph on its second sighting (steady state of a streaming client)
+    e2e_pass(0, E2W)
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(main)
-    cs.wait_event(e0)
-    h2d_copy(0)
-    for t in range(Kst):
-        b = t % 2
-        if t + 1 < Kst:
-            h2d_copy(t + 1)
-        main.wait_event(ev_in[b])
-        if t >= 2:
-            main.wait_event(ev_out[b])  # results of step t-2 copied out of this buffer set
-        if G == 1:  # results straight into this step's output buffers
-            one_step(tuple(stage[b]), res_d[b], res_i[b])
-        else:
-            dd, ii = one_step(tuple(stage[b]))
-            res_d[b].copy_(dd, non_blocking=True)
-            res_i[b].copy_(ii, non_blocking=True)
-        ev_done[b].record(main)
-        with torch.cuda.stream(cs):
-            cs.wait_event(ev_done[b])
-            h_d[t].copy_(res_d[b], non_blocking=True)
-            h_i[t].copy_(res_i[b], non_blocking=True)
-            ev_out[b].record(cs)
-    main.wait_stream(cs)
+    e2e_pass(E2W, Kst, e0)
     e1.record(main)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
@@ -523,7 +533,7 @@ def run_sivf(args):
     qps_at_09 = None
     recall_point = None
     if not args.no_sweep and G == 1:
-        lo = N_BASE + (n_dev_steps + Kst) * BATCH - N_BASE  # live window [lo, lo + N_BASE)
+        lo = N_BASE + (n_dev_steps + E2W + Kst) * BATCH - N_BASE  # live window [lo, lo + N_BASE)
         live_ids = np.arange(lo, lo + N_BASE)
         assert s2["live"] == N_BASE
         Xl = torch.from_numpy(gen.range(lo, N_BASE)).to(dev)
@@ -686,7 +696,9 @@ def run_sivf(args):
         "cpu_baseline": cpu,
         "e2e": {"value": 1e3 / e2e_ms, "unit": "steps/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                 "method": "sivf_sliding_window_step from pinned host buffers; H2D of step t+1 and D2H of step t "
-                          "on a copy stream overlap step t (two staging sets)",
+                          "on a copy stream overlap step t (two staging sets); timed after 4 untimed steps of the "
+                          "same loop (the API has then cached its step graph for both staging sets); the first "
+                          "H2D and the last D2H are inside the timed region",
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clk_s,
