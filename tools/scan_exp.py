@@ -24,7 +24,7 @@ for b in range(0, N, 65536):
 del X
 Q = torch.from_numpy(gen.queries(0, NQ)).cuda()
 configs = os.environ.get("CONFIGS", "0,1,3,35,39,43,47,63,64,16").split(",")
-ix.set_option(9, int(os.environ.get("SEEDLIST", "1")))  # SIVF_OPT_SEED_LIST
+ix.set_option(9, int(os.environ.get("SEEDLIST", "0")))  # SIVF_OPT_SEED_LIST (library default 0)
 splits = [int(v) for v in os.environ.get("SPLITS", "1").split(",")]
 stages = [int(v) for v in os.environ.get("STAGES", "0").split(",")]
 seeds = [int(v) for v in os.environ.get("SEEDS", "0").split(",")]
