@@ -149,6 +149,32 @@ def test_search_graph_cache_replay():
     assert len(set(launches)) == 1 and launches[0] > 0
 
 
+# ------------------------------------------------------------------ sivf_probe / sivf_search_probed
+def test_probe_and_probed_search_edges():
+    # host-detectable argument errors enqueue nothing; empty batches are no-ops; probe
+    # sets in any order give the same result (the order only steers the work)
+    gen = Generator(sift_shape(seed=0x7E57))
+    X = gen.range(0, 8000)
+    C = O.kmeans(X[:4000], 32, 5, 3)
+    g, o = make_pair(128, 32, 8000, C, max_batch=8000, max_queries=64, max_nprobe=16)
+    ins(g, o, np.arange(8000), X)
+    Q = T(gen.queries(0, 64))
+    with pytest.raises(S.SivfError):
+        g.probe(Q, 17)  # nprobe > max_nprobe
+    with pytest.raises(S.SivfError):
+        g.probe(T(gen.queries(0, 65)), 8)  # nq > max_queries
+    assert g.probe(Q[:0], 8).shape == (0, 8)
+    p = g.probe(Q, 8)
+    d0, i0 = g.search(Q, 10, 8)
+    d1, i1 = g.search_probed(Q, p, 10)
+    d2, i2 = g.search_probed(Q, p.flip(1).contiguous(), 10)  # reversed probe order
+    assert torch.equal(i0, i1) and torch.equal(d0, d1) and torch.equal(i0, i2) and torch.equal(d0, d2)
+    with pytest.raises(S.SivfError):
+        g.search_probed(Q, p, 0)  # k = 0
+    d3, i3 = g.search_probed(Q[:0], p[:0], 10)
+    assert d3.shape == (0, 10)
+
+
 # ------------------------------------------------------------------ per-list seed of the bounds
 @pytest.mark.parametrize("kind", ["sift", "float"])
 def test_seed_list_changes_nothing(kind):
