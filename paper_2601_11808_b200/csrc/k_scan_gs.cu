@@ -46,12 +46,13 @@ namespace {
 
 constexpr int GQ = 128;          // queries per work item (UMMA M)
 constexpr int GG = 8;            // slabs per group (UMMA N = 256: each streamed A chunk serves 8 slabs)
-constexpr int NSTG = 2;          // stage ring depth
+constexpr int NSTG = 4;          // stage ring depth
 constexpr int NBG = 2;           // TMEM accumulators (GN = 256 columns each)
 constexpr int GN = GG * 32;      // columns per group
 constexpr int NGM = 4;           // group metadata ring
-constexpr int ACH = 32768;       // A chunk bytes: 128 rows x 64 dims x 2 B x (hi, lo)
-constexpr int STG = ACH + GG * 4 * 2048;  // stage: A chunk + B chunk (8 slabs x 4 row groups x 2 KB)
+constexpr int ACH = GQ * kGsKch * 4;  // A chunk bytes: 128 rows x 32 dims x 2 B x (hi, lo)
+constexpr int BPS = kGsKch * 128;       // B chunk bytes per slab: 4 row groups x [hi | lo] pieces
+constexpr int STG = ACH + GG * BPS;  // stage: A chunk + B chunk (8 slabs x 4 row groups x 1 KB)
 constexpr int GS_THREADS = 6 * 32;
 
 struct GsMeta {
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(GQ) k_gs_prep(GsArgs a, uint16_t* __restrict__
                                                 float* __restrict__ gs_qs) {
   const DevState& st = a.st;
   const int ntiles = st.sctr[I_NTILES];
-  const int row = threadIdx.x, Dg = st.Dg, nch = Dg >> 6;
+  const int row = threadIdx.x, Dg = st.Dg, nch = Dg / kGsKch;
   for (int w = blockIdx.x; w < ntiles; w += gridDim.x) {
     if (a.doff[w] < 0 || row >= a.work_n[w]) continue;
     const int q = a.inv_pairs[a.work_p0[w] + row] / a.nprobe;
@@ -174,7 +175,8 @@ __global__ void __launch_bounds__(GQ) k_gs_prep(GsArgs a, uint16_t* __restrict__
         hw[e2] = *reinterpret_cast<const uint32_t*>(&hh);
         lw[e2] = *reinterpret_cast<const uint32_t*>(&ll);
       }
-      unsigned char* p = A + (size_t)(c8 >> 3) * ACH + (row >> 3) * 1024 + (c8 & 7) * 128 + (row & 7) * 16;
+      constexpr int KC8 = kGsKch / 8;  // K-cores per chunk
+      unsigned char* p = A + (size_t)(c8 / KC8) * ACH + (row >> 3) * (KC8 * 128) + (c8 % KC8) * 128 + (row & 7) * 16;
       *reinterpret_cast<uint4*>(p) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
       *reinterpret_cast<uint4*>(p + ACH / 2) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) k_scan_gs(GsArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const DevState& st = a.st;
-  const int conc = st.conc, nch = st.Dg >> 6;
+  const int conc = st.conc, nch = st.Dg / kGsKch;
   GsMeta* gm = reinterpret_cast<GsMeta*>(smem + (size_t)NSTG * STG);
   uint2* pring = reinterpret_cast<uint2*>(gm + NGM);  // [128] live (slab, bitmap) records
   uint64_t* full = reinterpret_cast<uint64_t*>(pring + 128);  // [NSTG] producer -> MMA (tx bytes)
@@ -265,15 +267,15 @@ __global__ void __launch_bounds__(GS_THREADS, 1) k_scan_gs(GsArgs a) {
           __syncwarp();
           unsigned char* sb = smem + (size_t)stg * STG;
           if (lane == 0) {
-            mbar_arrive_expect_tx(&full[stg], (uint32_t)ACH + (uint32_t)nv * 8192u);
+            mbar_arrive_expect_tx(&full[stg], (uint32_t)ACH + (uint32_t)nv * (uint32_t)BPS);
             bulk_g2s(sb, reinterpret_cast<const unsigned char*>(a.gs_a) + ((size_t)w * nch + c) * ACH, ACH, &full[stg]);
           }
           __syncwarp();
-          if (lane < nv)  // slab `lane`'s chunk c: its 4 row-group pieces, one 8-KB copy (chunk-major record)
-            bulk_g2s(sb + ACH + lane * 8192,
+          if (lane < nv)  // slab `lane`'s chunk c: its 4 row-group pieces, one copy (chunk-major record)
+            bulk_g2s(sb + ACH + lane * BPS,
                      reinterpret_cast<const unsigned char*>(st.payload_g) + (size_t)sr * recg_bytes(st.Dg) +
-                         (size_t)c * 8192,
-                     8192, &full[stg]);
+                         (size_t)c * BPS,
+                     BPS, &full[stg]);
         }
         ++gseq;
       };
@@ -330,9 +332,11 @@ __global__ void __launch_bounds__(GS_THREADS, 1) k_scan_gs(GsArgs a) {
         if (lane == 0) {
           const uint32_t A = smem_u32(smem + (size_t)stg * STG), B = A + ACH;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ah = umma_sdesc(A + 256u * kk, 128u, 1024u), al = umma_sdesc(A + ACH / 2 + 256u * kk, 128u, 1024u);
-            const uint64_t bh = umma_sdesc(B + 256u * kk, 128u, 2048u), bl = umma_sdesc(B + 1024u + 256u * kk, 128u, 2048u);
+          for (int kk = 0; kk < kGsKch / 16; ++kk) {
+            const uint64_t ah = umma_sdesc(A + 256u * kk, 128u, kGsKch * 16u),
+                           al = umma_sdesc(A + ACH / 2 + 256u * kk, 128u, kGsKch * 16u);
+            const uint64_t bh = umma_sdesc(B + 256u * kk, 128u, kGsKch * 32u),
+                           bl = umma_sdesc(B + kGsKch * 16u + 256u * kk, 128u, kGsKch * 32u);
             umma_f16_ss(dt, ah, bh, idesc, (c | kk) != 0 ? 1u : 0u);
             umma_f16_ss(dt, ah, bl, idesc, 1u);
             umma_f16_ss(dt, al, bh, idesc, 1u);

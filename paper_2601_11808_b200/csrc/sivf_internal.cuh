@@ -38,15 +38,17 @@ __host__ __device__ __forceinline__ size_t rec16_norm_off(int Dh, int n) {
 __host__ __device__ __forceinline__ size_t rec16_id_off(int Dh, int n) { return rec16_norm_off(Dh, n) + 32; }
 // The split-fp16 scan copy of a slab for D > 128 (k_scan_gs.cu; Dg = D rounded
 // up to 64): x * 2^e_x (e_x per vector, slab_xs = 2^-e_x) = hi + lo, hi =
-// fp16_rn(x 2^e), lo = fp16_rn(x 2^e - hi).  Per slab Dg/64 dim chunks x 4 row
-// groups (chunk-major: one 8-KB bulk copy per slab and chunk), each piece
-// [hi: 8 K-cores x 8 slots x 8 halves = 1 KB][lo: 1 KB]: one 2-KB piece per
+// fp16_rn(x 2^e), lo = fp16_rn(x 2^e - hi).  Per slab Dg/32 dim chunks x 4 row
+// groups (chunk-major: one 4-KB bulk copy per slab and chunk), each piece
+// [hi: 4 K-cores x 8 slots x 8 halves = 512 B][lo: 512 B]: one 1-KB piece per
 // (chunk, row group) holds both halves of an UMMA B operand slice (K-major
-// SWIZZLE_NONE, LBO = 128 B, SBO = 2 KB in the stage).
+// SWIZZLE_NONE, LBO = 128 B, SBO = 1 KB in the stage).
+constexpr int kGsKch = 32;  // dims per chunk of the split copy and of the GEMM scan's K loop
 __host__ __device__ __forceinline__ size_t recg_bytes(int Dg) { return (size_t)128 * Dg; }
 // byte offset of (slot n, dim d, part: 0 hi / 1 lo) inside a slab's copy
 __host__ __device__ __forceinline__ size_t recg_off(int Dg, int n, int d, int part) {
-  return ((size_t)(d >> 6) * 4 + (n >> 3)) * 2048 + part * 1024 + ((d >> 3) & 7) * 128 + (n & 7) * 16 + (d & 7) * 2;
+  return ((size_t)(d / kGsKch) * 4 + (n >> 3)) * (kGsKch * 32) + part * (kGsKch * 16) + ((d >> 3) % (kGsKch / 8)) * 128 +
+         (n & 7) * 16 + (d & 7) * 2;
 }
 // slab_flag bits
 constexpr uint32_t kFlagIntegral = 1u;  // every value an integer with |v| <= 2048 (exact in tf32 and fp16)
