@@ -134,51 +134,77 @@ __global__ void __launch_bounds__(1024) k_gs_offsets(DevState st, const int32_t*
   }
 }
 
+// Split-fp16 copy of each query, once per query (its work items gather it below):
+// x 2^e = hi + lo (e from the row's largest |v|, as k_append does for the slabs),
+// ||q||^2 and 2^-e_q.  Warp per query.
+__global__ void __launch_bounds__(256) k_gs_qsplit(DevState st, const float* __restrict__ Q, int64_t nq,
+                                                   uint16_t* __restrict__ qh, uint16_t* __restrict__ ql,
+                                                   float* __restrict__ qqn, float* __restrict__ qqs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (q >= nq) return;  // warp-uniform
+  const float* qr = Q + q * st.D;
+  const int Dg = st.Dg;
+  float mx = 0.f, nrm = 0.f;
+  for (int d = lane; d < st.D; d += 32) {
+    const float v = __ldg(qr + d);
+    mx = fmaxf(mx, fabsf(v));
+    nrm = fmaf(v, v, nrm);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    nrm += __shfl_xor_sync(kFull, nrm, o);
+  }
+  int e = 0;
+  if (mx > 0.f && mx <= 3.4e38f) {
+    int ex;
+    frexpf(mx, &ex);
+    e = 15 - ex;
+    e = e < -120 ? -120 : e > 120 ? 120 : e;
+  }
+  if (lane == 0) {
+    qqn[q] = nrm;
+    qqs[q] = ldexpf(1.f, -e);
+  }
+  for (int d = 2 * lane; d < Dg; d += 64) {
+    const float s0 = ldexpf(d < st.D ? __ldg(qr + d) : 0.f, e), s1 = ldexpf(d + 1 < st.D ? __ldg(qr + d + 1) : 0.f, e);
+    const __half h0 = __float2half_rn(s0), h1 = __float2half_rn(s1);
+    const __half l0 = __float2half_rn(s0 - __half2float(h0)), l1 = __float2half_rn(s1 - __half2float(h1));
+    *reinterpret_cast<__half2*>(qh + q * Dg + d) = __halves2half2(h0, h1);
+    *reinterpret_cast<__half2*>(ql + q * Dg + d) = __halves2half2(l0, l1);
+  }
+}
+
 // Split-fp16 query tile of each dense work item: A[item][chunk] = [hi: 16 row
-// groups x 8 K-cores x 8 rows x 8 halves][lo: same] (K-major SWIZZLE_NONE,
-// LBO = 128 B, SBO = 1 KB), ||q||^2 and 2^-e_q per row.  Rows >= nqt are not
-// written (their accumulator rows are never read).
+// groups x K-cores x 8 rows x 8 halves][lo: same] (K-major SWIZZLE_NONE,
+// LBO = 128 B, SBO = K-cores x 128 B), gathered from the per-query split copies
+// (16-B K-cores), and ||q||^2, 2^-e_q per row.  Rows >= nqt are not written (their
+// accumulator rows are never read).  Thread = row: the warp's stores of one K-core
+// are 4 contiguous 128-B core matrices.
 __global__ void __launch_bounds__(GQ) k_gs_prep(GsArgs a, uint16_t* __restrict__ gs_a, float* __restrict__ gs_qn,
-                                                float* __restrict__ gs_qs) {
+                                                float* __restrict__ gs_qs, const uint16_t* __restrict__ qh,
+                                                const uint16_t* __restrict__ ql, const float* __restrict__ qqn,
+                                                const float* __restrict__ qqs) {
   const DevState& st = a.st;
   const int ntiles = st.sctr[I_NTILES];
   const int row = threadIdx.x, Dg = st.Dg, nch = Dg / kGsKch;
+  constexpr int KC8 = kGsKch / 8;  // K-cores per chunk
   for (int w = blockIdx.x; w < ntiles; w += gridDim.x) {
     if (a.doff[w] < 0 || row >= a.work_n[w]) continue;
     const int q = a.inv_pairs[a.work_p0[w] + row] / a.nprobe;
-    const float* qr = a.Q + (int64_t)q * st.D;
-    float mx = 0.f, nrm = 0.f;
-    for (int d = 0; d < st.D; ++d) {
-      const float v = __ldg(qr + d);
-      mx = fmaxf(mx, fabsf(v));
-      nrm = fmaf(v, v, nrm);
-    }
-    int e = 0;
-    if (mx > 0.f && mx <= 3.4e38f) {
-      int ex;
-      frexpf(mx, &ex);
-      e = 15 - ex;
-      e = e < -120 ? -120 : e > 120 ? 120 : e;
-    }
-    gs_qn[(size_t)w * GQ + row] = nrm;
-    gs_qs[(size_t)w * GQ + row] = ldexpf(1.f, -e);
-    unsigned char* A = reinterpret_cast<unsigned char*>(gs_a) + (size_t)w * nch * ACH;
+    gs_qn[(size_t)w * GQ + row] = qqn[q];
+    gs_qs[(size_t)w * GQ + row] = qqs[q];
+    const uint4* sh = reinterpret_cast<const uint4*>(qh + (size_t)q * Dg);
+    const uint4* sl = reinterpret_cast<const uint4*>(ql + (size_t)q * Dg);
+    unsigned char* A = reinterpret_cast<unsigned char*>(gs_a) + (size_t)w * nch * ACH + (row >> 3) * (KC8 * 128) +
+                       (row & 7) * 16;
+#pragma unroll 4
     for (int c8 = 0; c8 < (Dg >> 3); ++c8) {
-      uint32_t hw[4], lw[4];
-#pragma unroll
-      for (int e2 = 0; e2 < 4; ++e2) {
-        const int d = 8 * c8 + 2 * e2;
-        const float s0 = ldexpf(d < st.D ? __ldg(qr + d) : 0.f, e), s1 = ldexpf(d + 1 < st.D ? __ldg(qr + d + 1) : 0.f, e);
-        const __half h0 = __float2half_rn(s0), h1 = __float2half_rn(s1);
-        const __half l0 = __float2half_rn(s0 - __half2float(h0)), l1 = __float2half_rn(s1 - __half2float(h1));
-        const __half2 hh = __halves2half2(h0, h1), ll = __halves2half2(l0, l1);
-        hw[e2] = *reinterpret_cast<const uint32_t*>(&hh);
-        lw[e2] = *reinterpret_cast<const uint32_t*>(&ll);
-      }
-      constexpr int KC8 = kGsKch / 8;  // K-cores per chunk
-      unsigned char* p = A + (size_t)(c8 / KC8) * ACH + (row >> 3) * (KC8 * 128) + (c8 % KC8) * 128 + (row & 7) * 16;
-      *reinterpret_cast<uint4*>(p) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-      *reinterpret_cast<uint4*>(p + ACH / 2) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      const uint4 hv = __ldg(sh + c8), lv = __ldg(sl + c8);
+      unsigned char* p = A + (size_t)(c8 / KC8) * ACH + (c8 % KC8) * 128;
+      *reinterpret_cast<uint4*>(p) = hv;
+      *reinterpret_cast<uint4*>(p + ACH / 2) = lv;
     }
   }
 }
@@ -593,15 +619,17 @@ cudaError_t setup_scan_gs(Index& ix) {
 // After the search front (work items of <= 128 queries, nb = 1): offsets,
 // query tiles, the GEMM scan, the fallback items; then (merge phase) the
 // per-query selection straight into (dist, ids).
-cudaError_t launch_scan_gs(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s) {
+cudaError_t launch_scan_gs(Index& ix, const float* d_q, int64_t nq, int k, int nprobe, cudaStream_t s) {
   Scratch& sc = ix.sc;
   GsArgs a{ix.st,      d_q,       nprobe,    k,         sc.inv_pairs, sc.work_l, sc.work_p0, sc.work_n,
            sc.gs_a,    sc.gs_qn,  sc.gs_qs,  sc.item_doff, sc.item_dlen, sc.item_nlive, sc.dense};
   k_gs_offsets<<<1, 1024, 0, s>>>(ix.st, sc.work_l, sc.work_n, sc.dense_cap, sc.item_doff, sc.item_dlen);
-  k_gs_prep<<<4 * ix.num_sms, GQ, 0, s>>>(a, sc.gs_a, sc.gs_qn, sc.gs_qs);
+  k_gs_qsplit<<<(unsigned)ceil_div(nq * 32, (int64_t)256), 256, 0, s>>>(ix.st, d_q, nq, sc.gs_qh, sc.gs_ql, sc.gs_qqn,
+                                                                       sc.gs_qqs);
+  k_gs_prep<<<4 * ix.num_sms, GQ, 0, s>>>(a, sc.gs_a, sc.gs_qn, sc.gs_qs, sc.gs_qh, sc.gs_ql, sc.gs_qqn, sc.gs_qqs);
   k_scan_gs<<<ix.num_sms, GS_THREADS, kGsSmem, s>>>(a);
   k_gs_fallback<<<2 * ix.num_sms, 256, 0, s>>>(a, sc.partial);
-  ix.launches += 4;
+  ix.launches += 5;
   return cudaGetLastError();
 }
 

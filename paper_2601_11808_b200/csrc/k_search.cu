@@ -491,7 +491,7 @@ cudaError_t launch_scan_tc(Index& ix, const float* d_q, int k, int nprobe, cudaS
 int scan_tc_tile();
 bool scan_gs_supported(const Index& ix);
 cudaError_t setup_scan_gs(Index& ix);
-cudaError_t launch_scan_gs(Index& ix, const float* d_q, int k, int nprobe, cudaStream_t s);
+cudaError_t launch_scan_gs(Index& ix, const float* d_q, int64_t nq, int k, int nprobe, cudaStream_t s);
 cudaError_t launch_select_gs(Index& ix, const float* d_q, int64_t nq, int k, int nprobe, float* d_dist,
                              int64_t* d_ids, cudaStream_t s);
 
@@ -599,7 +599,7 @@ cudaError_t launch_search_back(Index& ix, const SearchPlan& p, const float* d_q,
   {
     PhaseTimer pt(ix, SIVF_PH_SCAN, s);
     if (p.gs) {
-      e = launch_scan_gs(ix, d_q, k, nprobe, s);
+      e = launch_scan_gs(ix, d_q, nq, k, nprobe, s);
     } else if (p.tc) {
       e = launch_seed_bound(ix, d_q, nq, k, nprobe, s);  // after the front reset gthr to +inf
       if (e == cudaSuccess && p.nb == 2 && ix.tc_two_phase) {

@@ -25,7 +25,7 @@ struct Layout {
   int64_t q_rows;
   size_t x_tiles, x_norm, c_tiles, c_norm, c_csa, c_cnb, cand, cand_ubv, cand_cnt;
   int64_t tc_rows, cap_assign, cap_probe;
-  size_t gs_a, gs_qn, gs_qs, item_doff, item_dlen, item_nlive, item_of, pair_pos, dense;
+  size_t gs_a, gs_qn, gs_qs, gs_qh, gs_ql, gs_qqn, gs_qqs, item_doff, item_dlen, item_nlive, item_of, pair_pos, dense;
   int64_t gs_items, dense_cap;
   int64_t Dp, Dh, Dg, cap_local, dir_half, max_rows, max_chunks, coarse_rows, max_work;
 };
@@ -168,6 +168,13 @@ Layout make_layout(const sivf_config* c, bool view = false) {
   L.gs_a = take(L, (size_t)L.gs_items * L.Dg * 512);
   L.gs_qn = take(L, (size_t)L.gs_items * 128 * 4);
   L.gs_qs = take(L, (size_t)L.gs_items * 128 * 4);
+  {
+    const size_t mq = (size_t)(c->max_queries > 0 ? c->max_queries : 1);
+    L.gs_qh = take(L, L.Dg ? mq * L.Dg * 2 : 0);
+    L.gs_ql = take(L, L.Dg ? mq * L.Dg * 2 : 0);
+    L.gs_qqn = take(L, L.Dg ? mq * 4 : 0);
+    L.gs_qqs = take(L, L.Dg ? mq * 4 : 0);
+  }
   L.item_doff = take(L, L.Dg ? (size_t)(L.max_work + 1) * 8 : 0);
   L.item_dlen = take(L, L.Dg ? (size_t)L.max_work * 4 : 0);
   L.item_nlive = take(L, L.Dg ? (size_t)L.max_work * 4 : 0);
@@ -268,6 +275,10 @@ void carve_scratch(Scratch& sc, void* d_arena, const Layout& L) {
   sc.gs_a = at<uint16_t>(d_arena, L.gs_a);
   sc.gs_qn = at<float>(d_arena, L.gs_qn);
   sc.gs_qs = at<float>(d_arena, L.gs_qs);
+  sc.gs_qh = at<uint16_t>(d_arena, L.gs_qh);
+  sc.gs_ql = at<uint16_t>(d_arena, L.gs_ql);
+  sc.gs_qqn = at<float>(d_arena, L.gs_qqn);
+  sc.gs_qqs = at<float>(d_arena, L.gs_qqs);
   sc.item_doff = at<int64_t>(d_arena, L.item_doff);
   sc.item_dlen = at<int32_t>(d_arena, L.item_dlen);
   sc.item_nlive = at<int32_t>(d_arena, L.item_nlive);

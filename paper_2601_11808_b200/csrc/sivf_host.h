@@ -59,6 +59,10 @@ struct Scratch {
   uint16_t* gs_a = nullptr;         // [gs_items][Dg/64][hi 16 KB | lo 16 KB] split-fp16 query tiles
   float* gs_qn = nullptr;           // [gs_items][128] ||q||^2
   float* gs_qs = nullptr;           // [gs_items][128] 2^-e_q
+  uint16_t* gs_qh = nullptr;        // [max_queries][Dg] split-fp16 hi half of each query (k_gs_qsplit)
+  uint16_t* gs_ql = nullptr;        // [max_queries][Dg] lo half
+  float* gs_qqn = nullptr;          // [max_queries] ||q||^2
+  float* gs_qqs = nullptr;          // [max_queries] 2^-e_q
   int64_t* item_doff = nullptr;     // [max_work + 1] item's region in dense (-1: SIMT fallback)
   int32_t* item_dlen = nullptr;     // [max_work] directory length at planning (row stride = 32 dlen)
   int32_t* item_nlive = nullptr;    // [max_work] live slabs scanned
