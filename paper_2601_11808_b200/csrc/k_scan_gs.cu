@@ -583,12 +583,27 @@ __global__ void __launch_bounds__(128) k_gs_select(GsArgs a, const int32_t* __re
     const int dl = __shfl_sync(kFull, m_dl, src), nl = __shfl_sync(kFull, m_nl, src);
     const int32_t* hdr = reinterpret_cast<const int32_t*>(a.dense + doff);
     const float* rowp = a.dense + doff + gs_hdr(dl) + (int64_t)(pos - __shfl_sync(kFull, m_p0, src)) * kSlot * dl;
-    for (int j0 = 0; j0 < nl; j0 += 4) {
-      float d4[4];
+    // R = 1: software-pipelined (the next PB slabs' distances are in flight while these
+    // are filtered); R > 1: the registers go to the top-k, one batch at a time
+    constexpr int PB = R == 1 ? 8 : 4;
+    float dn[PB];
+    if (R == 1) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) d4[u] = j0 + u < nl ? __ldcs(rowp + (int64_t)(j0 + u) * kSlot + lane) : INFINITY;
+      for (int u = 0; u < PB; ++u) dn[u] = u < nl ? __ldcs(rowp + (int64_t)u * kSlot + lane) : INFINITY;
+    }
+    for (int j0 = 0; j0 < nl; j0 += PB) {
+      float d4[PB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PB; ++u) {
+        if (R == 1) {
+          d4[u] = dn[u];
+          dn[u] = j0 + PB + u < nl ? __ldcs(rowp + (int64_t)(j0 + PB + u) * kSlot + lane) : INFINITY;
+        } else {
+          d4[u] = j0 + u < nl ? __ldcs(rowp + (int64_t)(j0 + u) * kSlot + lane) : INFINITY;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < PB; ++u) {
         const uint32_t kth_hi = (uint32_t)(kth >> 32);
         const bool pass = d4[u] < INFINITY && __float_as_uint(d4[u]) <= kth_hi;
         if (!__ballot_sync(kFull, pass)) continue;
