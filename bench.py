@@ -37,8 +37,8 @@ N_BASE, DIM, NLIST, BATCH, NQ, K, NPROBE = 1_000_000, 128, 1024, 10_000, 10_000,
 N_TRAIN, N_ITER, SEED = 262_144, 20, 0x51F7
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_scan_tc launch, from the committed ncu
 # --set full capture of this bench step (per launch; compare with roofline.hbm_view).
-SCAN_TRAFFIC_NCU = 520.811264e6 + 27.171584e6
-SCAN_TRAFFIC_SRC = "profiles/r03g_scan_full.txt (ncu --set full, bench.py --steps 1 --warmup 1 --no-sweep --no-cpu --no-extra)"
+SCAN_TRAFFIC_NCU = 518.173952e6 + 26.920192e6
+SCAN_TRAFFIC_SRC = "profiles/r03h_scan_full.txt (ncu --set full, bench.py --steps 1 --warmup 1 --no-sweep --no-cpu --no-extra)"
 WORKLOAD = ("SIFT1M-shaped sliding step: 1M x 128 fp32 live window, nlist=1024; per step insert 10k new + "
             "delete 10k oldest + search 10k queries (k=10, nprobe=32) + reclaim")
 
